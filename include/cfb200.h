@@ -1,0 +1,182 @@
+/*
+ * cfb200.h — C ABI of the B200-native iteration engine for the UV-decomposition
+ * ADMM conic solver (arXiv 2203.05027, reference package `conefree`).
+ *
+ * The reference is pure Python/numpy and has no FFI; each entry point below
+ * replaces one reference function (file:line relative to /root/reference/pkg/src/conefree)
+ * and is bound from Python with ctypes by paper_2203_05027_b200/_lib.py
+ * (see INTEGRATION.md for the binding a maintainer would add to conefree).
+ *
+ * Conventions
+ *   - plain pointers + sizes only; no torch / numpy types cross this boundary.
+ *   - every function returns int: CF_OK (0) or a CF_E* code; cf_last_error()
+ *     returns a thread-local message for the last failure on this thread.
+ *   - fp64 everywhere (the reference computes in float64, model.py:59-61).
+ *   - "canonical order" of nonzeros = column-major (sorted by column, then row),
+ *     exactly the order build_uv produces (uv.py:76); y and gamma vectors of
+ *     SolverState are exchanged in that order.
+ *   - a plan owns all device memory it allocates; one plan is driven from one
+ *     host thread at a time; plans are independent of each other.
+ */
+#ifndef CFB200_H
+#define CFB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CF_ABI_VERSION 1
+
+/* return codes */
+#define CF_OK 0
+#define CF_EINVAL 1          /* bad argument (sizes, nulls, unsupported shape) */
+#define CF_ECUDA 2           /* CUDA runtime failure (message in cf_last_error) */
+#define CF_ENOMEM 3          /* device allocation failed */
+#define CF_EPROBLEM 4        /* validate() found violations: see cf_problem_checks */
+#define CF_ESTATE 5          /* call not valid in the plan's current state */
+
+/* report status, mirrors the strings of solver.py:241,272,323 */
+#define CF_STATUS_RUNNING 0
+#define CF_STATUS_SOLVED 1
+#define CF_STATUS_MAX_ITERS 2
+#define CF_STATUS_DIVERGED 3
+
+/* termination modes, solver.py:58 TERM_MODES */
+#define CF_TERM_OSQP 0
+#define CF_TERM_SCS 1
+#define CF_TERM_TARGET 2
+
+typedef struct cf_plan cf_plan;
+
+/* Solver settings. Replaces SolverConfig (solver.py:61-103). The norm-dependent
+ * bounds are computed by the caller exactly as check_termination does
+ * (solver.py:252-271) so host and device take bit-identical decisions. */
+typedef struct cf_config {
+    double mu;                 /* SolverConfig.mu */
+    int64_t max_iters;         /* SolverConfig.max_iters */
+    int64_t check_every;       /* SolverConfig.check_every */
+    int32_t term_mode;         /* CF_TERM_* */
+    int32_t reserved0;
+    double eps_abs;            /* osqp: eps_abs */
+    double eps_rel;            /* osqp: eps_rel */
+    double b_inf;              /* osqp: _norms(p.b)[0] */
+    double c_inf;              /* osqp: _norms(p.c)[0] */
+    double scs_prim_bound;     /* scs: eps_prim * (1.0 + _norms(p.b)[1]) */
+    double scs_dual_bound;     /* scs: eps_dual * (1.0 + _norms(p.c)[1]) */
+    double eps_gap;            /* scs: eps_gap */
+    double target_prim_res;    /* target mode */
+    double target_gap;         /* target mode */
+} cf_config;
+
+/* One evaluated report. Replaces IterationReport (solver.py:141-158). */
+typedef struct cf_report {
+    int64_t iter;
+    int32_t status;            /* CF_STATUS_* after check_termination */
+    int32_t nonfinite;         /* 1 when any state entry was non-finite (solver.py:208-211) */
+    double prim_res_inf, prim_res_2;
+    double dual_res_inf, dual_res_2;
+    double stat_res_inf, stat_res_2;
+    double ax_inf, atl_inf;
+    double cone_gap;
+    double pobj, dobj, gap;
+} cf_report;
+
+/* Problem-check counters filled by cf_plan_create (model.py:152-217). */
+typedef struct cf_problem_checks {
+    int64_t bad_row;           /* rows outside [0, m)      model.py:155 */
+    int64_t bad_col;           /* cols outside [0, n)      model.py:158 */
+    int64_t nonfinite_val;     /* non-finite values        model.py:161 */
+    int64_t zero_val;          /* exact zero values        model.py:164 */
+    int64_t duplicates;        /* duplicate positions      model.py:167-175 */
+    int64_t nonfinite_b;       /* model.py:198-201 */
+    int64_t nonfinite_c;
+} cf_problem_checks;
+
+/* ---------------------------------------------------------------- basics */
+const char* cf_last_error(void);
+int cf_abi_version(void);
+/* number of visible CUDA devices (0 on a CPU-only host; never an error) */
+int cf_device_count(int* count);
+
+/* ---------------------------------------------------------------- setup
+ * cf_plan_create: validate + build_uv + ConeWorkview.from_spec on the device.
+ * Replaces validate's triplet/vector checks (model.py:152-201), build_uv
+ * (uv.py:64-98) and ConeWorkview.from_spec (cones.py:39-59).
+ *   rows/cols/vals: o triplets in ANY order (model.py:47-49); int64/int64/f64.
+ *   b (m), c (n): f64.  block_sizes (n_blocks, host): the ConeSpec.
+ *   inputs_on_device: 0 = rows/cols/vals/b/c are host pointers (copied with
+ *   cudaMemcpyAsync), 1 = device pointers (read, never written or retained).
+ *   stream: cudaStream_t the plan issues all work on (NULL = the plan creates one).
+ * On CF_EPROBLEM, *checks tells which checks failed and *out is NULL; the
+ * caller produces the reference's messages (solver.py:300-302). */
+int cf_plan_create(int64_t m, int64_t n, int64_t o,
+                   const int64_t* rows, const int64_t* cols, const double* vals,
+                   const double* b, const double* c,
+                   int64_t n_blocks, const int64_t* block_sizes,
+                   int inputs_on_device, void* stream,
+                   cf_problem_checks* checks, cf_plan** out);
+int cf_plan_destroy(cf_plan* plan);
+/* dims and the device tile geometry chosen at setup (for tests/bench). */
+int cf_plan_info(const cf_plan* plan, int64_t* m, int64_t* n, int64_t* o,
+                 int64_t* row_tiles, int64_t* col_tiles, int64_t* big_cones, int32_t* all_unit);
+/* replace b and/or c (device or host per inputs_on_device; NULL = keep). */
+int cf_plan_set_rhs(cf_plan* plan, const double* b, const double* c, int inputs_on_device);
+
+/* ---------------------------------------------------------------- state
+ * cf_plan_set_state: warm start (solver.py:278,309). Host vectors; y, gamma
+ * in canonical order (length o). NULL for all = cold start (SolverState.zeros,
+ * solver.py:118-127). mu is needed for the one-time warm-start correction. */
+int cf_plan_set_state(cf_plan* plan, double mu,
+                      const double* x, const double* y, const double* z,
+                      const double* lam, const double* gamma, const double* delta);
+/* Keep b - r of every iteration so cf_plan_get_state can rebuild y (costs 8m
+ * bytes per iteration; off by default, on for parity probing). */
+int cf_plan_set_export(cf_plan* plan, int keep);
+/* Export the full SolverState (solver.py:106-116) at the current iteration;
+ * any output may be NULL. y/gamma are reconstructed in canonical order. */
+int cf_plan_get_state(cf_plan* plan, double* x, double* y, double* z,
+                      double* lam, double* gamma, double* delta, int64_t* iter);
+
+/* ---------------------------------------------------------------- loop
+ * cf_plan_iterate: n_iters iterations of solver.py:313-317 (x, y, z, duals)
+ * with no report; for parity probing and benchmarking. */
+int cf_plan_iterate(cf_plan* plan, double mu, int64_t n_iters);
+/* compute_report (solver.py:206-242) at the current state; status is
+ * CF_STATUS_RUNNING or CF_STATUS_DIVERGED (no termination test). */
+int cf_plan_report(cf_plan* plan, double mu, cf_report* out);
+/* The whole loop of solve() (solver.py:309-334) from the current state:
+ * reports every check_every iterations and at max_iters, device-side
+ * termination (check_termination, solver.py:245-272) with early exit.
+ * trace: caller buffer of trace_cap reports; *n_reports = entries written
+ * (the last one is the SolveResult.report). x_out (n), lam_out (m): host. */
+int cf_plan_solve(cf_plan* plan, const cf_config* cfg,
+                  double* x_out, double* lam_out,
+                  cf_report* trace, int64_t trace_cap, int64_t* n_reports);
+
+/* ---------------------------------------------------------------- operators
+ * Matrix-free products on device vectors (uv.py:106-131 composed):
+ *   cf_apply_A : y = U(V^T x) = A x     (apply_U . apply_Vt)
+ *   cf_apply_At: x = V(U^T y) = A^T y   (apply_V . apply_Ut)
+ * Sums run sequentially in canonical order, bit-identical to np.bincount. */
+int cf_apply_A(cf_plan* plan, const double* x_dev, double* y_dev);
+int cf_apply_At(cf_plan* plan, const double* y_dev, double* x_dev);
+/* project_product (cones.py:103-110) of a device n-vector onto the plan's cone. */
+int cf_project(cf_plan* plan, const double* w_dev, double* out_dev);
+
+/* ---------------------------------------------------------------- timing
+ * CUDA-event time of the last cf_plan_iterate / cf_plan_solve loop (ms),
+ * kernel launches issued by it, and the event time of row/col passes when
+ * profiling was enabled with cf_plan_set_profiling(plan, 1). */
+int cf_plan_last_timing(const cf_plan* plan, double* loop_ms, int64_t* launches,
+                        double* row_pass_ms, double* col_pass_ms, int64_t* timed_iters);
+int cf_plan_set_profiling(cf_plan* plan, int enable);
+/* Synchronise the plan's stream. */
+int cf_plan_sync(cf_plan* plan);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CFB200_H */

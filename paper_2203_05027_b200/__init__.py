@@ -1,0 +1,42 @@
+"""B200-native iteration engine for the UV-decomposition ADMM conic solver.
+
+Drop-in for the reference package ``conefree`` (arXiv 2203.05027): the same
+``solve(p, cfg=None, init=None) -> SolveResult`` API and problem types, with
+the iteration loop (solver.py:312-327) running as hand-written sm_100a fp64
+kernels in ``libcfb200.so``. Importing the package needs no
+GPU; creating a plan (``solve``) does, and fails loudly without one.
+"""
+
+from .api import (
+    IterationReport,
+    SolveResult,
+    SolverConfig,
+    SolverState,
+    check_termination,
+    solve,
+)
+from .engine import DevicePlan
+from .instances import GeneratedInstance, GenSpec, generate, generate_witnessed, shape_for_nnz
+from .problem import ConeSpec, ProblemInstance, TripletMatrix, ValidationReport, validate
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "ConeSpec",
+    "DevicePlan",
+    "GenSpec",
+    "GeneratedInstance",
+    "IterationReport",
+    "ProblemInstance",
+    "SolveResult",
+    "SolverConfig",
+    "SolverState",
+    "TripletMatrix",
+    "ValidationReport",
+    "check_termination",
+    "generate",
+    "generate_witnessed",
+    "shape_for_nnz",
+    "solve",
+    "validate",
+]

@@ -1,0 +1,228 @@
+"""The drop-in solver API: ``solve(p, cfg=None, init=None) -> SolveResult``.
+
+Same signature, types, semantics and errors as the reference
+``conefree.solver`` (solver.py:61-334):
+
+* ``SolverConfig`` (solver.py:61-103) — same fields, defaults and ValueErrors.
+* ``SolverState`` (:106-138), ``IterationReport`` (:141-158),
+  ``SolveResult`` (:161-165).
+* ``check_termination`` (:245-272) — host restatement; ``solve`` uses it to
+  re-decide every device report and refuses to return if the device and the
+  host disagree (they evaluate the same IEEE expressions on the same numbers).
+* ``solve`` (:275-334) — validate, build, warm start, loop with a report every
+  ``check_every`` iterations and at ``max_iters``, early exit on a terminal
+  status. The loop body runs on the GPU only (libcfb200, sm_100a); there is no
+  CPU path.
+
+The ``p``, ``cfg`` and ``init`` arguments are duck-typed, so the reference's
+own ``ProblemInstance`` / ``SolverConfig`` / ``SolverState`` objects work too.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, replace
+from typing import NamedTuple
+
+import numpy as np
+
+from .engine import DevicePlan, ProblemRejected, config_struct
+from .problem import cone_sizes_array, validate
+
+__all__ = [
+    "SolverConfig",
+    "SolverState",
+    "IterationReport",
+    "SolveResult",
+    "check_termination",
+    "solve",
+    "norms",
+]
+
+TERM_MODES = ("osqp", "scs", "target")
+
+
+@dataclass(frozen=True)
+class SolverConfig:
+    """Penalty, iteration budget and termination test (solver.py:61-103)."""
+
+    mu: float = 1.0
+    max_iters: int = 100_000
+    check_every: int = 25
+    term_mode: str = "scs"
+    eps_abs: float = 1e-4
+    eps_rel: float = 1e-3
+    eps_prim: float = 1e-3
+    eps_dual: float = 1e-3
+    eps_gap: float = 1e-3
+    target_prim_res: float | None = None
+    target_gap: float | None = None
+
+    def __post_init__(self):
+        if not self.mu > 0:
+            raise ValueError("mu must be > 0")
+        if self.max_iters < 1:
+            raise ValueError("max_iters must be >= 1")
+        if self.check_every < 1:
+            raise ValueError("check_every must be >= 1")
+        if self.term_mode not in TERM_MODES:
+            raise ValueError(f"term_mode must be one of {TERM_MODES}")
+        for field in ("eps_abs", "eps_rel", "eps_prim", "eps_dual", "eps_gap"):
+            if getattr(self, field) < 0:
+                raise ValueError(f"{field} must be >= 0")
+        if self.term_mode == "target" and (self.target_prim_res is None or self.target_gap is None):
+            raise ValueError("target mode needs target_prim_res and target_gap")
+
+
+@dataclass
+class SolverState:
+    """Iterates x, y, z and multipliers lam, gamma, delta (solver.py:106-138).
+
+    y and gamma are o-length, in canonical (column-major) nonzero order.
+    """
+
+    x: np.ndarray
+    y: np.ndarray
+    z: np.ndarray
+    lam: np.ndarray
+    gamma: np.ndarray
+    delta: np.ndarray
+    iter: int = 0
+
+    @classmethod
+    def zeros(cls, f) -> "SolverState":
+        """Cold start for anything with m, n, o (e.g. the reference's UVFactors)."""
+        m, n, o = int(f.m), int(f.n), int(f.o)
+        return cls(x=np.zeros(n), y=np.zeros(o), z=np.zeros(n), lam=np.zeros(m), gamma=np.zeros(o),
+                   delta=np.zeros(n))
+
+    def copy(self) -> "SolverState":
+        return SolverState(x=self.x.copy(), y=self.y.copy(), z=self.z.copy(), lam=self.lam.copy(),
+                           gamma=self.gamma.copy(), delta=self.delta.copy(), iter=self.iter)
+
+
+@dataclass(frozen=True)
+class IterationReport:
+    """Residual norms, objectives and status at one evaluated iteration."""
+
+    iter: int
+    prim_res_inf: float
+    prim_res_2: float
+    dual_res_inf: float
+    dual_res_2: float
+    stat_res_inf: float
+    stat_res_2: float
+    ax_inf: float
+    atl_inf: float
+    cone_gap: float
+    pobj: float
+    dobj: float
+    gap: float
+    status: str = "running"
+
+
+class SolveResult(NamedTuple):
+    x: np.ndarray
+    lam: np.ndarray
+    report: IterationReport
+    trace: tuple
+
+
+def norms(v) -> tuple:
+    """(inf-norm, 2-norm) exactly as solver.py:200-203."""
+    v = np.asarray(v, dtype=np.float64)
+    if v.size == 0:
+        return 0.0, 0.0
+    return float(np.max(np.abs(v))), float(math.sqrt(np.dot(v, v)))
+
+
+def _decide(report, cfg, b_norms, c_norms) -> str:
+    """check_termination with the problem norms precomputed (solver.py:245-272)."""
+    if report.status == "diverged":
+        return "diverged"
+    if report.status != "running":
+        return report.status
+    if cfg.term_mode == "osqp":
+        eps_prim = cfg.eps_abs + cfg.eps_rel * max(report.ax_inf, b_norms[0])
+        eps_dual = cfg.eps_abs + cfg.eps_rel * max(report.atl_inf, c_norms[0])
+        ok = report.prim_res_inf < eps_prim and report.stat_res_inf < eps_dual
+    elif cfg.term_mode == "scs":
+        ok = (
+            report.prim_res_2 <= cfg.eps_prim * (1.0 + b_norms[1])
+            and report.stat_res_2 <= cfg.eps_dual * (1.0 + c_norms[1])
+            and abs(report.gap) <= cfg.eps_gap * (1.0 + abs(report.pobj) + abs(report.dobj))
+        )
+    else:
+        ok = report.prim_res_2 < cfg.target_prim_res and abs(report.gap) < cfg.target_gap
+    return "solved" if ok else "running"
+
+
+def check_termination(report, cfg, p) -> str:
+    """Map a report onto solved/running/diverged for the configured mode."""
+    return _decide(report, cfg, norms(p.b), norms(p.c))
+
+
+def _host_shapes_ok(p) -> bool:
+    a = p.A
+    if np.asarray(p.b).size != a.num_rows or np.asarray(p.c).size != a.num_cols:
+        return False
+    sizes = cone_sizes_array(p.cones)
+    return bool(sizes.size == 0 or sizes.min() >= 1) and int(sizes.sum()) == a.num_cols
+
+
+def _raise_invalid(p):
+    rep = validate(p)
+    if rep.ok:  # pragma: no cover - the device and host checks disagree
+        raise RuntimeError("device validation rejected a problem the host validate() accepts")
+    raise ValueError("invalid problem: " + "; ".join(rep.violations[:3]))
+
+
+def _to_report(d: dict) -> IterationReport:
+    return IterationReport(
+        iter=d["iter"], prim_res_inf=d["prim_res_inf"], prim_res_2=d["prim_res_2"],
+        dual_res_inf=d["dual_res_inf"], dual_res_2=d["dual_res_2"], stat_res_inf=d["stat_res_inf"],
+        stat_res_2=d["stat_res_2"], ax_inf=d["ax_inf"], atl_inf=d["atl_inf"], cone_gap=d["cone_gap"],
+        pobj=d["pobj"], dobj=d["dobj"], gap=d["gap"],
+        status="diverged" if d["nonfinite"] else "running",
+    )
+
+
+def build_plan(p, stream: int | None = None) -> DevicePlan:
+    """validate + build_uv on the device; raises ValueError like solver.py:300-307."""
+    if not _host_shapes_ok(p):
+        _raise_invalid(p)
+    try:
+        return DevicePlan.from_problem(p, stream=stream)
+    except ProblemRejected:
+        _raise_invalid(p)
+
+
+def run_plan(plan: DevicePlan, p, cfg, b_norms=None, c_norms=None) -> SolveResult:
+    """Run the solve() loop on an existing plan from its current state."""
+    b_norms = norms(p.b) if b_norms is None else b_norms
+    c_norms = norms(p.c) if c_norms is None else c_norms
+    x, lam, raw = plan.run(config_struct(cfg, b_norms, c_norms))
+    trace = []
+    for d in raw:
+        rep = _to_report(d)
+        status = _decide(rep, cfg, b_norms, c_norms)
+        if status == "running" and rep.iter == cfg.max_iters:
+            status = "max_iters"
+        if status != d["status"]:
+            raise RuntimeError(
+                f"device termination test ({d['status']}) disagrees with check_termination ({status}) "
+                f"at iteration {rep.iter}")
+        trace.append(replace(rep, status=status))
+    return SolveResult(x=x, lam=lam, report=trace[-1], trace=tuple(trace))
+
+
+def solve(p, cfg: SolverConfig | None = None, init: SolverState | None = None) -> SolveResult:
+    """Run the ADMM loop on the GPU until a terminal status (solver.py:275-334)."""
+    cfg = cfg or SolverConfig()
+    plan = build_plan(p)
+    try:
+        if init is not None:
+            plan.set_state(cfg.mu, init, export=False)
+        return run_plan(plan, p, cfg)
+    finally:
+        plan.close()

@@ -1,0 +1,384 @@
+// C ABI of libcfb200 (include/cfb200.h): plan lifetime, warm start / state
+// export, the iteration loop of solve() (solver.py:309-334) with device-side
+// termination, and the matrix-free operators.
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "cf_common.h"
+
+namespace cf {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
+    cudaGetLastError();  // clear sticky-free errors
+    set_error(std::string(what) + " failed: " + cudaGetErrorString(e) + " (" + file + ":" + std::to_string(line) + ")");
+    return e == cudaErrorMemoryAllocation ? CF_ENOMEM : CF_ECUDA;
+}
+
+namespace {
+
+int check_plan(const cf_plan* p, const char* fn) {
+    if (!p) {
+        set_error(std::string(fn) + ": plan is NULL");
+        return CF_EINVAL;
+    }
+    return CF_OK;
+}
+
+int check_mu(double mu, const char* fn) {
+    if (!(mu > 0)) {
+        set_error(std::string(fn) + ": mu must be > 0");
+        return CF_EINVAL;
+    }
+    return CF_OK;
+}
+
+// options of the next iteration: warm-start corrections
+IterOpts next_opts(const cf_plan* p, double mu, bool report) {
+    IterOpts o;
+    o.mu = mu;
+    o.report = report;
+    if (p->since_warm == 0) {
+        o.vterm = p->vterm1.p;
+        o.rcorr = p->rcorr.p;
+    } else if (p->since_warm == 1) {
+        o.ccorr = p->ccorr.p;
+    }
+    return o;
+}
+
+void advance(cf_plan* p, int64_t iters, bool br_written) {
+    p->iter += iters;
+    p->since_warm = (int)std::min<int64_t>(2, p->since_warm + iters);
+    if (iters > 0) p->br_valid = br_written;
+}
+
+}  // namespace
+}  // namespace cf
+
+using namespace cf;
+
+extern "C" {
+
+const char* cf_last_error(void) { return g_last_error.c_str(); }
+
+int cf_abi_version(void) { return CF_ABI_VERSION; }
+
+int cf_device_count(int* count) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        n = 0;
+    }
+    if (count) *count = n;
+    return CF_OK;
+}
+
+int cf_plan_destroy(cf_plan* p) {
+    if (!p) return CF_OK;
+    if (p->stream) cudaStreamSynchronize(p->stream);
+    if (p->host_reports) cudaFreeHost(p->host_reports);
+    if (p->ev0) cudaEventDestroy(p->ev0);
+    if (p->ev1) cudaEventDestroy(p->ev1);
+    for (cudaEvent_t e : p->prof_events) cudaEventDestroy(e);
+    cudaStream_t st = p->own_stream ? p->stream : nullptr;
+    delete p;  // DevBuf destructors free device memory
+    if (st) cudaStreamDestroy(st);
+    return CF_OK;
+}
+
+int cf_plan_info(const cf_plan* p, int64_t* m, int64_t* n, int64_t* o, int64_t* row_tiles, int64_t* col_tiles,
+                 int64_t* big_cones, int32_t* all_unit) {
+    CF_TRY(check_plan(p, "cf_plan_info"));
+    if (m) *m = p->m;
+    if (n) *n = p->n;
+    if (o) *o = p->o;
+    if (row_tiles) *row_tiles = p->row_tiles;
+    if (col_tiles) *col_tiles = p->col_tiles;
+    if (big_cones) *big_cones = p->n_big;
+    if (all_unit) *all_unit = p->all_unit ? 1 : 0;
+    return CF_OK;
+}
+
+int cf_plan_set_rhs(cf_plan* p, const double* b, const double* c, int on_device) {
+    CF_TRY(check_plan(p, "cf_plan_set_rhs"));
+    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (b && p->m) CF_CUDA(cudaMemcpyAsync(p->b.p, b, p->m * 8, kind, p->stream));
+    if (c && p->n) CF_CUDA(cudaMemcpyAsync(p->c.p, c, p->n * 8, kind, p->stream));
+    if (b) CF_TRY(launch_row_diag(p));
+    CF_CUDA(cudaStreamSynchronize(p->stream));
+    return CF_OK;
+}
+
+int cf_plan_set_state(cf_plan* p, double mu, const double* x, const double* y, const double* z, const double* lam,
+                      const double* gamma, const double* delta) {
+    CF_TRY(check_plan(p, "cf_plan_set_state"));
+    CF_TRY(check_mu(mu, "cf_plan_set_state"));
+    const int given = (x != nullptr) + (y != nullptr) + (z != nullptr) + (lam != nullptr) + (gamma != nullptr) +
+                      (delta != nullptr);
+    if (given != 0 && given != 6) {
+        set_error("cf_plan_set_state: give all six vectors (warm start) or none (cold start)");
+        return CF_EINVAL;
+    }
+    cudaStream_t st = p->stream;
+    const int64_t m = p->m, n = p->n, o = p->o;
+    p->br_valid = false;
+    p->iter = 0;
+    p->export_mu = mu;
+    CF_CUDA(cudaMemsetAsync(p->h.p, 0, std::max<int64_t>(m, 1) * 8, st));
+    if (given == 0) {
+        CF_CUDA(cudaMemsetAsync(p->x.p, 0, std::max<int64_t>(n, 1) * 8, st));
+        CF_CUDA(cudaMemsetAsync(p->z.p, 0, std::max<int64_t>(n, 1) * 8, st));
+        CF_CUDA(cudaMemsetAsync(p->delta.p, 0, std::max<int64_t>(n, 1) * 8, st));
+        CF_CUDA(cudaMemsetAsync(p->lam.p, 0, std::max<int64_t>(m, 1) * 8, st));
+        p->since_warm = 2;
+        p->y0.release();
+        p->gamma0.release();
+        CF_CUDA(cudaStreamSynchronize(st));
+        return CF_OK;
+    }
+    if (n) {
+        CF_CUDA(cudaMemcpyAsync(p->x.p, x, n * 8, cudaMemcpyHostToDevice, st));
+        CF_CUDA(cudaMemcpyAsync(p->z.p, z, n * 8, cudaMemcpyHostToDevice, st));
+        CF_CUDA(cudaMemcpyAsync(p->delta.p, delta, n * 8, cudaMemcpyHostToDevice, st));
+    }
+    if (m) CF_CUDA(cudaMemcpyAsync(p->lam.p, lam, m * 8, cudaMemcpyHostToDevice, st));
+    CF_TRY(p->y0.alloc(o));
+    CF_TRY(p->gamma0.alloc(o));
+    CF_TRY(p->eps.alloc(o));
+    CF_TRY(p->vterm1.alloc(n));
+    CF_TRY(p->ccorr.alloc(n));
+    CF_TRY(p->rcorr.alloc(m));
+    if (o) {
+        CF_CUDA(cudaMemcpyAsync(p->y0.p, y, o * 8, cudaMemcpyHostToDevice, st));
+        CF_CUDA(cudaMemcpyAsync(p->gamma0.p, gamma, o * 8, cudaMemcpyHostToDevice, st));
+    }
+    CF_CUDA(cudaMemsetAsync(p->vterm1.p, 0, std::max<int64_t>(n, 1) * 8, st));
+    CF_CUDA(cudaMemsetAsync(p->ccorr.p, 0, std::max<int64_t>(n, 1) * 8, st));
+    CF_CUDA(cudaMemsetAsync(p->rcorr.p, 0, std::max<int64_t>(m, 1) * 8, st));
+    CF_TRY(launch_warm_start(p, mu));
+    p->since_warm = 0;
+    CF_CUDA(cudaStreamSynchronize(st));  // host inputs may be freed after return
+    return CF_OK;
+}
+
+int cf_plan_set_export(cf_plan* p, int keep) {
+    CF_TRY(check_plan(p, "cf_plan_set_export"));
+    p->keep_br = keep != 0;
+    return CF_OK;
+}
+
+int cf_plan_get_state(cf_plan* p, double* x, double* y, double* z, double* lam, double* gamma, double* delta,
+                      int64_t* iter) {
+    CF_TRY(check_plan(p, "cf_plan_get_state"));
+    cudaStream_t st = p->stream;
+    const int64_t m = p->m, n = p->n, o = p->o;
+    if (x && n) CF_CUDA(cudaMemcpyAsync(x, p->x.p, n * 8, cudaMemcpyDeviceToHost, st));
+    if (z && n) CF_CUDA(cudaMemcpyAsync(z, p->z.p, n * 8, cudaMemcpyDeviceToHost, st));
+    if (delta && n) CF_CUDA(cudaMemcpyAsync(delta, p->delta.p, n * 8, cudaMemcpyDeviceToHost, st));
+    if (lam && m) CF_CUDA(cudaMemcpyAsync(lam, p->lam.p, m * 8, cudaMemcpyDeviceToHost, st));
+    if (iter) *iter = p->iter;
+    if ((y || gamma) && o) {
+        if (p->iter == 0) {
+            if (p->since_warm == 0) {
+                if (y) CF_CUDA(cudaMemcpyAsync(y, p->y0.p, o * 8, cudaMemcpyDeviceToHost, st));
+                if (gamma) CF_CUDA(cudaMemcpyAsync(gamma, p->gamma0.p, o * 8, cudaMemcpyDeviceToHost, st));
+            } else {
+                if (y) std::memset(y, 0, o * 8);
+                if (gamma) std::memset(gamma, 0, o * 8);
+            }
+        } else {
+            if (y && !p->br_valid) {
+                set_error("cf_plan_get_state: y needs b - r of the last iteration; enable cf_plan_set_export "
+                          "before iterating");
+                return CF_ESTATE;
+            }
+            DevBuf<double> dy, dg;
+            if (y) CF_TRY(dy.alloc(o));
+            if (gamma) CF_TRY(dg.alloc(o));
+            // mu only enters through eps (first iteration after a warm start)
+            CF_TRY(launch_export(p, p->export_mu, y ? dy.p : nullptr, gamma ? dg.p : nullptr));
+            if (y) CF_CUDA(cudaMemcpyAsync(y, dy.p, o * 8, cudaMemcpyDeviceToHost, st));
+            if (gamma) CF_CUDA(cudaMemcpyAsync(gamma, dg.p, o * 8, cudaMemcpyDeviceToHost, st));
+            CF_CUDA(cudaStreamSynchronize(st));
+        }
+    }
+    CF_CUDA(cudaStreamSynchronize(st));
+    return CF_OK;
+}
+
+int cf_plan_iterate(cf_plan* p, double mu, int64_t n_iters) {
+    CF_TRY(check_plan(p, "cf_plan_iterate"));
+    CF_TRY(check_mu(mu, "cf_plan_iterate"));
+    if (n_iters < 0) {
+        set_error("cf_plan_iterate: n_iters < 0");
+        return CF_EINVAL;
+    }
+    int64_t launches = 0;
+    p->export_mu = mu;
+    prof_reset(p);
+    CF_CUDA(cudaEventRecord(p->ev0, p->stream));
+    for (int64_t t = 0; t < n_iters; ++t) {
+        IterOpts opt = next_opts(p, mu, false);
+        CF_TRY(launch_iteration(p, opt, nullptr, &launches));
+        advance(p, 1, p->keep_br);
+    }
+    CF_CUDA(cudaEventRecord(p->ev1, p->stream));
+    CF_CUDA(cudaEventSynchronize(p->ev1));
+    prof_collect(p);
+    float ms = 0;
+    CF_CUDA(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+    p->last_loop_ms = ms;
+    p->last_launches = launches;
+    p->last_timed_iters = n_iters;
+    return CF_OK;
+}
+
+int cf_plan_report(cf_plan* p, double mu, cf_report* out) {
+    CF_TRY(check_plan(p, "cf_plan_report"));
+    CF_TRY(check_mu(mu, "cf_plan_report"));
+    if (!out) {
+        set_error("cf_plan_report: out is NULL");
+        return CF_EINVAL;
+    }
+    CF_TRY(launch_report(p, mu, false, nullptr, p->iter, 0, nullptr, nullptr));
+    CF_CUDA(cudaMemcpyAsync(out, p->report_slot.p, sizeof(cf_report), cudaMemcpyDeviceToHost, p->stream));
+    CF_CUDA(cudaStreamSynchronize(p->stream));
+    return CF_OK;
+}
+
+int cf_plan_solve(cf_plan* p, const cf_config* cfg, double* x_out, double* lam_out, cf_report* trace,
+                  int64_t trace_cap, int64_t* n_reports) {
+    CF_TRY(check_plan(p, "cf_plan_solve"));
+    if (!cfg || !trace || !n_reports) {
+        set_error("cf_plan_solve: NULL cfg/trace/n_reports");
+        return CF_EINVAL;
+    }
+    CF_TRY(check_mu(cfg->mu, "cf_plan_solve"));
+    if (cfg->max_iters < 1 || cfg->check_every < 1) {
+        set_error("cf_plan_solve: max_iters and check_every must be >= 1");
+        return CF_EINVAL;
+    }
+    const int64_t n_chunks = (cfg->max_iters + cfg->check_every - 1) / cfg->check_every;
+    if (trace_cap < n_chunks) {
+        set_error("cf_plan_solve: trace_cap < ceil(max_iters / check_every)");
+        return CF_EINVAL;
+    }
+    *n_reports = 0;
+    cudaStream_t st = p->stream;
+    p->export_mu = cfg->mu;
+    prof_reset(p);
+    CF_CUDA(cudaMemsetAsync(p->done.p, 0, 4, st));
+    constexpr int kDepth = 3;  // chunks in flight before the host looks at a report
+    cudaEvent_t evs[kDepth];
+    for (int i = 0; i < kDepth; ++i) CF_CUDA(cudaEventCreateWithFlags(&evs[i], cudaEventDisableTiming));
+    int64_t launches = 0, read = 0, k_final = 0;
+    bool finished = false;
+    const int since_warm0 = p->since_warm;
+    int rc = CF_OK;
+    CF_CUDA(cudaEventRecord(p->ev0, st));
+    auto consume = [&](int64_t c) -> int {
+        CF_CUDA(cudaEventSynchronize(evs[c % kDepth]));
+        const cf_report& r = p->host_reports[c % p->host_ring];
+        trace[read++] = r;
+        if (r.status != CF_STATUS_RUNNING) {
+            finished = true;
+            k_final = r.iter;
+        }
+        return CF_OK;
+    };
+    for (int64_t c = 0; c < n_chunks && !finished; ++c) {
+        const int64_t k0 = c * cfg->check_every;
+        const int64_t nit = std::min(cfg->check_every, cfg->max_iters - k0);
+        for (int64_t i = 1; i <= nit; ++i) {
+            IterOpts opt = next_opts(p, cfg->mu, i == nit);
+            rc = launch_iteration(p, opt, p->done.p, &launches);
+            if (rc != CF_OK) break;
+            p->since_warm = (int)std::min<int64_t>(2, p->since_warm + 1);
+        }
+        if (rc != CF_OK) break;
+        const int64_t slot = c % p->host_ring;
+        rc = launch_report(p, cfg->mu, true, cfg, k0 + nit, slot, p->done.p, &launches);
+        if (rc != CF_OK) break;
+        CF_CUDA(cudaMemcpyAsync(p->host_reports + slot, p->report_slot.p + slot, sizeof(cf_report),
+                                cudaMemcpyDeviceToHost, st));
+        CF_CUDA(cudaEventRecord(evs[c % kDepth], st));
+        if (c - read + 1 >= kDepth) CF_TRY(consume(read));
+    }
+    while (rc == CF_OK && !finished && read < n_chunks) {
+        // drain the chunks still in flight
+        const int64_t enq = std::min<int64_t>(n_chunks, read + kDepth);
+        (void)enq;
+        CF_TRY(consume(read));
+    }
+    CF_CUDA(cudaEventRecord(p->ev1, st));
+    CF_CUDA(cudaEventSynchronize(p->ev1));
+    prof_collect(p);
+    for (int i = 0; i < kDepth; ++i) cudaEventDestroy(evs[i]);
+    if (rc != CF_OK) return rc;
+    float ms = 0;
+    CF_CUDA(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+    p->last_loop_ms = ms;
+    p->last_launches = launches;
+    if (!finished) k_final = cfg->max_iters;  // unreachable: the last report is max_iters
+    p->last_timed_iters = k_final;
+    // state bookkeeping: the device stopped after iteration k_final
+    p->since_warm = since_warm0;
+    advance(p, k_final, true);
+    *n_reports = read;
+    if (x_out && p->n) CF_CUDA(cudaMemcpyAsync(x_out, p->x.p, p->n * 8, cudaMemcpyDeviceToHost, st));
+    if (lam_out && p->m) CF_CUDA(cudaMemcpyAsync(lam_out, p->lam.p, p->m * 8, cudaMemcpyDeviceToHost, st));
+    CF_CUDA(cudaStreamSynchronize(st));
+    return CF_OK;
+}
+
+int cf_apply_A(cf_plan* p, const double* x_dev, double* y_dev) {
+    CF_TRY(check_plan(p, "cf_apply_A"));
+    CF_TRY(launch_spmv_rows(p, x_dev, y_dev));
+    CF_CUDA(cudaStreamSynchronize(p->stream));
+    return CF_OK;
+}
+
+int cf_apply_At(cf_plan* p, const double* y_dev, double* x_dev) {
+    CF_TRY(check_plan(p, "cf_apply_At"));
+    CF_TRY(launch_spmv_cols(p, y_dev, x_dev));
+    CF_CUDA(cudaStreamSynchronize(p->stream));
+    return CF_OK;
+}
+
+int cf_project(cf_plan* p, const double* w_dev, double* out_dev) {
+    CF_TRY(check_plan(p, "cf_project"));
+    CF_TRY(launch_project(p, w_dev, out_dev));
+    CF_CUDA(cudaStreamSynchronize(p->stream));
+    return CF_OK;
+}
+
+int cf_plan_last_timing(const cf_plan* p, double* loop_ms, int64_t* launches, double* row_pass_ms,
+                        double* col_pass_ms, int64_t* timed_iters) {
+    CF_TRY(check_plan(p, "cf_plan_last_timing"));
+    if (loop_ms) *loop_ms = p->last_loop_ms;
+    if (launches) *launches = p->last_launches;
+    if (row_pass_ms) *row_pass_ms = p->prof_row_ms;
+    if (col_pass_ms) *col_pass_ms = p->prof_col_ms;
+    if (timed_iters) *timed_iters = p->last_timed_iters;
+    return CF_OK;
+}
+
+int cf_plan_set_profiling(cf_plan* p, int enable) {
+    CF_TRY(check_plan(p, "cf_plan_set_profiling"));
+    p->profiling = enable != 0;
+    return CF_OK;
+}
+
+int cf_plan_sync(cf_plan* p) {
+    CF_TRY(check_plan(p, "cf_plan_sync"));
+    CF_CUDA(cudaStreamSynchronize(p->stream));
+    return CF_OK;
+}
+
+}  // extern "C"

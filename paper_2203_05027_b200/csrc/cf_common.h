@@ -1,0 +1,162 @@
+// Internal header of libcfb200: the plan object, error plumbing and the launch
+// wrappers shared by the setup / loop / API translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/cfb200.h"
+
+namespace cf {
+
+// ---------------------------------------------------------------- geometry
+constexpr int kThreads = 256;     // threads per tile CTA
+constexpr int kCap = 4096;        // nonzero products staged in smem per chunk (32 KB)
+constexpr int kMaxSeg = 1024;     // rows / columns per tile
+constexpr int kSmallCone = 512;   // cones up to this size are projected inside the column tile
+constexpr int kReportFieldsRow = 5;
+constexpr int kReportFieldsCol = 8;
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what, const char* file, int line);
+
+#define CF_CUDA(call)                                                       \
+    do {                                                                    \
+        cudaError_t _e = (call);                                            \
+        if (_e != cudaSuccess) return ::cf::cuda_fail(_e, #call, __FILE__, __LINE__); \
+    } while (0)
+#define CF_TRY(call)                     \
+    do {                                 \
+        int _rc = (call);                \
+        if (_rc != CF_OK) return _rc;    \
+    } while (0)
+#define CF_LAUNCHED() CF_CUDA(cudaGetLastError())
+
+// ---------------------------------------------------------------- device buffers
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    int alloc(size_t count) {
+        release();
+        if (count == 0) count = 1;  // keep a valid pointer for empty dims
+        cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+        if (e != cudaSuccess) {
+            p = nullptr;
+            cudaGetLastError();
+            set_error(std::string("cudaMalloc of ") + std::to_string(count * sizeof(T)) +
+                      " bytes failed: " + cudaGetErrorString(e));
+            return CF_ENOMEM;
+        }
+        n = count;
+        return CF_OK;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+}  // namespace cf
+
+// ---------------------------------------------------------------- the plan
+// Device image of one ProblemInstance after build_uv (uv.py:64-98): the
+// canonical nonzero list held twice, as CSC (= canonical order) and CSR
+// (rows, columns ascending inside a row), plus the iterate vectors of the
+// reduced two-pass iteration.
+struct cf_plan {
+    int64_t m = 0, n = 0, o = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+
+    // CSC (canonical order, uv.py:76)
+    cf::DevBuf<int32_t> colptr, rowidx;
+    cf::DevBuf<double> valc;
+    // CSR
+    cf::DevBuf<int32_t> rowptr, colidx;
+    cf::DevBuf<double> valr;
+    cf::DevBuf<int32_t> csr2csc;  // canonical position of each CSR entry
+
+    // problem vectors and cached diagonals (fu_diag uv.py:81; d*b for the row pass)
+    cf::DevBuf<double> b, c, fu, db;
+
+    // cones (cones.py:39-59) and column tiling
+    bool all_unit = true;
+    int64_t n_blocks = 0;
+    cf::DevBuf<int32_t> cone_ptr;      // block offsets (n_blocks+1), only when !all_unit
+    cf::DevBuf<int32_t> tile_start;    // column tile starts (col_tiles+1)
+    cf::DevBuf<int32_t> tile_cone;     // first cone of each column tile
+    cf::DevBuf<int32_t> tile_big;      // big-cone id of a tile, -1 otherwise
+    cf::DevBuf<int32_t> big_cone;      // cone index of each big cone
+    int64_t n_big = 0;
+    int32_t rows_per_tile = 256;
+    int32_t cols_per_tile = 256;
+    int64_t row_tiles = 0, col_tiles = 0;
+    cf::DevBuf<double> wbuf;           // w = x+ - delta/mu for big-cone columns
+
+    // iterate state: x, z, delta (n); lam, h (m); br = b - r (m) when kept
+    cf::DevBuf<double> x, z, delta, lam, h, br, ax;
+    bool keep_br = false;
+    bool br_valid = false;
+    int64_t iter = 0;                  // iterations applied since the last set_state
+    double export_mu = 1.0;            // mu of the last iterations (y export after a warm start)
+    int since_warm = 2;                // 0/1: next iteration needs warm-start correction
+    cf::DevBuf<double> vterm1, rcorr, ccorr;   // warm-start corrections (A.3)
+    cf::DevBuf<double> y0, gamma0, eps;        // init y/gamma and eps = gamma0 + U^T lam0
+
+    // report machinery
+    int32_t row_report_ctas = 0;
+    cf::DevBuf<double> part_row, part_col;     // per-CTA partials
+    cf::DevBuf<cf_report> report_slot;         // device report ring
+    cf::DevBuf<int32_t> done;                  // device early-exit flag
+    cf_report* host_reports = nullptr;         // pinned ring
+    int64_t host_ring = 0;
+
+    // timing
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    double last_loop_ms = 0.0;
+    int64_t last_launches = 0;
+    int64_t last_timed_iters = 0;
+    bool profiling = false;
+    double prof_row_ms = 0.0, prof_col_ms = 0.0;
+    std::vector<cudaEvent_t> prof_events;  // 3 per profiled iteration: start, after col pass, after row pass
+    size_t prof_used = 0;
+};
+
+namespace cf {
+
+// ---------------------------------------------------------------- launch wrappers (cf_kernels.cu)
+struct IterOpts {
+    double mu = 1.0;
+    bool report = false;         // write ax/br for the report of this iteration
+    const double* vterm = nullptr;
+    const double* ccorr = nullptr;
+    const double* rcorr = nullptr;
+};
+// one iteration (col pass + cones + row pass); returns kernel launches issued via *launches
+int launch_iteration(cf_plan* p, const IterOpts& opt, const int32_t* done, int64_t* launches);
+// y = A x (rows), x = A^T y (cols)
+int launch_spmv_rows(cf_plan* p, const double* x, double* y);
+int launch_spmv_cols(cf_plan* p, const double* y, double* x);
+// report of the current state into p->report_slot[slot]; termination per cfg (nullable)
+int launch_report(cf_plan* p, double mu, bool ax_ready, const cf_config* cfg, int64_t k,
+                  int64_t slot, const int32_t* done, int64_t* launches);
+int launch_project(cf_plan* p, const double* w, double* out);
+int launch_export(cf_plan* p, double mu, double* y, double* gamma);
+int launch_warm_start(cf_plan* p, double mu);
+// setup helpers
+int launch_row_diag(cf_plan* p);
+// profiling: reset before a loop, fold the recorded per-pass event times after its final sync
+void prof_reset(cf_plan* p);
+void prof_collect(cf_plan* p);
+
+}  // namespace cf

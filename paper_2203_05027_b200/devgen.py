@@ -1,0 +1,126 @@
+"""GPU instance generator for the large configs (C2: 100M nonzeros) — bench tooling.
+
+Same recipe as the reference generator (generate.py:1-18, :103-140), built on
+the device because the host recipe needs ~16 GB and ~4 minutes at 1e8
+nonzeros: distinct uniform cell positions, N(0,1) values (zeros redrawn), a
+primal witness x = Proj_K(N(0,1)) with b = A x, and in bounded mode
+c = Proj_K(N(0,1)) - A^T N(0,1). The random stream is torch's Philox, not
+numpy's PCG64, so instances are not bit-identical to ``instances.generate``
+for the same seed; both solvers are always fed the SAME arrays.
+
+Returns device tensors plus the DevicePlan already built from them (A x and
+A^T y of the witness products run through libcfb200's own operators).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .engine import DevicePlan
+
+__all__ = ["DeviceInstance", "generate_device", "c2_spec", "c3_spec", "to_host_problem"]
+
+
+@dataclass
+class DeviceInstance:
+    m: int
+    n: int
+    o: int
+    cone_kind: str
+    rows: "object"   # torch int64 [o], row-major sorted
+    cols: "object"   # torch int64 [o]
+    vals: "object"   # torch float64 [o]
+    b: "object"      # torch float64 [m]
+    c: "object"      # torch float64 [n]
+    block_sizes: np.ndarray
+    plan: DevicePlan | None = None
+
+
+def c2_spec():
+    """C2: LP m=5M, n=10M, 100M nonzeros (density 2e-6)."""
+    return dict(m=5_000_000, n=10_000_000, density=2e-6, cone_kind="lp")
+
+
+def c3_spec():
+    """C3: SOCP m=2M, n=4M, 40M nonzeros, 1M K4 cones."""
+    return dict(m=2_000_000, n=4_000_000, density=5e-6, cone_kind="socp4")
+
+
+def _distinct_positions(torch, gen, total: int, count: int, device):
+    """count distinct cells uniform over [0, total), sorted (uniform without replacement)."""
+    draw = count + count // 64 + 1024
+    pos = torch.unique(torch.randint(0, total, (draw,), generator=gen, device=device, dtype=torch.int64))
+    while pos.numel() < count:
+        more = torch.randint(0, total, (2 * (count - pos.numel()) + 1024,), generator=gen, device=device,
+                             dtype=torch.int64)
+        pos = torch.unique(torch.cat([pos, more]))
+    if pos.numel() > count:
+        keep = torch.randperm(pos.numel(), generator=gen, device=device)[:count]
+        pos = torch.sort(pos[keep]).values
+    return pos
+
+
+def generate_device(m: int, n: int, density: float, cone_kind: str = "lp", seed: int = 0,
+                    bounded_mode: bool = True, keep_plan: bool = True, stream: int | None = None) -> DeviceInstance:
+    import torch
+
+    dev = torch.device("cuda")
+    o = int(round(m * n * density))
+    if o < 1:
+        raise ValueError("instance has no nonzeros")
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(int(seed))
+    pos = _distinct_positions(torch, gen, m * n, o, dev)
+    rows = pos // n
+    cols = pos % n
+    del pos
+    vals = torch.randn(o, generator=gen, device=dev, dtype=torch.float64)
+    while True:
+        zero = vals == 0.0
+        nz = int(zero.sum())
+        if nz == 0:
+            break
+        vals[zero] = torch.randn(nz, generator=gen, device=dev, dtype=torch.float64)
+    if cone_kind == "lp":
+        sizes = np.ones(n, dtype=np.int64)
+    elif cone_kind == "socp4":
+        if n % 4:
+            raise ValueError("socp4 requires n divisible by 4")
+        sizes = np.full(n // 4, 4, dtype=np.int64)
+    else:
+        raise ValueError(cone_kind)
+    b = torch.zeros(m, dtype=torch.float64, device=dev)
+    c = torch.zeros(n, dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
+    plan = DevicePlan.from_device(m, n, o, rows.data_ptr(), cols.data_ptr(), vals.data_ptr(), b.data_ptr(),
+                                  c.data_ptr(), sizes, stream=stream)
+    xdot = torch.randn(n, generator=gen, device=dev, dtype=torch.float64)
+    xf = torch.empty_like(xdot)
+    plan.project(xdot.data_ptr(), xf.data_ptr())
+    plan.apply_A(xf.data_ptr(), b.data_ptr())                 # b = A Proj_K(xdot)
+    if bounded_mode:
+        lam = torch.randn(m, generator=gen, device=dev, dtype=torch.float64)
+        sd = torch.randn(n, generator=gen, device=dev, dtype=torch.float64)
+        s = torch.empty_like(sd)
+        plan.project(sd.data_ptr(), s.data_ptr())
+        atl = torch.empty(n, dtype=torch.float64, device=dev)
+        plan.apply_At(lam.data_ptr(), atl.data_ptr())
+        c.copy_(s - atl)                                       # c = Proj_K(s) - A^T lam
+    else:
+        c.copy_(torch.randn(n, generator=gen, device=dev, dtype=torch.float64))
+    torch.cuda.synchronize()
+    plan.set_rhs(b.data_ptr(), c.data_ptr(), on_device=True)
+    inst = DeviceInstance(m, n, o, cone_kind, rows, cols, vals, b, c, sizes, plan if keep_plan else None)
+    if not keep_plan:
+        plan.close()
+    return inst
+
+
+def to_host_problem(inst: DeviceInstance):
+    """Copy a device instance to a host ProblemInstance (this package's types)."""
+    from .problem import ConeSpec, ProblemInstance, TripletMatrix
+
+    a = TripletMatrix(inst.m, inst.n, inst.rows.cpu().numpy(), inst.cols.cpu().numpy(), inst.vals.cpu().numpy())
+    return ProblemInstance(a, inst.b.cpu().numpy(), inst.c.cpu().numpy(), ConeSpec(inst.block_sizes))
