@@ -13,10 +13,10 @@
 namespace cf {
 
 // ---------------------------------------------------------------- geometry
-constexpr int kThreads = 256;     // threads per tile CTA
-constexpr int kCap = 4096;        // nonzero products staged in smem per chunk (32 KB)
-constexpr int kMaxSeg = 1024;     // rows / columns per tile
-constexpr int kSmallCone = 512;   // cones up to this size are projected inside the column tile
+constexpr int kThreads = 256;     // threads of the simple (non-pass) kernels
+constexpr int kTileNnz = 2048;    // nonzeros per tile (= pass::kPCap)
+constexpr int kTileSeg = 256;     // rows / columns per tile (= pass::kPSeg)
+constexpr int kSmallCone = 256;   // cones up to this size are projected inside the column tile
 constexpr int kReportFieldsRow = 5;
 constexpr int kReportFieldsCol = 8;
 
@@ -48,7 +48,8 @@ struct DevBuf {
     int alloc(size_t count) {
         release();
         if (count == 0) count = 1;  // keep a valid pointer for empty dims
-        cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+        // +64 bytes: the pass engine's bulk copies read 16-byte-aligned supersets
+        cudaError_t e = cudaMalloc(&p, count * sizeof(T) + 64);
         if (e != cudaSuccess) {
             p = nullptr;
             cudaGetLastError();
@@ -98,9 +99,13 @@ struct cf_plan {
     cf::DevBuf<int32_t> tile_big;      // big-cone id of a tile, -1 otherwise
     cf::DevBuf<int32_t> big_cone;      // cone index of each big cone
     int64_t n_big = 0;
-    int32_t rows_per_tile = 256;
-    int32_t cols_per_tile = 256;
+    cf::DevBuf<int2> row_tb, col_tb;   // tile boundaries {first segment, first nonzero}
     int64_t row_tiles = 0, col_tiles = 0;
+    // row-pass column panels: the CSR is stored panel-major (segment = panel*m + row)
+    // so each row-pass launch gathers only one panel's slice of x (L2-resident)
+    int32_t n_panels = 1;
+    int64_t panel_cols = 0;
+    std::vector<int64_t> row_panel_tile;   // first row tile of each panel (n_panels+1)
     cf::DevBuf<double> wbuf;           // w = x+ - delta/mu for big-cone columns
 
     // iterate state: x, z, delta (n); lam, h (m); br = b - r (m) when kept
@@ -118,6 +123,7 @@ struct cf_plan {
     cf::DevBuf<double> part_row, part_col;     // per-CTA partials
     cf::DevBuf<cf_report> report_slot;         // device report ring
     cf::DevBuf<int32_t> done;                  // device early-exit flag
+    cf::DevBuf<int32_t> nf_flag;               // report: non-finite implicit y/gamma
     cf_report* host_reports = nullptr;         // pinned ring
     int64_t host_ring = 0;
 
@@ -155,6 +161,7 @@ int launch_export(cf_plan* p, double mu, double* y, double* gamma);
 int launch_warm_start(cf_plan* p, double mu);
 // setup helpers
 int launch_row_diag(cf_plan* p);
+int max_col_report_ctas();
 // profiling: reset before a loop, fold the recorded per-pass event times after its final sync
 void prof_reset(cf_plan* p);
 void prof_collect(cf_plan* p);

@@ -11,53 +11,20 @@
 //   row pass (CSR)                    r = fu*(d*b + A x+);  lam+ = lam + mu*(r - b);
 //                                     h+ = (b - r) - lam+/mu
 //
-// Both passes run the same tile engine: a CTA owns a tile of up to kMaxSeg
-// segments (rows or columns) whose nonzeros are contiguous; it streams the
-// tile's (index, value) pairs with coalesced evict-first loads, gathers the
-// dense operand (x or h, kept L2-resident with evict-last), stages the
-// products in shared memory and then reduces each segment SEQUENTIALLY in
-// storage order - the order np.bincount uses (uv.py:10-12) - so A x and
-// A^T lam are bit-identical to the reference's apply_U(apply_Vt(x)) and
-// apply_V(apply_Ut(lam)). Everything is compiled with -fmad=false so every
-// fp64 operation rounds like its numpy counterpart.
+// Both passes (and the report's A^T lam pass, and the plain operators) run on
+// the persistent TMA-pipelined tile engine of cf_pass.cuh with a per-pass
+// policy struct (RowIter, ColIter, ColReport, RowSpmv, ColSpmv) supplying the
+// staged epilogue vectors and the epilogue. Segment sums are sequential in
+// storage order, so A x and A^T lam are bit-identical to the reference's
+// apply_U(apply_Vt(x)) and apply_V(apply_Ut(lam)). Everything is compiled with
+// -fmad=false so every fp64 operation rounds like its numpy counterpart.
 #include <cmath>
 
 #include "cf_common.h"
+#include "cf_pass.cuh"
 
 namespace cf {
 namespace {
-
-// ---------------------------------------------------------------- memory helpers
-__device__ __forceinline__ uint64_t policy_evict_first() {
-    uint64_t p;
-    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ uint64_t policy_evict_last() {
-    uint64_t p;
-    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-// streamed once per pass: do not pollute L1, leave L2 first
-__device__ __forceinline__ double ld_stream(const double* ptr, uint64_t pol) {
-    double v;
-    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(ptr), "l"(pol));
-    return v;
-}
-__device__ __forceinline__ int32_t ld_stream(const int32_t* ptr, uint64_t pol) {
-    int32_t v;
-    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(ptr), "l"(pol));
-    return v;
-}
-// random gather of the dense operand: keep it resident in L2
-__device__ __forceinline__ double ld_gather(const double* ptr, uint64_t pol) {
-    double v;
-    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(ptr), "l"(pol));
-    return v;
-}
-__device__ __forceinline__ void st_keep(double* ptr, double v, uint64_t pol) {
-    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(ptr), "d"(v), "l"(pol) : "memory");
-}
 
 // np.max semantics: NaN propagates
 __device__ __forceinline__ double nanmax(double a, double b) { return (a > b || a != a) ? a : b; }
@@ -88,140 +55,8 @@ __device__ double block_reduce(double v, double* sh, Op op) {
     return v;
 }
 
-// ---------------------------------------------------------------- tile engine
-// sacc[s] = sum_{k in [sptr[s], sptr[s+1])} val[k] * g[idx[k]], sequential in k.
-// Chunks of kCap products go through shared memory, so segments of any
-// length are handled (a segment spanning chunks keeps its partial in sacc).
-// Thread t owns segments t, t+kThreads, ... in both the init and the reduce
-// phase, so no barrier is needed between them.
-__device__ __forceinline__ void tile_gather_reduce(const int32_t* __restrict__ idx,
-                                                   const double* __restrict__ val,
-                                                   const double* __restrict__ g, const int32_t* sptr,
-                                                   int nseg, double* sacc, double* sprod) {
-    const uint64_t pol_s = policy_evict_first();
-    const uint64_t pol_g = policy_evict_last();
-    const int k0 = sptr[0], k1 = sptr[nseg];
-    for (int s = threadIdx.x; s < nseg; s += kThreads) sacc[s] = 0.0;
-    for (int c0 = k0; c0 < k1; c0 += kCap) {
-        const int len = min(kCap, k1 - c0);
-        const int32_t* ip = idx + c0;
-        const double* vp = val + c0;
-        int t = threadIdx.x;
-        for (; t + 3 * kThreads < len; t += 4 * kThreads) {
-            const int j0 = ld_stream(ip + t, pol_s);
-            const int j1 = ld_stream(ip + t + kThreads, pol_s);
-            const int j2 = ld_stream(ip + t + 2 * kThreads, pol_s);
-            const int j3 = ld_stream(ip + t + 3 * kThreads, pol_s);
-            const double a0 = ld_stream(vp + t, pol_s);
-            const double a1 = ld_stream(vp + t + kThreads, pol_s);
-            const double a2 = ld_stream(vp + t + 2 * kThreads, pol_s);
-            const double a3 = ld_stream(vp + t + 3 * kThreads, pol_s);
-            const double g0 = ld_gather(g + j0, pol_g);
-            const double g1 = ld_gather(g + j1, pol_g);
-            const double g2 = ld_gather(g + j2, pol_g);
-            const double g3 = ld_gather(g + j3, pol_g);
-            sprod[t] = __dmul_rn(a0, g0);
-            sprod[t + kThreads] = __dmul_rn(a1, g1);
-            sprod[t + 2 * kThreads] = __dmul_rn(a2, g2);
-            sprod[t + 3 * kThreads] = __dmul_rn(a3, g3);
-        }
-        for (; t < len; t += kThreads)
-            sprod[t] = __dmul_rn(ld_stream(vp + t, pol_s), ld_gather(g + ld_stream(ip + t, pol_s), pol_g));
-        __syncthreads();
-        for (int s = threadIdx.x; s < nseg; s += kThreads) {
-            const int a = max(sptr[s], c0) - c0;
-            const int e = min(sptr[s + 1], c0 + len) - c0;
-            if (a < e) {
-                double acc = sacc[s];
-                for (int k = a; k < e; ++k) acc = __dadd_rn(acc, sprod[k]);
-                sacc[s] = acc;
-            }
-        }
-        __syncthreads();
-    }
-}
-
-// ---------------------------------------------------------------- row pass
-struct RowArgs {
-    const int32_t* rowptr;
-    const int32_t* colidx;
-    const double* val;
-    const double* x;      // gathered operand
-    const double* b;
-    const double* fu;
-    const double* db;     // d * b
-    double* lam;
-    double* h;
-    double* br;           // optional: b - r (SolverState.y export, report finiteness)
-    double* ax;           // optional: A x (report)
-    const double* rcorr;  // optional warm-start correction U eps / mu
-    int32_t m;
-    int32_t rows_per_tile;
-    double mu;
-    const int32_t* done;
-};
-
-// MODE 0: ADMM row update (y_update + lam/gamma parts of dual_update,
-//         solver.py:179-183,194-195). MODE 1: ax = A x only (apply_U . apply_Vt).
-template <int MODE>
-__global__ void __launch_bounds__(kThreads) k_row_pass(const RowArgs a) {
-    if (a.done && *a.done) return;
-    __shared__ double sprod[kCap];
-    __shared__ double sacc[kMaxSeg];
-    __shared__ int32_t sptr[kMaxSeg + 1];
-    const int r0 = blockIdx.x * a.rows_per_tile;
-    const int nseg = min(a.rows_per_tile, a.m - r0);
-    for (int s = threadIdx.x; s <= nseg; s += kThreads) sptr[s] = a.rowptr[r0 + s];
-    __syncthreads();
-    tile_gather_reduce(a.colidx, a.val, a.x, sptr, nseg, sacc, sprod);
-    const uint64_t pol_keep = policy_evict_last();
-    for (int s = threadIdx.x; s < nseg; s += kThreads) {
-        const int i = r0 + s;
-        const double axi = sacc[s];
-        if (MODE == 1) {
-            a.ax[i] = axi;
-            continue;
-        }
-        const double bi = a.b[i], li = a.lam[i];
-        double si = a.db[i] + axi;                 // (U t)_i with t = a b + x (App. A)
-        if (a.rcorr) si = si - a.rcorr[i];
-        const double r = a.fu[i] * si;              // r = U y+ = fu * U t
-        const double ln = li + a.mu * (r - bi);    // solver.py:194
-        const double bmr = bi - r;
-        const double hi = bmr - ln / a.mu;          // h = b - r - lam+/mu
-        a.lam[i] = ln;
-        st_keep(a.h + i, hi, pol_keep);
-        if (a.br) a.br[i] = bmr;
-        if (a.ax) a.ax[i] = axi;
-    }
-}
-
-// ---------------------------------------------------------------- column pass
-struct ColArgs {
-    const int32_t* colptr;
-    const int32_t* rowidx;
-    const double* val;
-    const double* h;        // gathered operand
-    const double* c;
-    double* x;
-    double* z;
-    double* delta;
-    const double* vterm;    // optional: V(y0 + gamma0/mu) replaces cnt*x + A^T h (first warm iteration)
-    const double* ccorr;    // optional: V eps / mu subtracted (second warm iteration)
-    const int32_t* tile_start;
-    const int32_t* tile_cone;
-    const int32_t* tile_big;
-    const int32_t* cone_ptr;
-    double* wbuf;
-    int32_t n;
-    int32_t cols_per_tile;
-    double mu;
-    const int32_t* done;
-};
-
-// Lorentz-cone projection of one block (cones.py:76-92; branch order :78-80).
-// w, out, xp, dold, dnew are shared-memory (or global) arrays indexed by
-// position inside the block.
+// Lorentz-cone projection of one block (cones.py:76-92; branch order :78-80),
+// tail sum of squares sequential like np.bincount (cones.py:69-72).
 __device__ __forceinline__ void project_block_dev(const double* w, int q, double* out) {
     const double w0 = w[0];
     double ssq = 0.0;
@@ -238,85 +73,198 @@ __device__ __forceinline__ void project_block_dev(const double* w, int q, double
     }
 }
 
-// MODE 0: LP (all blocks of size 1, cones.py:108-109 shortcut), fused.
-// MODE 1: general cones; small cones projected in the tile, big cones deferred.
-// MODE 2: x = A^T y only (apply_V . apply_Ut).
-template <int MODE>
-__global__ void __launch_bounds__(kThreads) k_col_pass(const ColArgs a) {
-    if (a.done && *a.done) return;
-    __shared__ double sprod[kCap];
-    __shared__ double sacc[kMaxSeg];
-    __shared__ int32_t sptr[kMaxSeg + 1];
-    int c0, nseg;
-    if (a.tile_start) {
-        c0 = a.tile_start[blockIdx.x];
-        nseg = a.tile_start[blockIdx.x + 1] - c0;
-    } else {
-        c0 = blockIdx.x * a.cols_per_tile;
-        nseg = min(a.cols_per_tile, a.n - c0);
-    }
-    for (int s = threadIdx.x; s <= nseg; s += kThreads) sptr[s] = a.colptr[c0 + s];
-    __syncthreads();
-    tile_gather_reduce(a.rowidx, a.val, a.h, sptr, nseg, sacc, sprod);
-    if (MODE == 2) {
-        for (int s = threadIdx.x; s < nseg; s += kThreads) a.x[c0 + s] = sacc[s];
-        return;
-    }
-    const uint64_t pol_keep = policy_evict_last();
-    const double mu = a.mu;
-    // x-update (solver.py:168-176) in the reference's operand order:
-    // fv * (((V(..) + z) + delta/mu) - c/mu)
-    double* sxp = sprod;                 // x+      (reuses the product buffer)
-    double* sw = sprod + kMaxSeg;        // x+ - delta/mu
-    double* sd = sprod + 2 * kMaxSeg;    // delta (old)
-    double* sdn = sprod + 3 * kMaxSeg;   // delta+
-    for (int s = threadIdx.x; s < nseg; s += kThreads) {
-        const int j = c0 + s;
-        const int cnt = sptr[s + 1] - sptr[s];
-        const double fv = 1.0 / (1.0 + (double)cnt);   // uv.py:82
-        const double xj = a.x[j], zj = a.z[j], dj = a.delta[j], cj = a.c[j];
-        const double dm = dj / mu;
-        double v = a.vterm ? a.vterm[j] : __dadd_rn(__dmul_rn((double)cnt, xj), sacc[s]);
-        if (a.ccorr) v = v - a.ccorr[j];
-        const double xp = fv * (((v + zj) + dm) - cj / mu);
-        const double w = xp - dm;                        // z_update argument, solver.py:188
-        if (MODE == 0) {
-            const double zp = w > 0.0 ? w : 0.0;         // np.where(w > 0, w, 0): NaN -> 0, -0 -> +0
-            const double dp = dj + mu * (zp - xp);       // solver.py:196
-            st_keep(a.x + j, xp, pol_keep);
-            a.z[j] = zp;
-            a.delta[j] = dp;
-        } else {
-            sxp[s] = xp;
-            sw[s] = w;
-            sd[s] = dj;
+using pass::kPSeg;
+using pass::kReduceThreads;
+using pass::rtid;
+using pass::Smem;
+using pass::Stage;
+
+// ---------------------------------------------------------------- pass policies
+// Common layout accessors. Staged vectors are indexed by segment: for a row
+// panel p the segments are p*m + i, so vector bases are shifted by -seg_off.
+struct Layout {
+    const int32_t* ptr_;
+    const int32_t* idx_;
+    const double* val_;
+    const double* g_;
+    int32_t nvec_ = 0;
+    bool carry_ = false;
+    const double* vb_[pass::kPVecs] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    __device__ const int32_t* ptr() const { return ptr_; }
+    __device__ const int32_t* idx() const { return idx_; }
+    __device__ const double* val() const { return val_; }
+    __device__ const double* gvec() const { return g_; }
+    __device__ int nvec() const { return nvec_; }
+    __device__ const double* vec(int v) const { return vb_[v]; }
+    __device__ bool carry_in() const { return carry_; }
+    __device__ void check(double, int, double) {}
+    __device__ void finish(Smem&) {}
+};
+
+// Row pass of the iteration: y_update + lam/gamma of dual_update (solver.py:179-183,
+// 194-195) in the reduced form r = fu*(d*b + A x+), lam+ = lam + mu(r - b),
+// h = b - r - lam+/mu. With column panels, every panel but the last only
+// carries the partial row sums (in `carry`), continuing the sequential order.
+struct RowIter : Layout {
+    int64_t seg_off;       // p * m
+    bool last;             // last panel: ADMM update
+    double* carry;         // partial A x between panels (= the plan's ax buffer)
+    double* lam;
+    double* h;
+    double* br;            // optional: b - r
+    double* ax;            // optional: A x (report iterations)
+    const double* rcorr;   // optional: warm-start U eps / mu
+    double mu;
+    __device__ void epilogue(Smem& sm, Stage&, int, int s0, int nseg, const int32_t*, const double* const* vb) {
+        const uint64_t pl = pass::pol_last(), pf = pass::pol_first();
+        for (int q = rtid(); q < nseg; q += kReduceThreads) {
+            const int64_t i = s0 + q - seg_off;
+            const double axi = sm.acc[q];
+            if (!last) {
+                carry[i] = axi;
+                continue;
+            }
+            const double bi = vb[0][q], li = vb[1][q], fui = vb[2][q], dbi = vb[3][q];
+            double si = dbi + axi;                  // (U t)_i with t = a b + x
+            if (rcorr) si = si - rcorr[i];
+            const double r = fui * si;              // r = U y+ = fu (U t)
+            const double ln = li + mu * (r - bi);   // solver.py:194
+            const double bmr = bi - r;
+            const double hi = bmr - ln / mu;        // h = b - r - lam+/mu
+            pass::st_hint(lam + i, ln, pf);
+            pass::st_hint(h + i, hi, pl);           // gathered by the next column pass
+            if (br) br[i] = bmr;
+            if (ax) ax[i] = axi;
         }
     }
-    if (MODE == 0) return;
-    __syncthreads();
-    const int big = a.tile_big[blockIdx.x];
-    if (big >= 0) {  // part of a cone larger than kSmallCone: projected by k_big_cone
-        for (int s = threadIdx.x; s < nseg; s += kThreads) {
-            st_keep(a.x + c0 + s, sxp[s], pol_keep);
-            a.wbuf[c0 + s] = sw[s];
+};
+
+// y = A x (apply_U . apply_Vt, uv.py:106-131), panel by panel with y as the carry.
+struct RowSpmv : Layout {
+    int64_t seg_off;
+    double* y;
+    __device__ void epilogue(Smem& sm, Stage&, int, int s0, int nseg, const int32_t*, const double* const*) {
+        for (int q = rtid(); q < nseg; q += kReduceThreads) y[s0 + q - seg_off] = sm.acc[q];
+    }
+};
+
+// x = A^T y (apply_V . apply_Ut)
+struct ColSpmv : Layout {
+    double* y;
+    __device__ void epilogue(Smem& sm, Stage&, int, int s0, int nseg, const int32_t*, const double* const*) {
+        for (int q = rtid(); q < nseg; q += kReduceThreads) y[s0 + q] = sm.acc[q];
+    }
+};
+
+// Column pass of the iteration: x_update (solver.py:168-176) in the reduced form
+// V(y + gamma/mu) = cnt*x + A^T h, then z = Proj_K(x+ - delta/mu), delta update.
+struct ColIter : Layout {
+    double* x;
+    double* z;
+    double* delta;
+    const double* vterm;   // optional: V(y0 + gamma0/mu) (first warm iteration)
+    const double* ccorr;   // optional: V eps / mu (second warm iteration)
+    int32_t cones;         // 0 = all blocks of size 1 (cones.py:108-109 shortcut)
+    const int32_t* tile_cone;
+    const int32_t* tile_big;
+    const int32_t* cone_ptr;
+    double* wbuf;
+    double mu;
+    __device__ void epilogue(Smem& sm, Stage& st, int tile, int s0, int nseg, const int32_t* ptrb,
+                             const double* const* vb) {
+        const uint64_t pl = pass::pol_last(), pf = pass::pol_first();
+        // the staged index buffer is free after the gather phase: cone scratch
+        double* sxp = reinterpret_cast<double*>(st.idx);
+        double* sw = sxp + kPSeg;
+        double* sdn = sxp + 2 * kPSeg;
+        for (int q = rtid(); q < nseg; q += kReduceThreads) {
+            const int j = s0 + q;
+            const int cnt = ptrb[q + 1] - ptrb[q];
+            const double fv = 1.0 / (1.0 + (double)cnt);   // uv.py:82
+            const double xj = vb[0][q], zj = vb[1][q], dj = vb[2][q], cj = vb[3][q];
+            const double dm = dj / mu;
+            double v = vterm ? vterm[j] : __dadd_rn(__dmul_rn((double)cnt, xj), sm.acc[q]);
+            if (ccorr) v = v - ccorr[j];
+            const double xp = fv * (((v + zj) + dm) - cj / mu);   // solver.py:171-176 operand order
+            const double w = xp - dm;                            // solver.py:188
+            if (!cones) {
+                const double zp = w > 0.0 ? w : 0.0;             // NaN -> 0, -0 -> +0
+                const double dp = dj + mu * (zp - xp);           // solver.py:196
+                pass::st_hint(x + j, xp, pl);                    // gathered by the next row pass
+                pass::st_hint(z + j, zp, pf);
+                pass::st_hint(delta + j, dp, pf);
+            } else {
+                sxp[q] = xp;
+                sw[q] = w;
+            }
         }
-        return;
+        if (!cones) return;
+        pass::reducer_sync();
+        const int big = tile_big[tile];
+        if (big >= 0) {  // piece of a cone wider than a tile: k_big_cone projects it
+            for (int q = rtid(); q < nseg; q += kReduceThreads) {
+                pass::st_hint(x + s0 + q, sxp[q], pl);
+                wbuf[s0 + q] = sw[q];
+            }
+            return;
+        }
+        double* szp = sm.acc;  // A^T h no longer needed
+        const int q0 = tile_cone[tile], q1 = tile_cone[tile + 1];
+        for (int q = q0 + rtid(); q < q1; q += kReduceThreads) {
+            const int off = cone_ptr[q] - s0, size = cone_ptr[q + 1] - cone_ptr[q];
+            project_block_dev(sw + off, size, szp + off);
+            for (int t = 0; t < size; ++t) sdn[off + t] = vb[2][off + t] + mu * (szp[off + t] - sxp[off + t]);
+        }
+        pass::reducer_sync();
+        for (int q = rtid(); q < nseg; q += kReduceThreads) {
+            pass::st_hint(x + s0 + q, sxp[q], pl);
+            pass::st_hint(z + s0 + q, szp[q], pf);
+            pass::st_hint(delta + s0 + q, sdn[q], pf);
+        }
     }
-    double* sz = sacc;  // A^T h no longer needed
-    const int q0 = a.tile_cone[blockIdx.x], q1 = a.tile_cone[blockIdx.x + 1];
-    for (int q = q0 + threadIdx.x; q < q1; q += kThreads) {
-        const int off = a.cone_ptr[q] - c0;
-        const int sz_q = a.cone_ptr[q + 1] - a.cone_ptr[q];
-        project_block_dev(sw + off, sz_q, sz + off);
-        for (int t = 0; t < sz_q; ++t) sdn[off + t] = sd[off + t] + mu * (sz[off + t] - sxp[off + t]);
+};
+
+// Column part of compute_report (solver.py:208-225): atl = A^T lam (bincount order),
+// dual = atl + c, stat = dual - delta, pobj = c.x, cone_gap = max|x - z| and the
+// finiteness of x, z, delta and of the implicit y_k = x_j + a_k (b_i - r_i),
+// gamma_k = -a_k lam_i. Per-thread partials are reduced once per CTA (finish).
+// The gather warps own the per-nonzero checks, the reducer warps the rest;
+// both fold into the CTA's partials.
+struct ColReport : Layout {
+    const double* br;      // may be null
+    double* part;          // [kReportFieldsCol][gridDim.x]
+    int32_t* nf_flag;      // set by gather warps on a non-finite implicit y/gamma
+    double d2, dmx, s2, smx, amx, cx, cg, nf;
+    __device__ void check(double a, int i, double lam_i) {
+        if (!isfinite(a * lam_i) || (br && !isfinite(a * br[i]))) *nf_flag = 1;
     }
-    __syncthreads();
-    for (int s = threadIdx.x; s < nseg; s += kThreads) {
-        st_keep(a.x + c0 + s, sxp[s], pol_keep);
-        a.z[c0 + s] = sz[s];
-        a.delta[c0 + s] = sdn[s];
+    __device__ void epilogue(Smem& sm, Stage&, int, int, int nseg, const int32_t*, const double* const* vb) {
+        for (int q = rtid(); q < nseg; q += kReduceThreads) {
+            const double atl = sm.acc[q];
+            const double xj = vb[0][q], zj = vb[1][q], dj = vb[2][q], cj = vb[3][q];
+            const double dual = atl + cj;
+            const double stat = dual - dj;
+            d2 = d2 + dual * dual;
+            dmx = nanmax(dmx, fabs(dual));
+            s2 = s2 + stat * stat;
+            smx = nanmax(smx, fabs(stat));
+            amx = nanmax(amx, fabs(atl));
+            cx = cx + cj * xj;
+            cg = nanmax(cg, fabs(xj - zj));
+            if (!isfinite(xj) || !isfinite(zj) || !isfinite(dj)) nf = 1.0;
+        }
     }
-}
+    __device__ void finish(Smem& sm) {
+        const int G = gridDim.x;
+        const double vals[8] = {d2, dmx, s2, smx, amx, cx, cg, nf};
+        const bool is_sum[8] = {true, false, true, false, false, true, false, false};
+        for (int f = 0; f < 8; ++f) {
+            const double v = is_sum[f] ? pass::reducer_reduce(vals[f], sm.red, SumOp())
+                                       : pass::reducer_reduce(vals[f], sm.red, MaxOp());
+            if (rtid() == 0) part[f * G + blockIdx.x] = v;
+        }
+    }
+};
 
 // Cones larger than kSmallCone: one CTA per cone. Tail norm by a fixed
 // per-thread sequential split + deterministic tree (not the reference's
@@ -399,110 +347,10 @@ __global__ void __launch_bounds__(kThreads) k_row_report(const RowReportArgs a) 
     if (threadIdx.x == 0) a.part[4 * G + blockIdx.x] = v;
 }
 
-// Column part (solver.py:215-218,223,225): atl = A^T lam (sequential,
-// bincount order), dual = atl + c, stat = dual - delta; plus the finiteness
-// of x, z, delta and of the implicit y_k = x_j + a_k (b_i - r_i) and
-// gamma_k = -a_k lam_i (solver.py:208-211).
-struct ColReportArgs {
-    const int32_t* colptr;
-    const int32_t* rowidx;
-    const double* val;
-    const double* lam;
-    const double* br;    // may be null (then the y check reduces to x)
-    const double* c;
-    const double* x;
-    const double* z;
-    const double* delta;
-    const int32_t* tile_start;
-    int32_t n;
-    int32_t cols_per_tile;
-    double* part;        // [kReportFieldsCol][gridDim.x]
-    const int32_t* done;
-};
-__global__ void __launch_bounds__(kThreads) k_col_report(const ColReportArgs a) {
-    if (a.done && *a.done) return;
-    __shared__ double sprod[kCap];
-    __shared__ double sacc[kMaxSeg];
-    __shared__ int32_t sptr[kMaxSeg + 1];
-    __shared__ double sh[32];
-    int c0, nseg;
-    if (a.tile_start) {
-        c0 = a.tile_start[blockIdx.x];
-        nseg = a.tile_start[blockIdx.x + 1] - c0;
-    } else {
-        c0 = blockIdx.x * a.cols_per_tile;
-        nseg = min(a.cols_per_tile, a.n - c0);
-    }
-    for (int s = threadIdx.x; s <= nseg; s += kThreads) sptr[s] = a.colptr[c0 + s];
-    __syncthreads();
-    double nf = 0.0;
-    // same engine as the column pass, with the y/gamma checks in the gather loop
-    {
-        const uint64_t pol_s = policy_evict_first();
-        const int k0 = sptr[0], k1 = sptr[nseg];
-        for (int s = threadIdx.x; s < nseg; s += kThreads) sacc[s] = 0.0;
-        for (int cc = k0; cc < k1; cc += kCap) {
-            const int len = min(kCap, k1 - cc);
-            for (int t = threadIdx.x; t < len; t += kThreads) {
-                const int i = ld_stream(a.rowidx + cc + t, pol_s);
-                const double av = ld_stream(a.val + cc + t, pol_s);
-                const double p = __dmul_rn(av, a.lam[i]);
-                if (!finite(p)) nf = 1.0;
-                if (a.br && !finite(av * a.br[i])) nf = 1.0;
-                sprod[t] = p;
-            }
-            __syncthreads();
-            for (int s = threadIdx.x; s < nseg; s += kThreads) {
-                const int lo = max(sptr[s], cc) - cc;
-                const int hi = min(sptr[s + 1], cc + len) - cc;
-                if (lo < hi) {
-                    double acc = sacc[s];
-                    for (int k = lo; k < hi; ++k) acc = __dadd_rn(acc, sprod[k]);
-                    sacc[s] = acc;
-                }
-            }
-            __syncthreads();
-        }
-    }
-    double d2 = 0.0, dmx = 0.0, s2 = 0.0, smx = 0.0, amx = 0.0, cx = 0.0, cg = 0.0;
-    for (int s = threadIdx.x; s < nseg; s += kThreads) {
-        const int j = c0 + s;
-        const double atl = sacc[s];
-        const double xj = a.x[j], zj = a.z[j], dj = a.delta[j], cj = a.c[j];
-        const double dual = atl + cj;
-        const double stat = dual - dj;
-        d2 = d2 + dual * dual;
-        dmx = nanmax(dmx, fabs(dual));
-        s2 = s2 + stat * stat;
-        smx = nanmax(smx, fabs(stat));
-        amx = nanmax(amx, fabs(atl));
-        cx = cx + cj * xj;
-        cg = nanmax(cg, fabs(xj - zj));
-        if (!finite(xj) || !finite(zj) || !finite(dj)) nf = 1.0;
-    }
-    const int G = gridDim.x;
-    double v;
-    v = block_reduce(d2, sh, SumOp());
-    if (threadIdx.x == 0) a.part[0 * G + blockIdx.x] = v;
-    v = block_reduce(dmx, sh, MaxOp());
-    if (threadIdx.x == 0) a.part[1 * G + blockIdx.x] = v;
-    v = block_reduce(s2, sh, SumOp());
-    if (threadIdx.x == 0) a.part[2 * G + blockIdx.x] = v;
-    v = block_reduce(smx, sh, MaxOp());
-    if (threadIdx.x == 0) a.part[3 * G + blockIdx.x] = v;
-    v = block_reduce(amx, sh, MaxOp());
-    if (threadIdx.x == 0) a.part[4 * G + blockIdx.x] = v;
-    v = block_reduce(cx, sh, SumOp());
-    if (threadIdx.x == 0) a.part[5 * G + blockIdx.x] = v;
-    v = block_reduce(cg, sh, MaxOp());
-    if (threadIdx.x == 0) a.part[6 * G + blockIdx.x] = v;
-    v = block_reduce(nf, sh, MaxOp());
-    if (threadIdx.x == 0) a.part[7 * G + blockIdx.x] = v;
-}
-
 struct FinalizeArgs {
     const double* part_row;
     const double* part_col;
+    const int32_t* nf_flag;  // non-finite implicit y / gamma seen by the report's gather warps
     int32_t g_row;
     int32_t g_col;
     int64_t k;
@@ -554,7 +402,7 @@ __global__ void __launch_bounds__(1024) k_finalize(const FinalizeArgs a) {
     const double blam = f[3];
     r.dobj = -blam;
     r.gap = r.pobj + blam;
-    r.nonfinite = (f[4] > 0.0 || f[12] > 0.0) ? 1 : 0;
+    r.nonfinite = (f[4] > 0.0 || f[12] > 0.0 || (a.nf_flag && *a.nf_flag)) ? 1 : 0;
     int status = r.nonfinite ? CF_STATUS_DIVERGED : CF_STATUS_RUNNING;
     if (a.check && status == CF_STATUS_RUNNING) {
         const cf_config& c = a.cfg;
@@ -639,20 +487,26 @@ __global__ void k_warm_cols(const int32_t* colptr, const int32_t* rowidx, const 
 }
 // rcorr[i] = (sum_{p in row i} a_p eps_{csc(p)}) / mu
 __global__ void k_warm_rows(const int32_t* rowptr, const double* valr, const int32_t* csr2csc, const double* eps,
-                            double mu, double* rcorr, int64_t m) {
+                            double mu, double* rcorr, int64_t m, int32_t panels) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
         double s = 0.0;
-        for (int p = rowptr[i]; p < rowptr[i + 1]; ++p) s = s + valr[p] * eps[csr2csc[p]];
+        for (int32_t pn = 0; pn < panels; ++pn) {
+            const int64_t seg = pn * m + i;
+            for (int p = rowptr[seg]; p < rowptr[seg + 1]; ++p) s = s + valr[p] * eps[csr2csc[p]];
+        }
         rcorr[i] = s / mu;
     }
 }
 
 // fu_i = 1/(1 + sum a^2) (uv.py:81, bincount order = CSR order), db_i = d_i b_i
 __global__ void k_row_diag(const int32_t* rowptr, const double* valr, const double* b, double* fu, double* db,
-                           int64_t m) {
+                           int64_t m, int32_t panels) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
         double d = 0.0;
-        for (int p = rowptr[i]; p < rowptr[i + 1]; ++p) d = d + valr[p] * valr[p];
+        for (int32_t pn = 0; pn < panels; ++pn) {
+            const int64_t seg = pn * m + i;
+            for (int p = rowptr[seg]; p < rowptr[seg + 1]; ++p) d = d + valr[p] * valr[p];
+        }
         fu[i] = 1.0 / (1.0 + d);
         db[i] = d * b[i];
     }
@@ -665,39 +519,71 @@ inline int grid_for(int64_t work, int threads) {
     return (int)g;
 }
 
-RowArgs row_args(cf_plan* p) {
-    RowArgs a{};
-    a.rowptr = p->rowptr.p;
-    a.colidx = p->colidx.p;
-    a.val = p->valr.p;
-    a.x = p->x.p;
-    a.b = p->b.p;
-    a.fu = p->fu.p;
-    a.db = p->db.p;
-    a.lam = p->lam.p;
-    a.h = p->h.p;
-    a.m = (int32_t)p->m;
-    a.rows_per_tile = p->rows_per_tile;
-    return a;
+pass::Tiles row_panel_tiles(const cf_plan* p, int panel) {
+    const int64_t t0 = p->row_panel_tile[panel], t1 = p->row_panel_tile[panel + 1];
+    return pass::Tiles{p->row_tb.p + t0, (int32_t)(t1 - t0)};
 }
-ColArgs col_args(cf_plan* p) {
-    ColArgs a{};
-    a.colptr = p->colptr.p;
-    a.rowidx = p->rowidx.p;
-    a.val = p->valc.p;
-    a.h = p->h.p;
-    a.c = p->c.p;
-    a.x = p->x.p;
-    a.z = p->z.p;
-    a.delta = p->delta.p;
-    a.tile_start = p->all_unit ? nullptr : p->tile_start.p;
-    a.tile_cone = p->tile_cone.p;
-    a.tile_big = p->tile_big.p;
-    a.cone_ptr = p->cone_ptr.p;
-    a.wbuf = p->wbuf.p;
-    a.n = (int32_t)p->n;
-    a.cols_per_tile = p->cols_per_tile;
-    return a;
+pass::Tiles col_tiles(const cf_plan* p) { return pass::Tiles{p->col_tb.p, (int32_t)p->col_tiles}; }
+
+template <class P>
+int persistent_grid(int n_tiles) {
+    static int per_sm = -1;
+    static int sms = 0;
+    if (per_sm < 0) {
+        CF_CUDA(cudaFuncSetAttribute(pass::k_pass<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)pass::kSmemBytes));
+        CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pass::k_pass<P>, pass::kPThreads,
+                                                              pass::kSmemBytes));
+        int dev = 0;
+        CF_CUDA(cudaGetDevice(&dev));
+        CF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        if (per_sm < 1) per_sm = 1;
+    }
+    const int g = per_sm * sms;
+    return n_tiles < g ? (n_tiles > 0 ? n_tiles : 1) : g;
+}
+
+template <class P>
+int launch_pass(const P& pol, const pass::Tiles& T, const int32_t* done, cudaStream_t st, int* grid_out = nullptr) {
+    if (T.n_tiles == 0) return CF_OK;
+    const int grid = persistent_grid<P>(T.n_tiles);
+    if (grid_out) *grid_out = grid;
+    pass::k_pass<P><<<grid, pass::kPThreads, pass::kSmemBytes, st>>>(pol, T, done);
+    CF_LAUNCHED();
+    return CF_OK;
+}
+
+// the row pass of one iteration (or A x): one launch per column panel
+template <class Fill>
+int launch_row_panels(cf_plan* p, const double* g, const int32_t* done, int64_t* nl, Fill fill) {
+    for (int pn = 0; pn < p->n_panels; ++pn) {
+        const pass::Tiles T = row_panel_tiles(p, pn);
+        CF_TRY(fill(pn, T, g, done));
+        if (nl) ++*nl;
+    }
+    return CF_OK;
+}
+
+ColIter col_iter(cf_plan* p) {
+    ColIter c{};
+    c.ptr_ = p->colptr.p;
+    c.idx_ = p->rowidx.p;
+    c.val_ = p->valc.p;
+    c.g_ = p->h.p;
+    c.nvec_ = 4;
+    c.vb_[0] = p->x.p;
+    c.vb_[1] = p->z.p;
+    c.vb_[2] = p->delta.p;
+    c.vb_[3] = p->c.p;
+    c.x = p->x.p;
+    c.z = p->z.p;
+    c.delta = p->delta.p;
+    c.cones = p->all_unit ? 0 : 1;
+    c.tile_cone = p->tile_cone.p;
+    c.tile_big = p->tile_big.p;
+    c.cone_ptr = p->cone_ptr.p;
+    c.wbuf = p->wbuf.p;
+    return c;
 }
 
 }  // namespace
@@ -719,43 +605,61 @@ int launch_iteration(cf_plan* p, const IterOpts& opt, const int32_t* done, int64
         CF_CUDA(cudaEventRecord(e_a, p->stream));
     }
     if (p->n > 0) {
-        ColArgs a = col_args(p);
-        a.vterm = opt.vterm;
-        a.ccorr = opt.ccorr;
-        a.mu = opt.mu;
-        a.done = done;
-        if (p->all_unit) {
-            k_col_pass<0><<<(unsigned)p->col_tiles, kThreads, 0, p->stream>>>(a);
-        } else {
-            k_col_pass<1><<<(unsigned)p->col_tiles, kThreads, 0, p->stream>>>(a);
-            if (p->n_big > 0) {
-                BigConeArgs g{};
-                g.big_cone = p->big_cone.p;
-                g.cone_ptr = p->cone_ptr.p;
-                g.wbuf = p->wbuf.p;
-                g.x = p->x.p;
-                g.z = p->z.p;
-                g.delta = p->delta.p;
-                g.mu = opt.mu;
-                g.done = done;
-                k_big_cone<<<(unsigned)p->n_big, 1024, 0, p->stream>>>(g);
-                ++nl;
-            }
-        }
+        ColIter c = col_iter(p);
+        c.vterm = opt.vterm;
+        c.ccorr = opt.ccorr;
+        c.mu = opt.mu;
+        CF_TRY(launch_pass(c, col_tiles(p), done, p->stream));
         ++nl;
-        CF_LAUNCHED();
+        if (!p->all_unit && p->n_big > 0) {
+            BigConeArgs g{};
+            g.big_cone = p->big_cone.p;
+            g.cone_ptr = p->cone_ptr.p;
+            g.wbuf = p->wbuf.p;
+            g.x = p->x.p;
+            g.z = p->z.p;
+            g.delta = p->delta.p;
+            g.mu = opt.mu;
+            g.done = done;
+            k_big_cone<<<(unsigned)p->n_big, 1024, 0, p->stream>>>(g);
+            CF_LAUNCHED();
+            ++nl;
+        }
     }
     if (p->profiling) CF_CUDA(cudaEventRecord(e_b, p->stream));
     if (p->m > 0) {
-        RowArgs a = row_args(p);
-        a.mu = opt.mu;
-        a.done = done;
-        a.rcorr = opt.rcorr;
-        a.br = (opt.report || p->keep_br) ? p->br.p : nullptr;
-        a.ax = opt.report ? p->ax.p : nullptr;
-        k_row_pass<0><<<(unsigned)p->row_tiles, kThreads, 0, p->stream>>>(a);
-        ++nl;
-        CF_LAUNCHED();
+        const int64_t m = p->m;
+        CF_TRY(launch_row_panels(p, p->x.p, done, &nl, [&](int pn, const pass::Tiles& T, const double* g,
+                                                           const int32_t* dn) {
+            RowIter r{};
+            r.ptr_ = p->rowptr.p;
+            r.idx_ = p->colidx.p;
+            r.val_ = p->valr.p;
+            r.g_ = g;
+            r.seg_off = (int64_t)pn * m;
+            r.last = (pn == p->n_panels - 1);
+            r.carry = p->ax.p;
+            int nv = 0;
+            if (r.last) {
+                r.vb_[0] = p->b.p - r.seg_off;
+                r.vb_[1] = p->lam.p - r.seg_off;
+                r.vb_[2] = p->fu.p - r.seg_off;
+                r.vb_[3] = p->db.p - r.seg_off;
+                nv = 4;
+            }
+            if (pn > 0) {
+                r.vb_[nv++] = p->ax.p - r.seg_off;
+                r.carry_ = true;
+            }
+            r.nvec_ = nv;
+            r.lam = p->lam.p;
+            r.h = p->h.p;
+            r.mu = opt.mu;
+            r.rcorr = opt.rcorr;
+            r.br = (opt.report || p->keep_br) ? p->br.p : nullptr;
+            r.ax = opt.report ? p->ax.p : nullptr;
+            return launch_pass(r, T, dn, p->stream);
+        }));
     }
     if (p->profiling) CF_CUDA(cudaEventRecord(e_c, p->stream));
     if (launches) *launches += nl;
@@ -780,22 +684,34 @@ void prof_collect(cf_plan* p) {
 
 int launch_spmv_rows(cf_plan* p, const double* x, double* y) {
     if (p->m == 0) return CF_OK;
-    RowArgs a = row_args(p);
-    a.x = x;
-    a.ax = y;
-    k_row_pass<1><<<(unsigned)p->row_tiles, kThreads, 0, p->stream>>>(a);
-    CF_LAUNCHED();
-    return CF_OK;
+    const int64_t m = p->m;
+    return launch_row_panels(p, x, nullptr, nullptr, [&](int pn, const pass::Tiles& T, const double* g,
+                                                         const int32_t* dn) {
+        RowSpmv r{};
+        r.ptr_ = p->rowptr.p;
+        r.idx_ = p->colidx.p;
+        r.val_ = p->valr.p;
+        r.g_ = g;
+        r.seg_off = (int64_t)pn * m;
+        r.y = y;
+        if (pn > 0) {
+            r.vb_[0] = y - r.seg_off;
+            r.nvec_ = 1;
+            r.carry_ = true;
+        }
+        return launch_pass(r, T, dn, p->stream);
+    });
 }
 
 int launch_spmv_cols(cf_plan* p, const double* y, double* x) {
     if (p->n == 0) return CF_OK;
-    ColArgs a = col_args(p);
-    a.h = y;
-    a.x = x;
-    k_col_pass<2><<<(unsigned)p->col_tiles, kThreads, 0, p->stream>>>(a);
-    CF_LAUNCHED();
-    return CF_OK;
+    ColSpmv c{};
+    c.ptr_ = p->colptr.p;
+    c.idx_ = p->rowidx.p;
+    c.val_ = p->valc.p;
+    c.g_ = y;
+    c.y = x;
+    return launch_pass(c, col_tiles(p), nullptr, p->stream);
 }
 
 int launch_report(cf_plan* p, double mu, bool ax_ready, const cf_config* cfg, int64_t k, int64_t slot,
@@ -804,7 +720,7 @@ int launch_report(cf_plan* p, double mu, bool ax_ready, const cf_config* cfg, in
     int64_t nl = 0;
     if (!ax_ready) {
         CF_TRY(launch_spmv_rows(p, p->x.p, p->ax.p));
-        ++nl;
+        nl += p->n_panels;
     }
     if (p->m > 0) {
         RowReportArgs a{};
@@ -818,31 +734,31 @@ int launch_report(cf_plan* p, double mu, bool ax_ready, const cf_config* cfg, in
         ++nl;
         CF_LAUNCHED();
     }
+    int g_col = 0;
     if (p->n > 0) {
-        ColReportArgs a{};
-        a.colptr = p->colptr.p;
-        a.rowidx = p->rowidx.p;
-        a.val = p->valc.p;
-        a.lam = p->lam.p;
-        a.br = p->br_valid ? p->br.p : nullptr;
-        a.c = p->c.p;
-        a.x = p->x.p;
-        a.z = p->z.p;
-        a.delta = p->delta.p;
-        a.tile_start = p->all_unit ? nullptr : p->tile_start.p;
-        a.n = (int32_t)p->n;
-        a.cols_per_tile = p->cols_per_tile;
-        a.part = p->part_col.p;
-        a.done = done;
-        k_col_report<<<(unsigned)p->col_tiles, kThreads, 0, p->stream>>>(a);
+        CF_CUDA(cudaMemsetAsync(p->nf_flag.p, 0, 4, p->stream));
+        ColReport c{};
+        c.ptr_ = p->colptr.p;
+        c.idx_ = p->rowidx.p;
+        c.val_ = p->valc.p;
+        c.g_ = p->lam.p;
+        c.nvec_ = 4;
+        c.vb_[0] = p->x.p;
+        c.vb_[1] = p->z.p;
+        c.vb_[2] = p->delta.p;
+        c.vb_[3] = p->c.p;
+        c.br = p->br_valid ? p->br.p : nullptr;
+        c.part = p->part_col.p;
+        c.nf_flag = p->nf_flag.p;
+        CF_TRY(launch_pass(c, col_tiles(p), done, p->stream, &g_col));
         ++nl;
-        CF_LAUNCHED();
     }
     FinalizeArgs f{};
     f.part_row = p->part_row.p;
     f.part_col = p->part_col.p;
+    f.nf_flag = p->nf_flag.p;
     f.g_row = p->m > 0 ? p->row_report_ctas : 0;
-    f.g_col = p->n > 0 ? (int32_t)p->col_tiles : 0;
+    f.g_col = g_col;
     f.k = k;
     f.check = cfg ? 1 : 0;
     if (cfg) f.cfg = *cfg;
@@ -894,7 +810,7 @@ int launch_warm_start(cf_plan* p, double mu) {
     }
     if (p->m > 0) {
         k_warm_rows<<<grid_for(p->m, 128), 128, 0, p->stream>>>(p->rowptr.p, p->valr.p, p->csr2csc.p, p->eps.p, mu,
-                                                                p->rcorr.p, p->m);
+                                                                p->rcorr.p, p->m, p->n_panels);
         CF_LAUNCHED();
     }
     return CF_OK;
@@ -902,9 +818,12 @@ int launch_warm_start(cf_plan* p, double mu) {
 
 int launch_row_diag(cf_plan* p) {
     if (p->m == 0) return CF_OK;
-    k_row_diag<<<grid_for(p->m, 128), 128, 0, p->stream>>>(p->rowptr.p, p->valr.p, p->b.p, p->fu.p, p->db.p, p->m);
+    k_row_diag<<<grid_for(p->m, 128), 128, 0, p->stream>>>(p->rowptr.p, p->valr.p, p->b.p, p->fu.p, p->db.p, p->m,
+                                                          p->n_panels);
     CF_LAUNCHED();
     return CF_OK;
 }
+
+int max_col_report_ctas() { return persistent_grid<ColReport>(1 << 30); }
 
 }  // namespace cf

@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "cf_common.h"
 
@@ -78,14 +79,22 @@ __global__ void k_fill_csc(const uint64_t* keys, const int32_t* perm, const doub
 }
 
 // segment pointers from a sorted segment-id array: ptr[s] = first k with seg_of[k] >= s
-__global__ void k_ptr_from_sorted(const int32_t* seg_of, int64_t o, int64_t nseg, int32_t* ptr) {
+template <class SegT>
+__global__ void k_ptr_from_sorted(const SegT* seg_of, int64_t o, int64_t nseg, int32_t* ptr) {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < o; k += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t s = seg_of[k];
-        const int64_t sp = (k == 0) ? -1 : seg_of[k - 1];
+        const int64_t s = (int64_t)seg_of[k];
+        const int64_t sp = (k == 0) ? (int64_t)-1 : (int64_t)seg_of[k - 1];
         for (int64_t t = sp + 1; t <= s; ++t) ptr[t] = (int32_t)k;
         if (k == o - 1)
             for (int64_t t = s + 1; t <= nseg; ++t) ptr[t] = (int32_t)o;
     }
+}
+
+// row-pass segment of each canonical entry: panel(col) * m + row
+__global__ void k_row_keys(const int32_t* rowidx, const int32_t* colof, int64_t o, int64_t m, int64_t panel_cols,
+                           uint64_t* keys) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < o; k += (int64_t)gridDim.x * blockDim.x)
+        keys[k] = (uint64_t)(colof[k] / panel_cols) * (uint64_t)m + (uint64_t)rowidx[k];
 }
 
 __global__ void k_iota(int32_t* v, int64_t len) {
@@ -115,70 +124,102 @@ inline int bits_for(uint64_t maxval) {
     return b;
 }
 
-int pick_tile(double avg_nnz) {
-    const double target = 0.75 * kCap;
-    int t = (int)(target / std::max(avg_nnz, 1e-9));
-    t = std::max(32, std::min(kMaxSeg, t));
-    return (t / 32) * 32;
+// Greedy tiles over segments [0, nseg) of a compressed layout: a tile takes
+// consecutive units (a unit = one segment, or one whole cone of <= kSmallCone
+// columns) while it stays within kTileSeg segments and kTileNnz nonzeros; a
+// unit that alone exceeds the nonzero budget gets a tile of its own (the
+// engine streams it in chunks). Cones wider than kSmallCone are cut into
+// pieces of their own, flagged for k_big_cone.
+void tile_segments(const std::vector<int32_t>& ptr, int64_t s_begin, int64_t s_end, std::vector<int2>& tb,
+                   std::vector<int32_t>* tcone, std::vector<int32_t>* tbig, int32_t cone, int32_t bigid) {
+    int64_t s = s_begin;
+    while (s < s_end) {
+        int64_t e = s + 1;
+        while (e < s_end && e - s < kTileSeg && ptr[e + 1] - ptr[s] <= kTileNnz) ++e;
+        tb.push_back(make_int2((int)s, ptr[s]));
+        if (tcone) tcone->push_back(cone);
+        if (tbig) tbig->push_back(bigid);
+        s = e;
+    }
 }
 
-// Column tiles aligned to cone boundaries (cones.py:39-59 offsets). A tile
-// holds whole cones of size <= kSmallCone up to `cap` columns; a bigger cone
-// is split over its own tiles and projected by k_big_cone.
-int build_cone_tiles(cf_plan* p, const int64_t* sizes, int64_t nb) {
-    int cap = p->cols_per_tile;
-    for (int64_t q = 0; q < nb; ++q)
-        if (sizes[q] <= kSmallCone) cap = std::max<int>(cap, (int)sizes[q]);
-    p->cols_per_tile = cap;
-    std::vector<int32_t> cone_ptr(nb + 1), ts, tc, tb, big;
-    int64_t col = 0;
-    for (int64_t q = 0; q < nb; ++q) {
-        cone_ptr[q] = (int32_t)col;
-        col += sizes[q];
-    }
-    cone_ptr[nb] = (int32_t)col;
-    int64_t q = 0;
-    col = 0;
-    while (q < nb) {
-        if (sizes[q] > kSmallCone) {
-            const int32_t id = (int32_t)big.size();
-            big.push_back((int32_t)q);
-            for (int64_t s = 0; s < sizes[q]; s += cap) {
-                ts.push_back((int32_t)(col + s));
-                tc.push_back((int32_t)q);
-                tb.push_back(id);
-            }
-            col += sizes[q];
-            ++q;
-        } else {
-            ts.push_back((int32_t)col);
-            tc.push_back((int32_t)q);
-            tb.push_back(-1);
-            int64_t cols = 0;
-            while (q < nb && sizes[q] <= kSmallCone && cols + sizes[q] <= cap) {
-                cols += sizes[q];
-                ++q;
-            }
-            col += cols;
-        }
-    }
-    ts.push_back((int32_t)col);
-    tc.push_back((int32_t)nb);
-    p->col_tiles = (int64_t)ts.size() - 1;
-    p->n_big = (int64_t)big.size();
-    CF_TRY(p->cone_ptr.alloc(nb + 1));
-    CF_TRY(p->tile_start.alloc(ts.size()));
-    CF_TRY(p->tile_cone.alloc(tc.size()));
-    CF_TRY(p->tile_big.alloc(tb.size()));
-    CF_TRY(p->big_cone.alloc(std::max<size_t>(1, big.size())));
-    CF_CUDA(cudaMemcpyAsync(p->cone_ptr.p, cone_ptr.data(), cone_ptr.size() * 4, cudaMemcpyHostToDevice, p->stream));
-    CF_CUDA(cudaMemcpyAsync(p->tile_start.p, ts.data(), ts.size() * 4, cudaMemcpyHostToDevice, p->stream));
-    CF_CUDA(cudaMemcpyAsync(p->tile_cone.p, tc.data(), tc.size() * 4, cudaMemcpyHostToDevice, p->stream));
-    CF_CUDA(cudaMemcpyAsync(p->tile_big.p, tb.data(), tb.size() * 4, cudaMemcpyHostToDevice, p->stream));
-    if (!big.empty())
-        CF_CUDA(cudaMemcpyAsync(p->big_cone.p, big.data(), big.size() * 4, cudaMemcpyHostToDevice, p->stream));
-    // the host vectors die at return: make the copies complete first
+int build_tiles(cf_plan* p, const int64_t* sizes, int64_t nb) {
+    const int64_t m = p->m, n = p->n;
+    std::vector<int32_t> rp((int64_t)p->n_panels * m + 1), cp(n + 1);
+    CF_CUDA(cudaMemcpyAsync(rp.data(), p->rowptr.p, rp.size() * 4, cudaMemcpyDeviceToHost, p->stream));
+    CF_CUDA(cudaMemcpyAsync(cp.data(), p->colptr.p, (n + 1) * 4, cudaMemcpyDeviceToHost, p->stream));
     CF_CUDA(cudaStreamSynchronize(p->stream));
+    // rows, panel by panel (segment = panel*m + row)
+    const int64_t nsr = (int64_t)p->n_panels * m;
+    std::vector<int2> rtb;
+    p->row_panel_tile.assign(p->n_panels + 1, 0);
+    for (int pn = 0; pn < p->n_panels; ++pn) {
+        p->row_panel_tile[pn] = (int64_t)rtb.size();
+        tile_segments(rp, (int64_t)pn * m, (int64_t)(pn + 1) * m, rtb, nullptr, nullptr, 0, -1);
+    }
+    p->row_panel_tile[p->n_panels] = (int64_t)rtb.size();
+    rtb.push_back(make_int2((int)nsr, rp[nsr]));
+    p->row_tiles = (int64_t)rtb.size() - 1;
+    // columns
+    std::vector<int2> ctb;
+    std::vector<int32_t> tcone, tbig, big, cone_ptr;
+    if (p->all_unit) {
+        tile_segments(cp, 0, n, ctb, nullptr, nullptr, 0, -1);
+    } else {
+        cone_ptr.resize(nb + 1);
+        int64_t col = 0;
+        for (int64_t q = 0; q < nb; ++q) {
+            cone_ptr[q] = (int32_t)col;
+            col += sizes[q];
+        }
+        cone_ptr[nb] = (int32_t)col;
+        int64_t q = 0;
+        while (q < nb) {
+            const int64_t c0 = cone_ptr[q];
+            if (sizes[q] > kSmallCone) {
+                tile_segments(cp, c0, c0 + sizes[q], ctb, &tcone, &tbig, (int32_t)q, (int32_t)big.size());
+                big.push_back((int32_t)q);
+                ++q;
+                continue;
+            }
+            int64_t q1 = q + 1;
+            while (q1 < nb && sizes[q1] <= kSmallCone && cone_ptr[q1] + sizes[q1] - c0 <= kTileSeg &&
+                   cp[cone_ptr[q1] + sizes[q1]] - cp[c0] <= kTileNnz)
+                ++q1;
+            ctb.push_back(make_int2((int)c0, cp[c0]));
+            tcone.push_back((int32_t)q);
+            tbig.push_back(-1);
+            q = q1;
+        }
+        tcone.push_back((int32_t)nb);
+    }
+    ctb.push_back(make_int2((int)n, cp[n]));
+    p->col_tiles = (int64_t)ctb.size() - 1;
+    p->n_big = (int64_t)big.size();
+    CF_TRY(p->row_tb.alloc(rtb.size()));
+    CF_TRY(p->col_tb.alloc(ctb.size()));
+    CF_CUDA(cudaMemcpyAsync(p->row_tb.p, rtb.data(), rtb.size() * sizeof(int2), cudaMemcpyHostToDevice, p->stream));
+    CF_CUDA(cudaMemcpyAsync(p->col_tb.p, ctb.data(), ctb.size() * sizeof(int2), cudaMemcpyHostToDevice, p->stream));
+    if (p->all_unit) {
+        CF_TRY(p->tile_big.alloc(1));
+        CF_TRY(p->tile_cone.alloc(1));
+        CF_TRY(p->cone_ptr.alloc(1));
+        CF_TRY(p->big_cone.alloc(1));
+    } else {
+        CF_TRY(p->cone_ptr.alloc(cone_ptr.size()));
+        CF_TRY(p->tile_cone.alloc(tcone.size()));
+        CF_TRY(p->tile_big.alloc(std::max<size_t>(1, tbig.size())));
+        CF_TRY(p->big_cone.alloc(std::max<size_t>(1, big.size())));
+        CF_CUDA(cudaMemcpyAsync(p->cone_ptr.p, cone_ptr.data(), cone_ptr.size() * 4, cudaMemcpyHostToDevice,
+                                p->stream));
+        CF_CUDA(cudaMemcpyAsync(p->tile_cone.p, tcone.data(), tcone.size() * 4, cudaMemcpyHostToDevice, p->stream));
+        if (!tbig.empty())
+            CF_CUDA(cudaMemcpyAsync(p->tile_big.p, tbig.data(), tbig.size() * 4, cudaMemcpyHostToDevice, p->stream));
+        if (!big.empty())
+            CF_CUDA(cudaMemcpyAsync(p->big_cone.p, big.data(), big.size() * 4, cudaMemcpyHostToDevice, p->stream));
+        if (p->n_big) CF_TRY(p->wbuf.alloc(n));
+    }
+    CF_CUDA(cudaStreamSynchronize(p->stream));  // host vectors die at return
     return CF_OK;
 }
 
@@ -233,7 +274,19 @@ int build(cf_plan* p, const int64_t* rows, const int64_t* cols, const double* va
     CF_TRY(p->colptr.alloc(n + 1));
     CF_TRY(p->rowidx.alloc(o));
     CF_TRY(p->valc.alloc(o));
-    CF_TRY(p->rowptr.alloc(m + 1));
+    // column panels of the row pass: each panel's slice of x must stay L2-resident
+    {
+        double panel_mb = 48.0;
+        if (const char* env = getenv("CF_PANEL_MB")) panel_mb = atof(env);
+        const double xbytes = 8.0 * (double)n;
+        int panels = (int)std::ceil(xbytes / (panel_mb * 1048576.0));
+        if (panels < 1) panels = 1;
+        if (panels > 64) panels = 64;
+        if ((int64_t)panels * m >= (int64_t)INT32_MAX) panels = 1;  // tile segment ids are int32
+        p->n_panels = panels;
+        p->panel_cols = std::max<int64_t>(1, (n + panels - 1) / panels);
+    }
+    CF_TRY(p->rowptr.alloc((size_t)p->n_panels * m + 1));
     CF_TRY(p->colidx.alloc(o));
     CF_TRY(p->valr.alloc(o));
     CF_TRY(p->csr2csc.alloc(o));
@@ -270,28 +323,26 @@ int build(cf_plan* p, const int64_t* rows, const int64_t* cols, const double* va
             return CF_EPROBLEM;
         }
         CF_CUDA(cudaMemsetAsync(p->colptr.p, 0, (n + 1) * 4, st));
-        k_ptr_from_sorted<<<grid1d(o), 256, 0, st>>>(colof.p, o, n, p->colptr.p);
+        k_ptr_from_sorted<int32_t><<<grid1d(o), 256, 0, st>>>(colof.p, o, n, p->colptr.p);
         CF_LAUNCHED();
 
-        // ---- CSR: stable sort of canonical entries by row
-        cub::DoubleBuffer<uint32_t> rb(reinterpret_cast<uint32_t*>(i_a.p), reinterpret_cast<uint32_t*>(i_b.p));
-        CF_CUDA(cudaMemcpyAsync(rb.Current(), p->rowidx.p, o * 4, cudaMemcpyDeviceToDevice, st));
-        // k_a / k_b reused as int32 scratch for the permutation
-        int32_t* pa = reinterpret_cast<int32_t*>(k_a.p);
-        int32_t* pb = reinterpret_cast<int32_t*>(k_b.p);
-        k_iota<<<grid1d(o), 256, 0, st>>>(pa, o);
+        // ---- CSR panels: stable sort of canonical entries by (column panel, row); inside a
+        //      segment the entries keep canonical (column) order
+        const int64_t nseg_rows = (int64_t)p->n_panels * m;
+        CF_CUDA(cudaMemsetAsync(p->rowptr.p, 0, (nseg_rows + 1) * 4, st));
+        k_row_keys<<<grid1d(o), 256, 0, st>>>(p->rowidx.p, colof.p, o, m, p->panel_cols, k_a.p);
+        k_iota<<<grid1d(o), 256, 0, st>>>(i_a.p, o);
         CF_LAUNCHED();
-        cub::DoubleBuffer<int32_t> pbuf(pa, pb);
-        const int row_bits = bits_for((uint64_t)std::max<int64_t>(m - 1, 1));
+        cub::DoubleBuffer<uint64_t> rb(k_a.p, k_b.p);
+        cub::DoubleBuffer<int32_t> pbuf(i_a.p, i_b.p);
+        const int row_bits = bits_for((uint64_t)std::max<int64_t>(nseg_rows - 1, 1));
         size_t tmp2 = 0;
         CF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp2, rb, pbuf, (int64_t)o, 0, row_bits, st));
         if (tmp2 > tmp_bytes) CF_TRY(tmp.alloc(tmp2));
         CF_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp2, rb, pbuf, (int64_t)o, 0, row_bits, st));
         CF_CUDA(cudaMemcpyAsync(p->csr2csc.p, pbuf.Current(), o * 4, cudaMemcpyDeviceToDevice, st));
         k_fill_csr<<<grid1d(o), 256, 0, st>>>(p->csr2csc.p, colof.p, p->valc.p, o, p->colidx.p, p->valr.p);
-        CF_CUDA(cudaMemsetAsync(p->rowptr.p, 0, (m + 1) * 4, st));
-        k_ptr_from_sorted<<<grid1d(o), 256, 0, st>>>(reinterpret_cast<const int32_t*>(rb.Current()), o, m,
-                                                     p->rowptr.p);
+        k_ptr_from_sorted<uint64_t><<<grid1d(o), 256, 0, st>>>(rb.Current(), o, nseg_rows, p->rowptr.p);
         CF_LAUNCHED();
         CF_CUDA(cudaStreamSynchronize(st));  // scratch buffers are released at scope exit
     } else {
@@ -300,7 +351,7 @@ int build(cf_plan* p, const int64_t* rows, const int64_t* cols, const double* va
             return CF_EPROBLEM;
         }
         CF_CUDA(cudaMemsetAsync(p->colptr.p, 0, (n + 1) * 4, st));
-        CF_CUDA(cudaMemsetAsync(p->rowptr.p, 0, (m + 1) * 4, st));
+        CF_CUDA(cudaMemsetAsync(p->rowptr.p, 0, ((int64_t)p->n_panels * m + 1) * 4, st));
     }
 
     // ---- cached diagonals (uv.py:81-82; fv is recomputed in-kernel from colptr)
@@ -308,23 +359,12 @@ int build(cf_plan* p, const int64_t* rows, const int64_t* cols, const double* va
     CF_TRY(p->db.alloc(m));
     CF_TRY(launch_row_diag(p));
 
-    // ---- tiles
-    p->rows_per_tile = pick_tile(m ? (double)o / (double)m : 1.0);
-    p->cols_per_tile = pick_tile(n ? (double)o / (double)n : 1.0);
-    p->row_tiles = (m + p->rows_per_tile - 1) / p->rows_per_tile;
+    // ---- cones (cones.py:39-59) and tiles
     p->n_blocks = nb;
     int64_t maxsize = 0;
     for (int64_t q = 0; q < nb; ++q) maxsize = std::max(maxsize, sizes[q]);
     p->all_unit = (nb == 0 || maxsize == 1);
-    if (p->all_unit) {
-        p->col_tiles = (n + p->cols_per_tile - 1) / p->cols_per_tile;
-        CF_TRY(p->tile_big.alloc(1));
-        CF_TRY(p->tile_cone.alloc(1));
-        CF_TRY(p->cone_ptr.alloc(1));
-    } else {
-        CF_TRY(build_cone_tiles(p, sizes, nb));
-        if (p->n_big) CF_TRY(p->wbuf.alloc(n));
-    }
+    CF_TRY(build_tiles(p, sizes, nb));
 
     // ---- iterate state (SolverState.zeros, solver.py:118-127) and report buffers
     CF_TRY(p->x.alloc(n));
@@ -342,10 +382,12 @@ int build(cf_plan* p, const int64_t* rows, const int64_t* cols, const double* va
     CF_CUDA(cudaMemsetAsync(p->br.p, 0, std::max<int64_t>(m, 1) * 8, st));
     p->row_report_ctas = (int32_t)std::min<int64_t>(std::max<int64_t>((m + 255) / 256, 1), 148 * 4);
     CF_TRY(p->part_row.alloc((size_t)kReportFieldsRow * p->row_report_ctas));
-    CF_TRY(p->part_col.alloc((size_t)kReportFieldsCol * std::max<int64_t>(p->col_tiles, 1)));
+    CF_TRY(p->part_col.alloc((size_t)kReportFieldsCol * std::max(max_col_report_ctas(), 1)));
     p->host_ring = 64;
     CF_TRY(p->report_slot.alloc(p->host_ring));
     CF_TRY(p->done.alloc(1));
+    CF_TRY(p->nf_flag.alloc(1));
+    CF_CUDA(cudaMemsetAsync(p->nf_flag.p, 0, 4, st));
     CF_CUDA(cudaMemsetAsync(p->done.p, 0, 4, st));
     CF_CUDA(cudaMallocHost(&p->host_reports, p->host_ring * sizeof(cf_report)));
     CF_CUDA(cudaEventCreate(&p->ev0));

@@ -121,7 +121,7 @@ def test_big_cone_projection():
     p = ProblemInstance(TripletMatrix(1, n, [0], [0], [1.0]), [1.0], np.zeros(n), ConeSpec(sizes))
     want = oracle.project_product(sizes, w)
     with _plan(p) as plan:
-        assert plan.info()["big_cones"] == 3
+        assert plan.info()["big_cones"] == 4  # cones wider than kSmallCone=256
         out = torch.empty(n, dtype=torch.float64, device="cuda")
         plan.project(_device_vec(w).data_ptr(), out.data_ptr())
         assert rel_err(out.cpu().numpy(), want) <= 1e-13
@@ -309,3 +309,32 @@ def test_reference_types_accepted():
     assert res.report.status == "solved"
     np.testing.assert_allclose(res.x, [1.0, 0.0], atol=1e-6)
     np.testing.assert_allclose(res.lam, [-1.0], atol=1e-6)
+
+
+def test_row_panels_bit_identical(monkeypatch):
+    """Column panels of the row pass (CF_PANEL_MB) keep A x bit-identical and the iterates unchanged."""
+    import torch
+
+    monkeypatch.setenv("CF_PANEL_MB", "0.002")  # 2 KB of x per panel -> several panels
+    d = load_golden("iterates_lp_mu1.npz")
+    p = problem_from(d)
+    f = oracle.build_factors(p.A)
+    x = np.random.default_rng(5).standard_normal(f.n)
+    with _plan(p) as plan:
+        ax = torch.empty(f.m, dtype=torch.float64, device="cuda")
+        plan.apply_A(_device_vec(x).data_ptr(), ax.data_ptr())
+        np.testing.assert_array_equal(ax.cpu().numpy(), oracle.apply_U(f, oracle.apply_Vt(f, x)))
+        plan.set_state(1.0, None)
+        plan.iterate(1.0, 100)
+        st = plan.get_state()
+    for key in STATE_KEYS:
+        assert rel_err(st[key], d[f"k100_{key}"]) <= ITER_TOL, key
+    from paper_2203_05027_b200 import GenSpec, SolverConfig, generate, solve
+
+    q = generate(GenSpec(300, 900, 0.02, "lp", seed=8))
+    cfg = SolverConfig(max_iters=600)
+    res = solve(q, cfg)
+    monkeypatch.setenv("CF_PANEL_MB", "1000")
+    ref = solve(q, cfg)
+    np.testing.assert_array_equal(res.x, ref.x)
+    assert res.trace == ref.trace
