@@ -15,7 +15,7 @@ from ctypes import POINTER, Structure, c_char_p, c_double, c_int, c_int32, c_int
 __all__ = ["lib", "LIB_PATH", "CfConfig", "CfReport", "CfChecks", "check", "CfError",
            "STATUS_NAMES", "TERM_MODES"]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcfb200.so")
+LIB_PATH = os.environ.get("CF_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcfb200.so")
 
 CF_OK, CF_EINVAL, CF_ECUDA, CF_ENOMEM, CF_EPROBLEM, CF_ESTATE = range(6)
 STATUS_NAMES = ("running", "solved", "max_iters", "diverged")

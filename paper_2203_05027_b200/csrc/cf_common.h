@@ -16,9 +16,11 @@ namespace cf {
 constexpr int kThreads = 256;     // threads of the simple (non-pass) kernels
 constexpr int kTileNnz = 2048;    // nonzeros per tile (= pass::kPCap)
 constexpr int kTileSeg = 256;     // rows / columns per tile (= pass::kPSeg)
+constexpr int kTileDiag = 256;    // longest segment inside a multi-segment tile (= pass::kMaxDiag)
 constexpr int kSmallCone = 256;   // cones up to this size are projected inside the column tile
 constexpr int kReportFieldsRow = 5;
 constexpr int kReportFieldsCol = 8;
+constexpr int kMaxGroups = 4;     // upper bound of pass::kGroups (partial buffer sizing)
 
 // ---------------------------------------------------------------- errors
 void set_error(const std::string& msg);
@@ -99,7 +101,11 @@ struct cf_plan {
     cf::DevBuf<int32_t> tile_big;      // big-cone id of a tile, -1 otherwise
     cf::DevBuf<int32_t> big_cone;      // cone index of each big cone
     int64_t n_big = 0;
-    cf::DevBuf<int2> row_tb, col_tb;   // tile boundaries {first segment, first nonzero}
+    cf::DevBuf<int4> row_tb, col_tb;   // tile table {first segment, first nonzero, first joff, maxlen}
+    // jagged-diagonal copies of the CSR panels (rj_*) and of the CSC (cj_*) read by the passes
+    cf::DevBuf<int32_t> rj_idx, cj_idx;
+    cf::DevBuf<double> rj_val, cj_val;
+    cf::DevBuf<uint16_t> rj_perm, cj_perm, rj_joff, cj_joff;
     int64_t row_tiles = 0, col_tiles = 0;
     // row-pass column panels: the CSR is stored panel-major (segment = panel*m + row)
     // so each row-pass launch gathers only one panel's slice of x (L2-resident)

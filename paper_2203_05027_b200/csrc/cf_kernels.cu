@@ -73,32 +73,30 @@ __device__ __forceinline__ void project_block_dev(const double* w, int q, double
     }
 }
 
+using pass::kComputeThreads;
 using pass::kPSeg;
-using pass::kReduceThreads;
-using pass::rtid;
 using pass::Smem;
 using pass::Stage;
 
 // ---------------------------------------------------------------- pass policies
-// Common layout accessors. Staged vectors are indexed by segment: for a row
-// panel p the segments are p*m + i, so vector bases are shifted by -seg_off.
+// Staged vectors are indexed by segment: for a row panel p the segments are
+// p*m + i, so vector bases are shifted by -seg_off.
 struct Layout {
-    const int32_t* ptr_;
-    const int32_t* idx_;
-    const double* val_;
     const double* g_;
     int32_t nvec_ = 0;
     bool carry_ = false;
     const double* vb_[pass::kPVecs] = {nullptr, nullptr, nullptr, nullptr, nullptr};
-    __device__ const int32_t* ptr() const { return ptr_; }
-    __device__ const int32_t* idx() const { return idx_; }
-    __device__ const double* val() const { return val_; }
-    __device__ const double* gvec() const { return g_; }
-    __device__ int nvec() const { return nvec_; }
-    __device__ const double* vec(int v) const { return vb_[v]; }
-    __device__ bool carry_in() const { return carry_; }
-    __device__ void check(double, int, double) {}
-    __device__ void finish(Smem&) {}
+    static constexpr bool kGroupEpilogue = false;
+    static constexpr int kUnroll = pass::kUnroll;   // gathers in flight per thread
+    __device__ __forceinline__ const double* gvec() const { return g_; }
+    __device__ __forceinline__ int nvec() const { return nvec_; }
+    __device__ __forceinline__ const double* vec(int v) const { return vb_[v]; }
+    __device__ __forceinline__ bool carry_in() const { return carry_; }
+    const double* carry_src_ = nullptr;   // global base of the carried partial (last staged vector)
+    __device__ __forceinline__ const double* carry_src() const { return carry_src_; }
+    __device__ __forceinline__ void check(double, int, double) {}
+    __device__ __forceinline__ void group(Smem&, Stage&, int, int, int, const double* const*) {}
+    __device__ __forceinline__ void finish(Smem&) {}
 };
 
 // Row pass of the iteration: y_update + lam/gamma of dual_update (solver.py:179-183,
@@ -115,27 +113,25 @@ struct RowIter : Layout {
     double* ax;            // optional: A x (report iterations)
     const double* rcorr;   // optional: warm-start U eps / mu
     double mu;
-    __device__ void epilogue(Smem& sm, Stage&, int, int s0, int nseg, const int32_t*, const double* const* vb) {
-        const uint64_t pl = pass::pol_last(), pf = pass::pol_first();
-        for (int q = rtid(); q < nseg; q += kReduceThreads) {
-            const int64_t i = s0 + q - seg_off;
-            const double axi = sm.acc[q];
-            if (!last) {
-                carry[i] = axi;
-                continue;
-            }
-            const double bi = vb[0][q], li = vb[1][q], fui = vb[2][q], dbi = vb[3][q];
-            double si = dbi + axi;                  // (U t)_i with t = a b + x
-            if (rcorr) si = si - rcorr[i];
-            const double r = fui * si;              // r = U y+ = fu (U t)
-            const double ln = li + mu * (r - bi);   // solver.py:194
-            const double bmr = bi - r;
-            const double hi = bmr - ln / mu;        // h = b - r - lam+/mu
-            pass::st_hint(lam + i, ln, pf);
-            pass::st_hint(h + i, hi, pl);           // gathered by the next column pass
-            if (br) br[i] = bmr;
-            if (ax) ax[i] = axi;
+    pass::MuDiv div;
+    __device__ __forceinline__ void segment(Smem&, Stage&, int, int s0, int q, int, double axi, const double* const* vb) {
+        const int64_t i = s0 + q - seg_off;
+        if (!last) {
+            carry[i] = axi;
+            return;
         }
+        const double bi = vb[0][q], li = vb[1][q], fui = vb[2][q], dbi = vb[3][q];
+        double si = dbi + axi;                  // (U t)_i with t = a b + x
+        if (rcorr) si = si - rcorr[i];
+        const double r = fui * si;              // r = U y+ = fu (U t)
+        const double ln = li + mu * (r - bi);   // solver.py:194
+        const double bmr = bi - r;
+        const double hi = bmr - div(ln);        // h = b - r - lam+/mu
+        // on report iterations (ax != null) lam is gathered next by the report's A^T lam pass
+        pass::st_hint(lam + i, ln, ax ? pass::pol_last() : pass::pol_first());
+        pass::st_hint(h + i, hi, pass::pol_last());   // gathered by the next column pass
+        if (br) br[i] = bmr;
+        if (ax) ax[i] = axi;
     }
 };
 
@@ -143,83 +139,83 @@ struct RowIter : Layout {
 struct RowSpmv : Layout {
     int64_t seg_off;
     double* y;
-    __device__ void epilogue(Smem& sm, Stage&, int, int s0, int nseg, const int32_t*, const double* const*) {
-        for (int q = rtid(); q < nseg; q += kReduceThreads) y[s0 + q - seg_off] = sm.acc[q];
+    __device__ __forceinline__ void segment(Smem&, Stage&, int, int s0, int q, int, double acc, const double* const*) {
+        y[s0 + q - seg_off] = acc;
     }
 };
 
 // x = A^T y (apply_V . apply_Ut)
 struct ColSpmv : Layout {
     double* y;
-    __device__ void epilogue(Smem& sm, Stage&, int, int s0, int nseg, const int32_t*, const double* const*) {
-        for (int q = rtid(); q < nseg; q += kReduceThreads) y[s0 + q] = sm.acc[q];
+    __device__ __forceinline__ void segment(Smem&, Stage&, int, int s0, int q, int, double acc, const double* const*) {
+        y[s0 + q] = acc;
     }
 };
 
 // Column pass of the iteration: x_update (solver.py:168-176) in the reduced form
 // V(y + gamma/mu) = cnt*x + A^T h, then z = Proj_K(x+ - delta/mu), delta update.
+// CONES=false: all blocks of size 1 (cones.py:108-109 shortcut), fused per column.
+// CONES=true : x+ and w per column, then (group epilogue) one thread per cone.
+template <bool CONES>
 struct ColIter : Layout {
+    static constexpr bool kGroupEpilogue = CONES;
     double* x;
     double* z;
     double* delta;
     const double* vterm;   // optional: V(y0 + gamma0/mu) (first warm iteration)
     const double* ccorr;   // optional: V eps / mu (second warm iteration)
-    int32_t cones;         // 0 = all blocks of size 1 (cones.py:108-109 shortcut)
     const int32_t* tile_cone;
     const int32_t* tile_big;
     const int32_t* cone_ptr;
     double* wbuf;
     double mu;
-    __device__ void epilogue(Smem& sm, Stage& st, int tile, int s0, int nseg, const int32_t* ptrb,
-                             const double* const* vb) {
-        const uint64_t pl = pass::pol_last(), pf = pass::pol_first();
-        // the staged index buffer is free after the gather phase: cone scratch
-        double* sxp = reinterpret_cast<double*>(st.idx);
-        double* sw = sxp + kPSeg;
-        double* sdn = sxp + 2 * kPSeg;
-        for (int q = rtid(); q < nseg; q += kReduceThreads) {
-            const int j = s0 + q;
-            const int cnt = ptrb[q + 1] - ptrb[q];
-            const double fv = 1.0 / (1.0 + (double)cnt);   // uv.py:82
-            const double xj = vb[0][q], zj = vb[1][q], dj = vb[2][q], cj = vb[3][q];
-            const double dm = dj / mu;
-            double v = vterm ? vterm[j] : __dadd_rn(__dmul_rn((double)cnt, xj), sm.acc[q]);
-            if (ccorr) v = v - ccorr[j];
-            const double xp = fv * (((v + zj) + dm) - cj / mu);   // solver.py:171-176 operand order
-            const double w = xp - dm;                            // solver.py:188
-            if (!cones) {
-                const double zp = w > 0.0 ? w : 0.0;             // NaN -> 0, -0 -> +0
-                const double dp = dj + mu * (zp - xp);           // solver.py:196
-                pass::st_hint(x + j, xp, pl);                    // gathered by the next row pass
-                pass::st_hint(z + j, zp, pf);
-                pass::st_hint(delta + j, dp, pf);
-            } else {
-                sxp[q] = xp;
-                sw[q] = w;
-            }
+    pass::MuDiv div;
+    __device__ __forceinline__ void segment(Smem& sm, Stage&, int, int s0, int q, int cnt, double ath, const double* const* vb) {
+        const int j = s0 + q;
+        const double fv = cnt < pass::kFvTab ? sm.fvtab[cnt] : 1.0 / (1.0 + (double)cnt);   // uv.py:82
+        const double xj = vb[0][q], zj = vb[1][q], dj = vb[2][q], cj = vb[3][q];
+        const double dm = div(dj);
+        double v = vterm ? vterm[j] : __dadd_rn(__dmul_rn((double)cnt, xj), ath);
+        if (ccorr) v = v - ccorr[j];
+        const double xp = fv * (((v + zj) + dm) - div(cj));   // solver.py:171-176 operand order
+        const double w = xp - dm;                            // solver.py:188
+        if (!CONES) {
+            const double zp = w > 0.0 ? w : 0.0;             // NaN -> 0, -0 -> +0
+            const double dp = dj + mu * (zp - xp);           // solver.py:196
+            pass::st_hint(x + j, xp, pass::pol_last());      // gathered by the next row pass
+            pass::st_hint(z + j, zp, pass::pol_first());
+            pass::st_hint(delta + j, dp, pass::pol_first());
+        } else {
+            sm.cscr[pass::group_id()][0][q] = xp;
+            sm.cscr[pass::group_id()][1][q] = w;
         }
-        if (!cones) return;
-        pass::reducer_sync();
+    }
+    __device__ __forceinline__ void group(Smem& sm, Stage&, int tile, int s0, int nseg, const double* const* vb) {
+        const int gi = pass::group_id();
+        const double* sxp = sm.cscr[gi][0];
+        const double* sw = sm.cscr[gi][1];
+        double* sdn = sm.cscr[gi][2];
+        double* szp = sm.acc[gi];
+        const int t = pass::group_tid();
         const int big = tile_big[tile];
         if (big >= 0) {  // piece of a cone wider than a tile: k_big_cone projects it
-            for (int q = rtid(); q < nseg; q += kReduceThreads) {
-                pass::st_hint(x + s0 + q, sxp[q], pl);
+            for (int q = t; q < nseg; q += kComputeThreads) {
+                pass::st_hint(x + s0 + q, sxp[q], pass::pol_last());
                 wbuf[s0 + q] = sw[q];
             }
             return;
         }
-        double* szp = sm.acc;  // A^T h no longer needed
         const int q0 = tile_cone[tile], q1 = tile_cone[tile + 1];
-        for (int q = q0 + rtid(); q < q1; q += kReduceThreads) {
-            const int off = cone_ptr[q] - s0, size = cone_ptr[q + 1] - cone_ptr[q];
+        for (int c = q0 + t; c < q1; c += kComputeThreads) {
+            const int off = cone_ptr[c] - s0, size = cone_ptr[c + 1] - cone_ptr[c];
             project_block_dev(sw + off, size, szp + off);
-            for (int t = 0; t < size; ++t) sdn[off + t] = vb[2][off + t] + mu * (szp[off + t] - sxp[off + t]);
+            for (int u = 0; u < size; ++u) sdn[off + u] = vb[2][off + u] + mu * (szp[off + u] - sxp[off + u]);
         }
-        pass::reducer_sync();
-        for (int q = rtid(); q < nseg; q += kReduceThreads) {
-            pass::st_hint(x + s0 + q, sxp[q], pl);
-            pass::st_hint(z + s0 + q, szp[q], pf);
-            pass::st_hint(delta + s0 + q, sdn[q], pf);
+        pass::group_sync();
+        for (int q = t; q < nseg; q += kComputeThreads) {
+            pass::st_hint(x + s0 + q, sxp[q], pass::pol_last());
+            pass::st_hint(z + s0 + q, szp[q], pass::pol_first());
+            pass::st_hint(delta + s0 + q, sdn[q], pass::pol_first());
         }
     }
 };
@@ -228,40 +224,35 @@ struct ColIter : Layout {
 // dual = atl + c, stat = dual - delta, pobj = c.x, cone_gap = max|x - z| and the
 // finiteness of x, z, delta and of the implicit y_k = x_j + a_k (b_i - r_i),
 // gamma_k = -a_k lam_i. Per-thread partials are reduced once per CTA (finish).
-// The gather warps own the per-nonzero checks, the reducer warps the rest;
-// both fold into the CTA's partials.
 struct ColReport : Layout {
+    static constexpr int kUnroll = 4;   // 8 report accumulators per thread: keep register pressure low
     const double* br;      // may be null
     double* part;          // [kReportFieldsCol][gridDim.x]
-    int32_t* nf_flag;      // set by gather warps on a non-finite implicit y/gamma
     double d2, dmx, s2, smx, amx, cx, cg, nf;
-    __device__ void check(double a, int i, double lam_i) {
-        if (!isfinite(a * lam_i) || (br && !isfinite(a * br[i]))) *nf_flag = 1;
+    __device__ __forceinline__ void check(double a, int i, double lam_i) {
+        if (!isfinite(a * lam_i) || (br && !isfinite(a * br[i]))) nf = 1.0;
     }
-    __device__ void epilogue(Smem& sm, Stage&, int, int, int nseg, const int32_t*, const double* const* vb) {
-        for (int q = rtid(); q < nseg; q += kReduceThreads) {
-            const double atl = sm.acc[q];
-            const double xj = vb[0][q], zj = vb[1][q], dj = vb[2][q], cj = vb[3][q];
-            const double dual = atl + cj;
-            const double stat = dual - dj;
-            d2 = d2 + dual * dual;
-            dmx = nanmax(dmx, fabs(dual));
-            s2 = s2 + stat * stat;
-            smx = nanmax(smx, fabs(stat));
-            amx = nanmax(amx, fabs(atl));
-            cx = cx + cj * xj;
-            cg = nanmax(cg, fabs(xj - zj));
-            if (!isfinite(xj) || !isfinite(zj) || !isfinite(dj)) nf = 1.0;
-        }
+    __device__ __forceinline__ void segment(Smem&, Stage&, int, int, int q, int, double atl, const double* const* vb) {
+        const double xj = vb[0][q], zj = vb[1][q], dj = vb[2][q], cj = vb[3][q];
+        const double dual = atl + cj;
+        const double stat = dual - dj;
+        d2 = d2 + dual * dual;
+        dmx = nanmax(dmx, fabs(dual));
+        s2 = s2 + stat * stat;
+        smx = nanmax(smx, fabs(stat));
+        amx = nanmax(amx, fabs(atl));
+        cx = cx + cj * xj;
+        cg = nanmax(cg, fabs(xj - zj));
+        if (!isfinite(xj) || !isfinite(zj) || !isfinite(dj)) nf = 1.0;
     }
-    __device__ void finish(Smem& sm) {
+    __device__ __forceinline__ void finish(Smem& sm) {
         const int G = gridDim.x;
         const double vals[8] = {d2, dmx, s2, smx, amx, cx, cg, nf};
         const bool is_sum[8] = {true, false, true, false, false, true, false, false};
         for (int f = 0; f < 8; ++f) {
-            const double v = is_sum[f] ? pass::reducer_reduce(vals[f], sm.red, SumOp())
-                                       : pass::reducer_reduce(vals[f], sm.red, MaxOp());
-            if (rtid() == 0) part[f * G + blockIdx.x] = v;
+            const double v = is_sum[f] ? pass::group_reduce(vals[f], sm.red[pass::group_id()], SumOp())
+                                       : pass::group_reduce(vals[f], sm.red[pass::group_id()], MaxOp());
+            if (pass::group_tid() == 0) part[(f * pass::kGroups + pass::group_id()) * G + blockIdx.x] = v;
         }
     }
 };
@@ -524,6 +515,8 @@ pass::Tiles row_panel_tiles(const cf_plan* p, int panel) {
     return pass::Tiles{p->row_tb.p + t0, (int32_t)(t1 - t0)};
 }
 pass::Tiles col_tiles(const cf_plan* p) { return pass::Tiles{p->col_tb.p, (int32_t)p->col_tiles}; }
+pass::Jds row_jds(const cf_plan* p) { return pass::Jds{p->rj_idx.p, p->rj_val.p, p->rj_perm.p, p->rj_joff.p}; }
+pass::Jds col_jds(const cf_plan* p) { return pass::Jds{p->cj_idx.p, p->cj_val.p, p->cj_perm.p, p->cj_joff.p}; }
 
 template <class P>
 int persistent_grid(int n_tiles) {
@@ -544,31 +537,19 @@ int persistent_grid(int n_tiles) {
 }
 
 template <class P>
-int launch_pass(const P& pol, const pass::Tiles& T, const int32_t* done, cudaStream_t st, int* grid_out = nullptr) {
+int launch_pass(const P& pol, const pass::Jds& L, const pass::Tiles& T, const int32_t* done, cudaStream_t st,
+                int* grid_out = nullptr) {
     if (T.n_tiles == 0) return CF_OK;
     const int grid = persistent_grid<P>(T.n_tiles);
     if (grid_out) *grid_out = grid;
-    pass::k_pass<P><<<grid, pass::kPThreads, pass::kSmemBytes, st>>>(pol, T, done);
+    pass::k_pass<P><<<grid, pass::kPThreads, pass::kSmemBytes, st>>>(pol, L, T, done);
     CF_LAUNCHED();
     return CF_OK;
 }
 
-// the row pass of one iteration (or A x): one launch per column panel
-template <class Fill>
-int launch_row_panels(cf_plan* p, const double* g, const int32_t* done, int64_t* nl, Fill fill) {
-    for (int pn = 0; pn < p->n_panels; ++pn) {
-        const pass::Tiles T = row_panel_tiles(p, pn);
-        CF_TRY(fill(pn, T, g, done));
-        if (nl) ++*nl;
-    }
-    return CF_OK;
-}
-
-ColIter col_iter(cf_plan* p) {
-    ColIter c{};
-    c.ptr_ = p->colptr.p;
-    c.idx_ = p->rowidx.p;
-    c.val_ = p->valc.p;
+template <bool CONES>
+ColIter<CONES> col_iter(cf_plan* p, const IterOpts& opt) {
+    ColIter<CONES> c{};
     c.g_ = p->h.p;
     c.nvec_ = 4;
     c.vb_[0] = p->x.p;
@@ -578,11 +559,14 @@ ColIter col_iter(cf_plan* p) {
     c.x = p->x.p;
     c.z = p->z.p;
     c.delta = p->delta.p;
-    c.cones = p->all_unit ? 0 : 1;
     c.tile_cone = p->tile_cone.p;
     c.tile_big = p->tile_big.p;
     c.cone_ptr = p->cone_ptr.p;
     c.wbuf = p->wbuf.p;
+    c.vterm = opt.vterm;
+    c.ccorr = opt.ccorr;
+    c.mu = opt.mu;
+    c.div = pass::make_mudiv(opt.mu);
     return c;
 }
 
@@ -605,11 +589,11 @@ int launch_iteration(cf_plan* p, const IterOpts& opt, const int32_t* done, int64
         CF_CUDA(cudaEventRecord(e_a, p->stream));
     }
     if (p->n > 0) {
-        ColIter c = col_iter(p);
-        c.vterm = opt.vterm;
-        c.ccorr = opt.ccorr;
-        c.mu = opt.mu;
-        CF_TRY(launch_pass(c, col_tiles(p), done, p->stream));
+        if (p->all_unit) {
+            CF_TRY(launch_pass(col_iter<false>(p, opt), col_jds(p), col_tiles(p), done, p->stream));
+        } else {
+            CF_TRY(launch_pass(col_iter<true>(p, opt), col_jds(p), col_tiles(p), done, p->stream));
+        }
         ++nl;
         if (!p->all_unit && p->n_big > 0) {
             BigConeArgs g{};
@@ -627,39 +611,36 @@ int launch_iteration(cf_plan* p, const IterOpts& opt, const int32_t* done, int64
         }
     }
     if (p->profiling) CF_CUDA(cudaEventRecord(e_b, p->stream));
-    if (p->m > 0) {
-        const int64_t m = p->m;
-        CF_TRY(launch_row_panels(p, p->x.p, done, &nl, [&](int pn, const pass::Tiles& T, const double* g,
-                                                           const int32_t* dn) {
-            RowIter r{};
-            r.ptr_ = p->rowptr.p;
-            r.idx_ = p->colidx.p;
-            r.val_ = p->valr.p;
-            r.g_ = g;
-            r.seg_off = (int64_t)pn * m;
-            r.last = (pn == p->n_panels - 1);
-            r.carry = p->ax.p;
-            int nv = 0;
-            if (r.last) {
-                r.vb_[0] = p->b.p - r.seg_off;
-                r.vb_[1] = p->lam.p - r.seg_off;
-                r.vb_[2] = p->fu.p - r.seg_off;
-                r.vb_[3] = p->db.p - r.seg_off;
-                nv = 4;
-            }
-            if (pn > 0) {
-                r.vb_[nv++] = p->ax.p - r.seg_off;
-                r.carry_ = true;
-            }
-            r.nvec_ = nv;
-            r.lam = p->lam.p;
-            r.h = p->h.p;
-            r.mu = opt.mu;
-            r.rcorr = opt.rcorr;
-            r.br = (opt.report || p->keep_br) ? p->br.p : nullptr;
-            r.ax = opt.report ? p->ax.p : nullptr;
-            return launch_pass(r, T, dn, p->stream);
-        }));
+    const int64_t m = p->m;
+    for (int pn = 0; pn < p->n_panels && m > 0; ++pn) {
+        RowIter r{};
+        r.g_ = p->x.p;
+        r.seg_off = (int64_t)pn * m;
+        r.last = (pn == p->n_panels - 1);
+        r.carry = p->ax.p;
+        int nv = 0;
+        if (r.last) {
+            r.vb_[0] = p->b.p - r.seg_off;
+            r.vb_[1] = p->lam.p - r.seg_off;
+            r.vb_[2] = p->fu.p - r.seg_off;
+            r.vb_[3] = p->db.p - r.seg_off;
+            nv = 4;
+        }
+        if (pn > 0) {
+            r.vb_[nv++] = p->ax.p - r.seg_off;
+            r.carry_src_ = p->ax.p - r.seg_off;
+            r.carry_ = true;
+        }
+        r.nvec_ = nv;
+        r.lam = p->lam.p;
+        r.h = p->h.p;
+        r.mu = opt.mu;
+        r.div = pass::make_mudiv(opt.mu);
+        r.rcorr = opt.rcorr;
+        r.br = (opt.report || p->keep_br) ? p->br.p : nullptr;
+        r.ax = opt.report ? p->ax.p : nullptr;
+        CF_TRY(launch_pass(r, row_jds(p), row_panel_tiles(p, pn), done, p->stream));
+        ++nl;
     }
     if (p->profiling) CF_CUDA(cudaEventRecord(e_c, p->stream));
     if (launches) *launches += nl;
@@ -683,35 +664,29 @@ void prof_collect(cf_plan* p) {
 }
 
 int launch_spmv_rows(cf_plan* p, const double* x, double* y) {
-    if (p->m == 0) return CF_OK;
     const int64_t m = p->m;
-    return launch_row_panels(p, x, nullptr, nullptr, [&](int pn, const pass::Tiles& T, const double* g,
-                                                         const int32_t* dn) {
+    for (int pn = 0; pn < p->n_panels && m > 0; ++pn) {
         RowSpmv r{};
-        r.ptr_ = p->rowptr.p;
-        r.idx_ = p->colidx.p;
-        r.val_ = p->valr.p;
-        r.g_ = g;
+        r.g_ = x;
         r.seg_off = (int64_t)pn * m;
         r.y = y;
         if (pn > 0) {
             r.vb_[0] = y - r.seg_off;
+            r.carry_src_ = y - r.seg_off;
             r.nvec_ = 1;
             r.carry_ = true;
         }
-        return launch_pass(r, T, dn, p->stream);
-    });
+        CF_TRY(launch_pass(r, row_jds(p), row_panel_tiles(p, pn), nullptr, p->stream));
+    }
+    return CF_OK;
 }
 
 int launch_spmv_cols(cf_plan* p, const double* y, double* x) {
     if (p->n == 0) return CF_OK;
     ColSpmv c{};
-    c.ptr_ = p->colptr.p;
-    c.idx_ = p->rowidx.p;
-    c.val_ = p->valc.p;
     c.g_ = y;
     c.y = x;
-    return launch_pass(c, col_tiles(p), nullptr, p->stream);
+    return launch_pass(c, col_jds(p), col_tiles(p), nullptr, p->stream);
 }
 
 int launch_report(cf_plan* p, double mu, bool ax_ready, const cf_config* cfg, int64_t k, int64_t slot,
@@ -736,11 +711,8 @@ int launch_report(cf_plan* p, double mu, bool ax_ready, const cf_config* cfg, in
     }
     int g_col = 0;
     if (p->n > 0) {
-        CF_CUDA(cudaMemsetAsync(p->nf_flag.p, 0, 4, p->stream));
         ColReport c{};
-        c.ptr_ = p->colptr.p;
-        c.idx_ = p->rowidx.p;
-        c.val_ = p->valc.p;
+        c.d2 = c.dmx = c.s2 = c.smx = c.amx = c.cx = c.cg = c.nf = 0.0;
         c.g_ = p->lam.p;
         c.nvec_ = 4;
         c.vb_[0] = p->x.p;
@@ -749,14 +721,14 @@ int launch_report(cf_plan* p, double mu, bool ax_ready, const cf_config* cfg, in
         c.vb_[3] = p->c.p;
         c.br = p->br_valid ? p->br.p : nullptr;
         c.part = p->part_col.p;
-        c.nf_flag = p->nf_flag.p;
-        CF_TRY(launch_pass(c, col_tiles(p), done, p->stream, &g_col));
+        CF_TRY(launch_pass(c, col_jds(p), col_tiles(p), done, p->stream, &g_col));
+        g_col *= pass::kGroups;  // one partial per (field, group, CTA)
         ++nl;
     }
     FinalizeArgs f{};
     f.part_row = p->part_row.p;
     f.part_col = p->part_col.p;
-    f.nf_flag = p->nf_flag.p;
+    f.nf_flag = nullptr;
     f.g_row = p->m > 0 ? p->row_report_ctas : 0;
     f.g_col = g_col;
     f.k = k;

@@ -1,30 +1,30 @@
-// Persistent, warp-specialised, TMA-pipelined tile engine for the sparse passes (sm_100a).
+// Persistent, TMA-pipelined, jagged-diagonal tile engine for the sparse passes (sm_100a).
 //
-// A pass walks the nonzeros of one compressed layout (CSR panels for the row
-// pass, CSC for the column pass) tile by tile. A tile is a run of segments
-// (rows or columns) whose nonzeros are contiguous and, unless a single
-// segment is longer, fit one stage (kPCap). Tiles are cut on the host
-// (cf_setup.cu: greedy by nonzeros and segment count, cone-aligned for
-// columns). Each persistent CTA owns tiles blockIdx.x, +gridDim.x, ...
+// A pass walks one compressed layout (CSR panels for the row pass, CSC for the
+// column pass) tile by tile. A tile is a run of <= kPSeg segments (rows or
+// columns) with <= kPCap nonzeros, cut on the host (cf_setup.cu), or one
+// segment longer than kPCap ("long tile"). Inside a normal tile the nonzeros
+// are stored in JAGGED-DIAGONAL order (built once by k_build_jds): the tile's
+// segments are ranked by length (descending, stable), slot j holds segment
+// perm[j], and the k-th nonzero of slot j sits at joff[k] + j. So
+//   * thread j owns one segment: it gathers g[idx] for its nonzeros (8
+//     independent loads in flight) and sums the products SEQUENTIALLY in
+//     canonical order — np.bincount's order (uv.py:10-12), bit-identical;
+//   * a warp reads idx/val for 32 segments at consecutive shared-memory
+//     addresses (conflict-free), the k loop bound is warp-uniform and lanes
+//     drop out in length order (no product buffer, no reduction phase).
+// The L1TEX pipe's ~1 random sector per SM-cycle (the gathers) is then the
+// only hot resource besides HBM.
 //
-// Warp roles (one CTA per SM, kStages-deep shared-memory ring):
-//   producer warp : cp.async.bulk (TMA 1D) of a tile's index/value slices,
-//                   segment pointers and epilogue vectors -> stage, completing
-//                   on full[s]; every streamed byte carries an L2 evict-first
-//                   hint so the gathered vector stays L2-resident.
-//   gather warps  : g[idx] for every staged nonzero (8 independent loads per
-//                   lane in flight, evict-last), product written in place over
-//                   the staged value; arrive on prod[s]. They never wait for
-//                   the reduction, so the L1TEX pipe — whose ~1 random sector
-//                   per SM-cycle is the hard limit of this kernel — stays busy.
-//   reducer warps : one thread per segment sums its products SEQUENTIALLY in
-//                   storage order (np.bincount order, uv.py:10-12), starting
-//                   from the carried partial of the previous panel, then runs
-//                   the pass epilogue; arrive on empty[s] to free the stage.
-// A segment longer than kPCap is handled by the reducer warps alone, streaming
-// it through the stage in chunks (rare: only for pathological row lengths).
+// Warp roles: 1 producer warp issues cp.async.bulk (TMA 1D) of a future
+// tile's idx/val/perm/joff and its epilogue vectors into a kStages ring
+// (full[s] mbarrier, L2 evict-first hint on every streamed byte); kPSeg/32
+// compute warps consume (empty[s] when done). Compute warps progress through
+// tiles independently unless the policy needs a per-tile group barrier
+// (cones) or the tile is long (chunked through the stage by all of them).
 #pragma once
 
+#include <cmath>
 #include <cstdint>
 
 #include "cf_common.h"
@@ -32,35 +32,63 @@
 namespace cf {
 namespace pass {
 
-constexpr int kPCap = 2048;       // nonzeros per staged tile
-constexpr int kPSeg = 256;        // segments per tile (== reducer threads)
-constexpr int kStages = 5;        // ring depth
-constexpr int kGatherWarps = 8;
-constexpr int kReduceWarps = kPSeg / 32;
-constexpr int kGatherThreads = kGatherWarps * 32;
-constexpr int kReduceThreads = kReduceWarps * 32;
-constexpr int kPThreads = kGatherThreads + kReduceThreads + 32;   // + producer warp
-constexpr int kPVecs = 5;         // epilogue vectors staged per tile (incl. the panel carry)
-constexpr int kReduceBarrier = 1; // named barrier id of the reducer group
+#ifndef CF_STAGES
+#define CF_STAGES 4
+#endif
+#ifndef CF_GROUPS
+#define CF_GROUPS 2
+#endif
+#ifndef CF_UNROLL
+#define CF_UNROLL 12
+#endif
+constexpr int kPCap = 2048;        // nonzeros per staged tile
+constexpr int kPSeg = 256;         // segments per tile (== threads of a compute group)
+constexpr int kMaxDiag = 256;      // longest segment inside a normal tile (longer ones get their own tile)
+constexpr int kStages = CF_STAGES; // ring depth
+constexpr int kGroups = CF_GROUPS; // compute groups; group g consumes the CTA's tiles i = g, g+kGroups, ...
+constexpr int kUnroll = CF_UNROLL; // independent gathers in flight per thread
+constexpr int kComputeWarps = kPSeg / 32;      // per group
+constexpr int kComputeThreads = kPSeg;         // per group
+constexpr int kPThreads = kGroups * (kComputeThreads + 32);   // + one producer warp per group
+constexpr int kPVecs = 5;          // epilogue vectors staged per tile (incl. the panel carry)
+constexpr int kFvTab = 256;
+static_assert(kStages % kGroups == 0, "a ring slot must be reused by the same compute group (mbarrier parity)");
 
 struct alignas(16) Stage {
-    int32_t meta[4];                   // s0, s1, k0, k1 (written by the producer)
+    int32_t meta[4];                    // s0, nseg, k0, len (written by the producer)
+    int32_t meta2[4];                   // maxlen (0 = long tile), first joff entry
     int32_t idx[kPCap + 8];
     double val[kPCap + 4];
-    int32_t ptr[kPSeg + 12];
+    uint16_t perm[kPSeg + 16];
+    uint16_t joff[kMaxDiag + 16];
     double vec[kPVecs][kPSeg + 4];
 };
 
 struct Smem {
     Stage st[kStages];
     alignas(8) uint64_t full[kStages];
-    alignas(8) uint64_t prod[kStages];
     alignas(8) uint64_t empty[kStages];
-    double acc[kPSeg];
-    double red[32];
+    double fvtab[kFvTab];               // 1/(1+cnt) for small column counts (uv.py:82)
+    double acc[kGroups][kPSeg];         // segment sums of the current tile, natural order
+    int32_t cnt[kGroups][kPSeg];        // segment lengths
+    double cscr[kGroups][3][kPSeg];     // cone epilogue: x+, w, delta+
+    double red[kGroups][32];
 };
 
 constexpr size_t kSmemBytes = sizeof(Smem);
+
+// x / mu; exact multiply when mu is a power of two (then x * (1/mu) == x / mu bit for bit)
+struct MuDiv {
+    double mu, inv;
+    bool pow2;
+    __device__ __forceinline__ double operator()(double x) const { return pow2 ? x * inv : x / mu; }
+};
+__host__ inline MuDiv make_mudiv(double mu) {
+    int e = 0;
+    const double fr = frexp(mu, &e);
+    MuDiv d{mu, 1.0 / mu, fr == 0.5 && e > -1000 && e < 1000};
+    return d;
+}
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -106,23 +134,25 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
-__device__ __forceinline__ void reducer_sync() {
-    asm volatile("bar.sync %0, %1;" ::"n"(kReduceBarrier), "n"(kReduceThreads) : "memory");
+// compute group of the calling thread and its thread index inside the group
+__device__ __forceinline__ int group_id() { return (int)threadIdx.x / kComputeThreads; }
+__device__ __forceinline__ int group_tid() { return (int)threadIdx.x % kComputeThreads; }
+// named barrier of the caller's compute group (ids 1..kGroups; 0 is __syncthreads)
+__device__ __forceinline__ void group_sync() {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + group_id()), "n"(kComputeThreads) : "memory");
 }
 
-__device__ __forceinline__ int rtid() { return (int)threadIdx.x - kGatherThreads; }
-
-// deterministic reduction over the reducer group; result valid in reducer thread 0
+// deterministic reduction over the caller's compute group; result valid in its thread 0
 template <class Op>
-__device__ double reducer_reduce(double v, double* red, Op op) {
+__device__ double group_reduce(double v, double* red, Op op) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, off));
-    const int w = rtid() >> 5, l = rtid() & 31;
-    reducer_sync();
+    const int w = group_tid() >> 5, l = group_tid() & 31;
+    group_sync();
     if (l == 0) red[w] = v;
-    reducer_sync();
+    group_sync();
     if (w == 0) {
-        v = (l < kReduceWarps) ? red[l] : 0.0;
+        v = (l < kComputeWarps) ? red[l] : 0.0;
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, off));
     }
@@ -149,8 +179,7 @@ __device__ __forceinline__ void st_hint(double* p, double v, uint64_t pol) {
 }
 
 // Aligned superset copy of `count` elements starting at `first`: the copy
-// starts at the 16-byte boundary below `first`; the consumer finds element 0
-// at lead_of(first).
+// starts at the 16-byte boundary below `first`; element 0 lands at lead_of(first).
 template <class T>
 __device__ __forceinline__ int lead_of(const T* first) {
     return (int)(((uintptr_t)first & 15u) / sizeof(T));
@@ -165,49 +194,72 @@ __device__ __forceinline__ uint32_t span_bytes(const T* first, int64_t count) {
 template <class T>
 __device__ __forceinline__ void copy_span(void* dst, const T* first, int64_t count, uint64_t* bar, uint64_t pol) {
     const uint32_t bytes = span_bytes(first, count);
-    if (count > 0 && bytes) bulk_g2s(dst, (const void*)((uintptr_t)first & ~(uintptr_t)15u), bytes, bar, pol);
+    if (bytes) bulk_g2s(dst, (const void*)((uintptr_t)first & ~(uintptr_t)15u), bytes, bar, pol);
 }
 
-// Tile boundaries: tb[t] = {first segment, first nonzero}; tile t = [tb[t], tb[t+1]).
+// Tile table: tb[t] = {first segment, first nonzero, first joff entry, maxlen (0 = long tile)};
+// tile t spans [tb[t].x, tb[t+1].x) segments and [tb[t].y, tb[t+1].y) nonzeros.
 struct Tiles {
-    const int2* tb;
+    const int4* tb;
     int32_t n_tiles;
 };
 
+// The JDS layout of a pass: idx/val in jagged-diagonal order inside every
+// normal tile (canonical order inside long tiles), perm (slot -> local
+// segment, indexed by segment position) and joff (per-tile diagonal starts).
+struct Jds {
+    const int32_t* idx;
+    const double* val;
+    const uint16_t* perm;
+    const uint16_t* joff;
+};
+
 // ---------------------------------------------------------------- the engine
-// P (the pass policy) provides, all __device__ unless noted:
-//   int nvec() const; const double* vec(int v) const   staged epilogue vectors, indexed by segment
-//   const int32_t* ptr() / idx(); const double* val() / gvec()
-//   bool carry_in() const                               acc starts from staged vec[nvec()-1]
-//   void check(double a, int j, double g)               per-nonzero hook (report finiteness)
-//   void epilogue(Smem&, Stage&, int tile, int s0, int nseg, const int32_t* ptrb, const double* const* vecb)
-//                                                       reducer threads only (reducer_sync() allowed)
-//   void finish(Smem&)                                  reducer threads only, after the last tile
+// P (the pass policy) provides (device):
+//   int nvec() const; const double* vec(int v) const  staged epilogue vectors, indexed by segment
+//   bool carry_in() const                              acc starts from staged vec[nvec()-1]
+//   const double* gvec() const                         gathered operand
+//   static constexpr bool kGroupEpilogue               epilogue needs all segments of the tile at once
+//   void check(double a, int j, double g)              per-nonzero hook (report finiteness)
+//   void segment(Smem&, Stage&, int tile, int s0, int q, int cnt, double acc, const double* const* vecb)
+//                                                      thread-level epilogue of local segment q
+//   void group(Smem&, Stage&, int tile, int s0, int nseg, const double* const* vecb)
+//                                                      (kGroupEpilogue) after group_sync
+//   void finish(Smem&)                                 compute threads, after the last tile
 template <class P>
-__device__ __forceinline__ void issue_tile(const P& p, const Tiles& T, int t, Stage& st, uint64_t* bar,
-                                           uint64_t pol) {
-    const int2 lo = T.tb[t], hi = T.tb[t + 1];
-    const int s0 = lo.x, s1 = hi.x, k0 = lo.y, k1 = hi.y;
+__device__ __forceinline__ void issue_tile(const P& p, const Jds& L, const Tiles& T, int t, Stage& st,
+                                           uint64_t* bar, uint64_t pol) {
+    const int4 lo = T.tb[t], hi = T.tb[t + 1];
+    const int s0 = lo.x, nseg = hi.x - lo.x, k0 = lo.y, len = hi.y - lo.y, j0 = lo.z, maxlen = lo.w;
     st.meta[0] = s0;
-    st.meta[1] = s1;
+    st.meta[1] = nseg;
     st.meta[2] = k0;
-    st.meta[3] = k1;
-    const bool fits = (k1 - k0) <= kPCap;
+    st.meta[3] = len;
+    st.meta2[0] = maxlen;
+    st.meta2[1] = j0;
     const int nv = p.nvec();
-    uint32_t total = span_bytes(p.ptr() + s0, s1 - s0 + 1);
-    if (fits && k1 > k0) total += span_bytes(p.idx() + k0, k1 - k0) + span_bytes(p.val() + k0, k1 - k0);
-    for (int v = 0; v < nv; ++v) total += span_bytes(p.vec(v) + s0, s1 - s0);
-    mbar_expect_tx(bar, total);
-    copy_span(st.ptr, p.ptr() + s0, s1 - s0 + 1, bar, pol);
-    if (fits && k1 > k0) {
-        copy_span(st.idx, p.idx() + k0, k1 - k0, bar, pol);
-        copy_span(st.val, p.val() + k0, k1 - k0, bar, pol);
+    uint32_t total = 0;
+    if (maxlen > 0) {
+        total += span_bytes(L.idx + k0, len) + span_bytes(L.val + k0, len);
+        total += span_bytes(L.perm + s0, nseg) + span_bytes(L.joff + j0, maxlen + 1);
     }
-    for (int v = 0; v < nv; ++v) copy_span(st.vec[v], p.vec(v) + s0, s1 - s0, bar, pol);
+#pragma unroll
+    for (int v = 0; v < kPVecs; ++v)
+        if (v < nv) total += span_bytes(p.vec(v) + s0, nseg);
+    mbar_expect_tx(bar, total);
+    if (maxlen > 0) {
+        copy_span(st.idx, L.idx + k0, len, bar, pol);
+        copy_span(st.val, L.val + k0, len, bar, pol);
+        copy_span(st.perm, L.perm + s0, nseg, bar, pol);
+        copy_span(st.joff, L.joff + j0, maxlen + 1, bar, pol);
+    }
+#pragma unroll
+    for (int v = 0; v < kPVecs; ++v)
+        if (v < nv) copy_span(st.vec[v], p.vec(v) + s0, nseg, bar, pol);
 }
 
 template <class P>
-__global__ void __launch_bounds__(kPThreads, 1) k_pass(const P p0, const Tiles T, const int32_t* done) {
+__global__ void __launch_bounds__(kPThreads, 1) k_pass(const P p0, const Jds L, const Tiles T, const int32_t* done) {
     if (done && *done) return;
     P p = p0;  // per-thread mutable copy (report accumulators live in registers)
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -215,146 +267,146 @@ __global__ void __launch_bounds__(kPThreads, 1) k_pass(const P p0, const Tiles T
     const int G = gridDim.x;
     const int my = (T.n_tiles > (int)blockIdx.x) ? (T.n_tiles - (int)blockIdx.x + G - 1) / G : 0;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int c = threadIdx.x; c < kFvTab; c += blockDim.x) sm.fvtab[c] = 1.0 / (1.0 + (double)c);
+    (void)warp;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&sm.full[s], 1);
-            mbar_init(&sm.prod[s], kGatherWarps);
-            mbar_init(&sm.empty[s], kReduceWarps);
+            mbar_init(&sm.empty[s], kComputeWarps);
         }
         fence_mbar_init();
     }
     __syncthreads();
 
-    if (warp == kGatherWarps + kReduceWarps) {
-        // ------------------------------------------------ producer
+    if (warp >= kGroups * kComputeWarps) {
+        // ------------------------------------------------ producers: warp kGroups*kComputeWarps + g feeds
+        // group g, whose tiles i = g, g+kGroups, ... use ring slots i % kStages (slot ≡ g mod kGroups)
+        const int pg = warp - kGroups * kComputeWarps;
         if (lane == 0) {
             const uint64_t pf = pol_first();
-            for (int i = 0; i < my; ++i) {
+            for (int i = pg, n = 0; i < my; i += kGroups, ++n) {
                 const int s = i % kStages;
                 if (i >= kStages) {
                     mbar_wait(&sm.empty[s], (uint32_t)(((i / kStages) - 1) & 1));
                     fence_proxy_async();
                 }
-                issue_tile(p, T, blockIdx.x + i * G, sm.st[s], &sm.full[s], pf);
+                issue_tile(p, L, T, blockIdx.x + i * G, sm.st[s], &sm.full[s], pf);
             }
         }
         return;
     }
 
-    if (warp < kGatherWarps) {
-        // ------------------------------------------------ gatherers
-        const uint64_t pl = pol_last();
-        const double* __restrict__ g = p.gvec();
-        const int gt = threadIdx.x;
-        for (int i = 0; i < my; ++i) {
-            const int s = i % kStages;
-            Stage& st = sm.st[s];
-            mbar_wait(&sm.full[s], (uint32_t)((i / kStages) & 1));
-            const int k0 = st.meta[2], len = st.meta[3] - k0;
-            if (len <= kPCap) {
-                const int32_t* ib = st.idx + lead_of(p.idx() + k0);
-                double* vb = st.val + lead_of(p.val() + k0);
-                int e = gt;
-                for (; e + 7 * kGatherThreads < len; e += 8 * kGatherThreads) {
-                    int j[8];
-                    double gv[8];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) j[u] = ib[e + u * kGatherThreads];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) gv[u] = ld_gather(g + j[u], pl);
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const double a = vb[e + u * kGatherThreads];
-                        p.check(a, j[u], gv[u]);
-                        vb[e + u * kGatherThreads] = __dmul_rn(a, gv[u]);
-                    }
-                }
-                int j[8];
-                double gv[8];
-                int cnt = 0;
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int ee = e + u * kGatherThreads;
-                    j[u] = ee < len ? ib[ee] : 0;
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (e + u * kGatherThreads < len) gv[u] = ld_gather(g + j[u], pl);
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int ee = e + u * kGatherThreads;
-                    if (ee < len) {
-                        const double a = vb[ee];
-                        p.check(a, j[u], gv[u]);
-                        vb[ee] = __dmul_rn(a, gv[u]);
-                        ++cnt;
-                    }
-                }
-                (void)cnt;
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.prod[s]);
-        }
-        return;
-    }
-
-    // ---------------------------------------------------- reducers
-    const int rt = threadIdx.x - kGatherThreads;   // 0 .. kReduceThreads-1
-    const uint64_t pf = pol_first(), pl = pol_last();
-    for (int i = 0; i < my; ++i) {
+    // ---------------------------------------------------- compute warps
+    const uint64_t pl = pol_last(), pf = pol_first();
+    const double* __restrict__ g = p.gvec();
+    const int grp = group_id();
+    const int j = group_tid();   // slot within the tile
+    const int gw = j >> 5;       // warp within the group
+    for (int i = grp; i < my; i += kGroups) {
         const int s = i % kStages;
         Stage& st = sm.st[s];
-        mbar_wait(&sm.prod[s], (uint32_t)((i / kStages) & 1));
-        const int s0 = st.meta[0], s1 = st.meta[1], k0 = st.meta[2], k1 = st.meta[3];
-        const int nseg = s1 - s0, len = k1 - k0;
-        const int32_t* ptrb = st.ptr + lead_of(p.ptr() + s0);
-        const double* vecb[kPVecs];
+        mbar_wait(&sm.full[s], (uint32_t)((i / kStages) & 1));
+        const int s0 = st.meta[0], nseg = st.meta[1], k0 = st.meta[2], len = st.meta[3];
+        const int maxlen = st.meta2[0];
         const int nv = p.nvec();
+        const double* vecb[kPVecs];
 #pragma unroll
         for (int v = 0; v < kPVecs; ++v) vecb[v] = v < nv ? st.vec[v] + lead_of(p.vec(v) + s0) : nullptr;
-        const double* carry = p.carry_in() ? vecb[nv - 1] : nullptr;
-        if (len <= kPCap) {
-            const double* vb = st.val + lead_of(p.val() + k0);
-            for (int q = rt; q < nseg; q += kReduceThreads) {
-                const int a = ptrb[q] - k0, b = ptrb[q + 1] - k0;
-                double acc = carry ? carry[q] : 0.0;
-                int k = a;
-                for (; k + 3 < b; k += 4) {
-                    const double v0 = vb[k], v1 = vb[k + 1], v2 = vb[k + 2], v3 = vb[k + 3];
-                    acc = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(acc, v0), v1), v2), v3);
+        // the carried partial is always the last staged vector (p.carry_src() = its global base)
+        const double* carry = p.carry_in() ? st.vec[nv - 1] + lead_of(p.carry_src() + s0) : nullptr;
+        const int tile = (int)blockIdx.x + i * G;
+        if (maxlen > 0) {
+            const int32_t* ib = st.idx + lead_of(L.idx + k0);
+            const double* vb = st.val + lead_of(L.val + k0);
+            const uint16_t* pb = st.perm + lead_of(L.perm + s0);
+            const uint16_t* jb = st.joff + lead_of(L.joff + st.meta2[1]);
+            if (gw * 32 < nseg) {
+                const bool active = j < nseg;
+                const int q = active ? (int)pb[j] : 0;
+                double acc = (active && carry) ? carry[q] : 0.0;
+                int cnt = 0;
+                // lanes drop out in length order; the warp stops when its lane 0 is done
+                constexpr int U = P::kUnroll;
+                for (int k = 0; k < maxlen; k += U) {
+                    int e[U];
+                    bool ok[U];
+                    bool any = false;
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int kk = k + u;
+                        const int a = kk < maxlen ? (int)jb[kk] : 0;
+                        const int b = kk < maxlen ? (int)jb[kk + 1] : 0;
+                        ok[u] = active && (b - a) > j;
+                        e[u] = a + j;
+                        any |= ok[u];
+                    }
+                    if (!__any_sync(0xffffffffu, any)) break;
+                    int jj[U];
+                    double av[U], gv[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        jj[u] = ok[u] ? ib[e[u]] : 0;
+                        av[u] = ok[u] ? vb[e[u]] : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) gv[u] = ok[u] ? ld_gather(g + jj[u], pl) : 0.0;
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        if (ok[u]) {
+                            p.check(av[u], jj[u], gv[u]);
+                            acc = __dadd_rn(acc, __dmul_rn(av[u], gv[u]));
+                            ++cnt;
+                        }
                 }
-                for (; k < b; ++k) acc = __dadd_rn(acc, vb[k]);
-                sm.acc[q] = acc;
+                if (active) {
+                    if (P::kGroupEpilogue) {
+                        sm.acc[grp][q] = acc;
+                        sm.cnt[grp][q] = cnt;
+                    } else {
+                        p.segment(sm, st, tile, s0, q, cnt, acc, vecb);   // slot order, no barrier
+                    }
+                }
             }
         } else {
-            // one long segment: stream it through the stage's value buffer
-            for (int q = rt; q < nseg; q += kReduceThreads) sm.acc[q] = carry ? carry[q] : 0.0;
+            // long tile: one segment [k0, k0+len), canonical order, chunked through the stage
             double* buf = st.val;
-            const double* __restrict__ g = p.gvec();
-            for (int c0 = k0; c0 < k1; c0 += kPCap) {
-                const int cl = min(kPCap, k1 - c0);
-                for (int e = rt; e < cl; e += kReduceThreads) {
-                    const int jj = ld_first(p.idx() + c0 + e, pf);
-                    const double a = ld_first(p.val() + c0 + e, pf);
+            double* lacc = sm.acc[grp];
+            if (j == 0) {
+                lacc[0] = carry ? carry[0] : 0.0;
+                sm.cnt[grp][0] = len;
+            }
+            group_sync();
+            for (int c0 = 0; c0 < len; c0 += kPCap) {
+                const int cl = min(kPCap, len - c0);
+                for (int e = j; e < cl; e += kComputeThreads) {
+                    const int jj = ld_first(L.idx + k0 + c0 + e, pf);
+                    const double a = ld_first(L.val + k0 + c0 + e, pf);
                     const double gj = ld_gather(g + jj, pl);
                     p.check(a, jj, gj);
                     buf[e] = __dmul_rn(a, gj);
                 }
-                reducer_sync();
-                for (int q = rt; q < nseg; q += kReduceThreads) {
-                    const int a = max(ptrb[q], c0) - c0, b = min(ptrb[q + 1], c0 + cl) - c0;
-                    if (a < b) {
-                        double acc = sm.acc[q];
-                        for (int k = a; k < b; ++k) acc = __dadd_rn(acc, buf[k]);
-                        sm.acc[q] = acc;
-                    }
+                group_sync();
+                if (j == 0) {
+                    double acc = lacc[0];
+                    for (int e = 0; e < cl; ++e) acc = __dadd_rn(acc, buf[e]);
+                    lacc[0] = acc;
                 }
-                reducer_sync();
+                group_sync();
             }
+            if (!P::kGroupEpilogue && j == 0) p.segment(sm, st, tile, s0, 0, len, lacc[0], vecb);
+            group_sync();
         }
-        p.epilogue(sm, st, (int)blockIdx.x + i * G, s0, nseg, ptrb, vecb);
-        reducer_sync();
-        if ((rt & 31) == 0) mbar_arrive(&sm.empty[s]);
+        if (P::kGroupEpilogue) {
+            // cones: every column of the tile first (natural order), then one thread per cone
+            group_sync();
+            for (int q = j; q < nseg; q += kComputeThreads)
+                p.segment(sm, st, tile, s0, q, sm.cnt[grp][q], sm.acc[grp][q], vecb);
+            group_sync();
+            p.group(sm, st, tile, s0, nseg, vecb);
+            group_sync();   // sm.acc/cnt/cscr of this group are rewritten by its next tile
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[s]);
     }
     p.finish(sm);
 }

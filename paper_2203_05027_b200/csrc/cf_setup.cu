@@ -124,23 +124,109 @@ inline int bits_for(uint64_t maxval) {
     return b;
 }
 
-// Greedy tiles over segments [0, nseg) of a compressed layout: a tile takes
-// consecutive units (a unit = one segment, or one whole cone of <= kSmallCone
-// columns) while it stays within kTileSeg segments and kTileNnz nonzeros; a
-// unit that alone exceeds the nonzero budget gets a tile of its own (the
-// engine streams it in chunks). Cones wider than kSmallCone are cut into
-// pieces of their own, flagged for k_big_cone.
-void tile_segments(const std::vector<int32_t>& ptr, int64_t s_begin, int64_t s_end, std::vector<int2>& tb,
-                   std::vector<int32_t>* tcone, std::vector<int32_t>* tbig, int32_t cone, int32_t bigid) {
+// Jagged-diagonal layout of one tile (see cf_pass.cuh): segments ranked by
+// length (descending, stable), perm[rank] = local segment, the k-th nonzero
+// of rank j at k0 + joff[k] + j. A long tile (maxlen == 0) is copied as is.
+__global__ void __launch_bounds__(256) k_build_jds(const int32_t* ptr, const int32_t* isrc, const double* vsrc,
+                                                   const int4* tb, int32_t* idst, double* vdst, uint16_t* perm,
+                                                   uint16_t* joff) {
+    __shared__ int len[kTileSeg];
+    __shared__ int rnk[kTileSeg];
+    __shared__ int width[kTileDiag + 1];
+    __shared__ int jo[kTileDiag + 2];
+    const int t = blockIdx.x;
+    const int4 lo = tb[t], hi = tb[t + 1];
+    const int s0 = lo.x, nseg = hi.x - lo.x, k0 = lo.y, k1 = hi.y, j0 = lo.z, maxlen = lo.w;
+    if (maxlen == 0) {
+        for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+            idst[k] = isrc[k];
+            vdst[k] = vsrc[k];
+        }
+        if (threadIdx.x == 0) perm[s0] = 0;
+        return;
+    }
+    for (int q = threadIdx.x; q < nseg; q += blockDim.x) len[q] = ptr[s0 + q + 1] - ptr[s0 + q];
+    __syncthreads();
+    for (int q = threadIdx.x; q < nseg; q += blockDim.x) {
+        int r = 0;
+        const int lq = len[q];
+        for (int q2 = 0; q2 < nseg; ++q2) r += (len[q2] > lq) || (len[q2] == lq && q2 < q);
+        rnk[q] = r;
+        perm[s0 + r] = (uint16_t)q;
+    }
+    for (int k = threadIdx.x; k < maxlen; k += blockDim.x) {
+        int w = 0;
+        for (int q = 0; q < nseg; ++q) w += len[q] > k;
+        width[k] = w;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        jo[0] = 0;
+        for (int k = 0; k < maxlen; ++k) jo[k + 1] = jo[k] + width[k];
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k <= maxlen; k += blockDim.x) joff[j0 + k] = (uint16_t)jo[k];
+    for (int q = threadIdx.x; q < nseg; q += blockDim.x) {
+        const int src0 = ptr[s0 + q], r = rnk[q];
+        for (int kk = 0; kk < len[q]; ++kk) {
+            const int dst = k0 + jo[kk] + r;
+            idst[dst] = isrc[src0 + kk];
+            vdst[dst] = vsrc[src0 + kk];
+        }
+    }
+}
+
+// Greedy tile starts over segments [s_begin, s_end) of a compressed layout:
+// a tile takes consecutive segments while it stays within kTileSeg segments
+// and kTileNnz nonzeros; a segment that alone exceeds the nonzero budget gets
+// a (long) tile of its own.
+void tile_starts(const std::vector<int32_t>& ptr, int64_t s_begin, int64_t s_end, std::vector<int64_t>& starts) {
     int64_t s = s_begin;
     while (s < s_end) {
         int64_t e = s + 1;
-        while (e < s_end && e - s < kTileSeg && ptr[e + 1] - ptr[s] <= kTileNnz) ++e;
-        tb.push_back(make_int2((int)s, ptr[s]));
-        if (tcone) tcone->push_back(cone);
-        if (tbig) tbig->push_back(bigid);
+        const bool long_seg = ptr[s + 1] - ptr[s] > kTileDiag;
+        while (!long_seg && e < s_end && e - s < kTileSeg && ptr[e + 1] - ptr[s] <= kTileNnz &&
+               ptr[e + 1] - ptr[e] <= kTileDiag)
+            ++e;
+        starts.push_back(s);
         s = e;
     }
+}
+
+// tile table {s0, k0, joff start, maxlen} from tile starts (+ the final end segment)
+void tile_table(const std::vector<int32_t>& ptr, const std::vector<int64_t>& starts, int64_t s_end,
+                std::vector<int4>& tb, int64_t& joff_total) {
+    tb.clear();
+    joff_total = 0;
+    for (size_t t = 0; t < starts.size(); ++t) {
+        const int64_t s0 = starts[t], s1 = (t + 1 < starts.size()) ? starts[t + 1] : s_end;
+        const int64_t nnz = ptr[s1] - ptr[s0];
+        int maxlen = 0;
+        if (!(s1 - s0 == 1 && (nnz > kTileNnz || nnz > kTileDiag))) {
+            for (int64_t q = s0; q < s1; ++q) maxlen = std::max<int>(maxlen, ptr[q + 1] - ptr[q]);
+            maxlen = std::max(maxlen, 1);
+        }
+        tb.push_back(make_int4((int)s0, ptr[s0], (int)joff_total, maxlen));
+        if (maxlen > 0) joff_total += maxlen + 1;
+    }
+    tb.push_back(make_int4((int)s_end, ptr[s_end], (int)joff_total, 0));
+}
+
+int build_jds(cf_plan* p, const int32_t* ptr, const int32_t* isrc, const double* vsrc, const std::vector<int4>& tb,
+              int64_t nseg_total, int64_t joff_total, DevBuf<int4>& dtb, DevBuf<int32_t>& idst,
+              DevBuf<double>& vdst, DevBuf<uint16_t>& perm, DevBuf<uint16_t>& joff) {
+    CF_TRY(dtb.alloc(tb.size()));
+    CF_CUDA(cudaMemcpyAsync(dtb.p, tb.data(), tb.size() * sizeof(int4), cudaMemcpyHostToDevice, p->stream));
+    CF_TRY(idst.alloc(p->o));
+    CF_TRY(vdst.alloc(p->o));
+    CF_TRY(perm.alloc(nseg_total));
+    CF_TRY(joff.alloc(joff_total));
+    const int64_t ntiles = (int64_t)tb.size() - 1;
+    if (ntiles > 0) {
+        k_build_jds<<<(unsigned)ntiles, 256, 0, p->stream>>>(ptr, isrc, vsrc, dtb.p, idst.p, vdst.p, perm.p, joff.p);
+        CF_LAUNCHED();
+    }
+    return CF_OK;
 }
 
 int build_tiles(cf_plan* p, const int64_t* sizes, int64_t nb) {
@@ -151,20 +237,22 @@ int build_tiles(cf_plan* p, const int64_t* sizes, int64_t nb) {
     CF_CUDA(cudaStreamSynchronize(p->stream));
     // rows, panel by panel (segment = panel*m + row)
     const int64_t nsr = (int64_t)p->n_panels * m;
-    std::vector<int2> rtb;
+    std::vector<int64_t> rstarts;
     p->row_panel_tile.assign(p->n_panels + 1, 0);
     for (int pn = 0; pn < p->n_panels; ++pn) {
-        p->row_panel_tile[pn] = (int64_t)rtb.size();
-        tile_segments(rp, (int64_t)pn * m, (int64_t)(pn + 1) * m, rtb, nullptr, nullptr, 0, -1);
+        p->row_panel_tile[pn] = (int64_t)rstarts.size();
+        tile_starts(rp, (int64_t)pn * m, (int64_t)(pn + 1) * m, rstarts);
     }
-    p->row_panel_tile[p->n_panels] = (int64_t)rtb.size();
-    rtb.push_back(make_int2((int)nsr, rp[nsr]));
+    p->row_panel_tile[p->n_panels] = (int64_t)rstarts.size();
+    std::vector<int4> rtb;
+    int64_t rjoff = 0;
+    tile_table(rp, rstarts, nsr, rtb, rjoff);
     p->row_tiles = (int64_t)rtb.size() - 1;
-    // columns
-    std::vector<int2> ctb;
+    // columns (cone-aligned when the cone is not the orthant)
+    std::vector<int64_t> cstarts;
     std::vector<int32_t> tcone, tbig, big, cone_ptr;
     if (p->all_unit) {
-        tile_segments(cp, 0, n, ctb, nullptr, nullptr, 0, -1);
+        tile_starts(cp, 0, n, cstarts);
     } else {
         cone_ptr.resize(nb + 1);
         int64_t col = 0;
@@ -177,29 +265,52 @@ int build_tiles(cf_plan* p, const int64_t* sizes, int64_t nb) {
         while (q < nb) {
             const int64_t c0 = cone_ptr[q];
             if (sizes[q] > kSmallCone) {
-                tile_segments(cp, c0, c0 + sizes[q], ctb, &tcone, &tbig, (int32_t)q, (int32_t)big.size());
+                const size_t before = cstarts.size();
+                tile_starts(cp, c0, c0 + sizes[q], cstarts);
+                for (size_t t = before; t < cstarts.size(); ++t) {
+                    tcone.push_back((int32_t)q);
+                    tbig.push_back((int32_t)big.size());
+                }
                 big.push_back((int32_t)q);
                 ++q;
                 continue;
             }
             int64_t q1 = q + 1;
+            auto cone_ok = [&](int64_t qq) {  // no column of the cone needs a long tile
+                for (int64_t c = cone_ptr[qq]; c < cone_ptr[qq] + sizes[qq]; ++c)
+                    if (cp[c + 1] - cp[c] > kTileDiag) return false;
+                return true;
+            };
+            if (!cone_ok(q)) {  // cone with a very long column: treat like a big cone (k_big_cone)
+                const size_t before = cstarts.size();
+                tile_starts(cp, c0, c0 + sizes[q], cstarts);
+                for (size_t t = before; t < cstarts.size(); ++t) {
+                    tcone.push_back((int32_t)q);
+                    tbig.push_back((int32_t)big.size());
+                }
+                big.push_back((int32_t)q);
+                ++q;
+                continue;
+            }
             while (q1 < nb && sizes[q1] <= kSmallCone && cone_ptr[q1] + sizes[q1] - c0 <= kTileSeg &&
-                   cp[cone_ptr[q1] + sizes[q1]] - cp[c0] <= kTileNnz)
+                   cp[cone_ptr[q1] + sizes[q1]] - cp[c0] <= kTileNnz && cone_ok(q1))
                 ++q1;
-            ctb.push_back(make_int2((int)c0, cp[c0]));
+            cstarts.push_back(c0);
             tcone.push_back((int32_t)q);
             tbig.push_back(-1);
             q = q1;
         }
         tcone.push_back((int32_t)nb);
     }
-    ctb.push_back(make_int2((int)n, cp[n]));
+    std::vector<int4> ctb;
+    int64_t cjoff = 0;
+    tile_table(cp, cstarts, n, ctb, cjoff);
     p->col_tiles = (int64_t)ctb.size() - 1;
     p->n_big = (int64_t)big.size();
-    CF_TRY(p->row_tb.alloc(rtb.size()));
-    CF_TRY(p->col_tb.alloc(ctb.size()));
-    CF_CUDA(cudaMemcpyAsync(p->row_tb.p, rtb.data(), rtb.size() * sizeof(int2), cudaMemcpyHostToDevice, p->stream));
-    CF_CUDA(cudaMemcpyAsync(p->col_tb.p, ctb.data(), ctb.size() * sizeof(int2), cudaMemcpyHostToDevice, p->stream));
+    CF_TRY(build_jds(p, p->rowptr.p, p->colidx.p, p->valr.p, rtb, nsr, rjoff, p->row_tb, p->rj_idx, p->rj_val,
+                     p->rj_perm, p->rj_joff));
+    CF_TRY(build_jds(p, p->colptr.p, p->rowidx.p, p->valc.p, ctb, n, cjoff, p->col_tb, p->cj_idx, p->cj_val,
+                     p->cj_perm, p->cj_joff));
     if (p->all_unit) {
         CF_TRY(p->tile_big.alloc(1));
         CF_TRY(p->tile_cone.alloc(1));
@@ -382,7 +493,7 @@ int build(cf_plan* p, const int64_t* rows, const int64_t* cols, const double* va
     CF_CUDA(cudaMemsetAsync(p->br.p, 0, std::max<int64_t>(m, 1) * 8, st));
     p->row_report_ctas = (int32_t)std::min<int64_t>(std::max<int64_t>((m + 255) / 256, 1), 148 * 4);
     CF_TRY(p->part_row.alloc((size_t)kReportFieldsRow * p->row_report_ctas));
-    CF_TRY(p->part_col.alloc((size_t)kReportFieldsCol * std::max(max_col_report_ctas(), 1)));
+    CF_TRY(p->part_col.alloc((size_t)kReportFieldsCol * kMaxGroups * std::max(max_col_report_ctas(), 1)));
     p->host_ring = 64;
     CF_TRY(p->report_slot.alloc(p->host_ring));
     CF_TRY(p->done.alloc(1));
