@@ -305,6 +305,9 @@ def run_ours(args, spec, rank, world, local_rank):
         torch.cuda.empty_cache()
         tol = SolverConfig(eps_prim=args.eps, eps_dual=args.eps, eps_gap=args.eps,
                            max_iters=args.e2e_max_iters or 100_000)
+        # one untimed warm-up step: first-use costs of a fresh process (lazy kernel-module loading,
+        # first mapping of the memory pool) are not per-solve costs
+        solve(p, SolverConfig(max_iters=25))
         barrier()
         t0 = time.perf_counter()
         res = solve(p, tol)

@@ -14,6 +14,31 @@ static thread_local std::string g_last_error;
 
 void set_error(const std::string& msg) { g_last_error = msg; }
 
+cudaError_t pool_alloc(void** p, size_t bytes) {
+    static thread_local int configured_dev = -1;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (configured_dev != dev) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        cudaGetLastError();
+        configured_dev = dev;
+    }
+    e = cudaMallocAsync(p, bytes, 0);
+    if (e != cudaSuccess) return e;
+    return cudaStreamSynchronize(0);
+}
+
+void pool_free(void* p) {
+    // callers synchronise the plan stream before releasing (plan destroy, scoped setup scratch)
+    cudaFreeAsync(p, 0);
+    cudaStreamSynchronize(0);
+}
+
 int cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
     cudaGetLastError();  // clear sticky-free errors
     set_error(std::string(what) + " failed: " + cudaGetErrorString(e) + " (" + file + ":" + std::to_string(line) + ")");

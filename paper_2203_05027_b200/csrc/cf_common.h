@@ -39,6 +39,12 @@ int cuda_fail(cudaError_t e, const char* what, const char* file, int line);
 #define CF_LAUNCHED() CF_CUDA(cudaGetLastError())
 
 // ---------------------------------------------------------------- device buffers
+// Stream-ordered pool (cudaMallocAsync on the device's default pool with an unlimited release
+// threshold): plans created one after another reuse already-mapped memory instead of paying
+// cudaMalloc/cudaFree (and their implicit synchronisation) again. Allocation and release are
+// ordered on the legacy stream and synchronised, so a buffer is usable on any stream at return.
+cudaError_t pool_alloc(void** p, size_t bytes);
+void pool_free(void* p);
 template <class T>
 struct DevBuf {
     T* p = nullptr;
@@ -51,7 +57,7 @@ struct DevBuf {
         release();
         if (count == 0) count = 1;  // keep a valid pointer for empty dims
         // +64 bytes: the pass engine's bulk copies read 16-byte-aligned supersets
-        cudaError_t e = cudaMalloc(&p, count * sizeof(T) + 64);
+        cudaError_t e = pool_alloc(reinterpret_cast<void**>(&p), count * sizeof(T) + 64);
         if (e != cudaSuccess) {
             p = nullptr;
             cudaGetLastError();
@@ -63,7 +69,7 @@ struct DevBuf {
         return CF_OK;
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) pool_free(p);
         p = nullptr;
         n = 0;
     }

@@ -12,7 +12,9 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 
 #include "cf_common.h"
@@ -334,10 +336,30 @@ int build_tiles(cf_plan* p, const int64_t* sizes, int64_t nb) {
     return CF_OK;
 }
 
+// CF_VERBOSE=1: per-stage wall times of the setup on stderr
+struct StageClock {
+    bool on;
+    cudaStream_t st;
+    std::chrono::steady_clock::time_point t0, last;
+    explicit StageClock(cudaStream_t s) : on(getenv("CF_VERBOSE") != nullptr), st(s) {
+        t0 = last = std::chrono::steady_clock::now();
+    }
+    void mark(const char* what) {
+        if (!on) return;
+        cudaStreamSynchronize(st);
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "[cf setup] %-28s %8.2f ms (total %8.2f ms)\n", what,
+                std::chrono::duration<double, std::milli>(now - last).count(),
+                std::chrono::duration<double, std::milli>(now - t0).count());
+        last = now;
+    }
+};
+
 int build(cf_plan* p, const int64_t* rows, const int64_t* cols, const double* vals, const double* bsrc,
           const double* csrc, int64_t nb, const int64_t* sizes, int on_device, cf_problem_checks* chk) {
     const int64_t m = p->m, n = p->n, o = p->o;
     cudaStream_t st = p->stream;
+    StageClock clk(st);
     DevBuf<int64_t> drows, dcols;
     DevBuf<double> dvals;
     if (!on_device) {
@@ -358,6 +380,7 @@ int build(cf_plan* p, const int64_t* rows, const int64_t* cols, const double* va
     if (m) CF_CUDA(cudaMemcpyAsync(p->b.p, bsrc, m * 8, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
     if (n) CF_CUDA(cudaMemcpyAsync(p->c.p, csrc, n * 8, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
 
+    clk.mark("inputs H2D");
     // ---- validate (model.py:152-201)
     DevBuf<ull> counts;
     CF_TRY(counts.alloc(8));
@@ -381,6 +404,7 @@ int build(cf_plan* p, const int64_t* rows, const int64_t* cols, const double* va
         return CF_EPROBLEM;  // keys would be meaningless
     }
 
+    clk.mark("validate counters");
     // ---- canonical order: radix sort of col*m + row (uv.py:76)
     CF_TRY(p->colptr.alloc(n + 1));
     CF_TRY(p->rowidx.alloc(o));
@@ -422,6 +446,7 @@ int build(cf_plan* p, const int64_t* rows, const int64_t* cols, const double* va
         CF_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, kb, ib, (int64_t)o, 0, end_bit, st));
         const uint64_t* skeys = kb.Current();
         const int32_t* sperm = ib.Current();
+        clk.mark("canonical sort");
         k_count_dups<<<grid1d(o), 256, 0, st>>>(skeys, o, counts.p + 4);
         k_fill_csc<<<grid1d(o), 256, 0, st>>>(skeys, sperm, vals, o, m, p->rowidx.p, colof.p, p->valc.p);
         CF_LAUNCHED();
@@ -437,6 +462,7 @@ int build(cf_plan* p, const int64_t* rows, const int64_t* cols, const double* va
         k_ptr_from_sorted<int32_t><<<grid1d(o), 256, 0, st>>>(colof.p, o, n, p->colptr.p);
         CF_LAUNCHED();
 
+        clk.mark("csc fill + dup check");
         // ---- CSR panels: stable sort of canonical entries by (column panel, row); inside a
         //      segment the entries keep canonical (column) order
         const int64_t nseg_rows = (int64_t)p->n_panels * m;
@@ -465,6 +491,7 @@ int build(cf_plan* p, const int64_t* rows, const int64_t* cols, const double* va
         CF_CUDA(cudaMemsetAsync(p->rowptr.p, 0, ((int64_t)p->n_panels * m + 1) * 4, st));
     }
 
+    clk.mark("csr panel sort + fill");
     // ---- cached diagonals (uv.py:81-82; fv is recomputed in-kernel from colptr)
     CF_TRY(p->fu.alloc(m));
     CF_TRY(p->db.alloc(m));
@@ -475,7 +502,9 @@ int build(cf_plan* p, const int64_t* rows, const int64_t* cols, const double* va
     int64_t maxsize = 0;
     for (int64_t q = 0; q < nb; ++q) maxsize = std::max(maxsize, sizes[q]);
     p->all_unit = (nb == 0 || maxsize == 1);
+    clk.mark("row diag");
     CF_TRY(build_tiles(p, sizes, nb));
+    clk.mark("tiles + jds");
 
     // ---- iterate state (SolverState.zeros, solver.py:118-127) and report buffers
     CF_TRY(p->x.alloc(n));
@@ -504,6 +533,7 @@ int build(cf_plan* p, const int64_t* rows, const int64_t* cols, const double* va
     CF_CUDA(cudaEventCreate(&p->ev0));
     CF_CUDA(cudaEventCreate(&p->ev1));
     CF_CUDA(cudaStreamSynchronize(st));
+    clk.mark("state + report buffers");
     p->iter = 0;
     p->since_warm = 2;
     return CF_OK;
