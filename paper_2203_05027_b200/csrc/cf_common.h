@@ -14,7 +14,10 @@ namespace cf {
 
 // ---------------------------------------------------------------- geometry
 constexpr int kThreads = 256;     // threads of the simple (non-pass) kernels
-constexpr int kTileNnz = 2048;    // nonzeros per tile (= pass::kPCap)
+#ifndef CF_PCAP
+#define CF_PCAP 2048
+#endif
+constexpr int kTileNnz = CF_PCAP;  // nonzeros per tile (= pass::kPCap)
 constexpr int kTileSeg = 256;     // rows / columns per tile (= pass::kPSeg)
 constexpr int kTileDiag = 256;    // longest segment inside a multi-segment tile (= pass::kMaxDiag)
 constexpr int kSmallCone = 256;   // cones up to this size are projected inside the column tile

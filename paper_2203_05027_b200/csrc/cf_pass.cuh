@@ -41,7 +41,10 @@ namespace pass {
 #ifndef CF_UNROLL
 #define CF_UNROLL 12
 #endif
-constexpr int kPCap = 2048;        // nonzeros per staged tile
+#ifndef CF_PCAP
+#define CF_PCAP 2048
+#endif
+constexpr int kPCap = CF_PCAP;     // nonzeros per staged tile
 constexpr int kPSeg = 256;         // segments per tile (== threads of a compute group)
 constexpr int kMaxDiag = 256;      // longest segment inside a normal tile (longer ones get their own tile)
 constexpr int kStages = CF_STAGES; // ring depth
@@ -227,9 +230,8 @@ struct Jds {
 //                                                      (kGroupEpilogue) after group_sync
 //   void finish(Smem&)                                 compute threads, after the last tile
 template <class P>
-__device__ __forceinline__ void issue_tile(const P& p, const Jds& L, const Tiles& T, int t, Stage& st,
-                                           uint64_t* bar, uint64_t pol) {
-    const int4 lo = T.tb[t], hi = T.tb[t + 1];
+__device__ __forceinline__ void issue_tile(const P& p, const Jds& L, int4 lo, int4 hi, Stage& st, uint64_t* bar,
+                                           uint64_t pol) {
     const int s0 = lo.x, nseg = hi.x - lo.x, k0 = lo.y, len = hi.y - lo.y, j0 = lo.z, maxlen = lo.w;
     st.meta[0] = s0;
     st.meta[1] = nseg;
@@ -284,13 +286,27 @@ __global__ void __launch_bounds__(kPThreads, 1) k_pass(const P p0, const Jds L, 
         const int pg = warp - kGroups * kComputeWarps;
         if (lane == 0) {
             const uint64_t pf = pol_first();
-            for (int i = pg, n = 0; i < my; i += kGroups, ++n) {
+            // the tile-table entries of the next tile are loaded before waiting for its slot,
+            // so the copies start the moment the slot frees
+            int4 lo = make_int4(0, 0, 0, 0), hi = lo;
+            if (pg < my) {
+                lo = T.tb[blockIdx.x + pg * G];
+                hi = T.tb[blockIdx.x + pg * G + 1];
+            }
+            for (int i = pg; i < my; i += kGroups) {
                 const int s = i % kStages;
+                int4 nlo = lo, nhi = hi;
+                if (i + kGroups < my) {
+                    nlo = T.tb[blockIdx.x + (i + kGroups) * G];
+                    nhi = T.tb[blockIdx.x + (i + kGroups) * G + 1];
+                }
                 if (i >= kStages) {
                     mbar_wait(&sm.empty[s], (uint32_t)(((i / kStages) - 1) & 1));
                     fence_proxy_async();
                 }
-                issue_tile(p, L, T, blockIdx.x + i * G, sm.st[s], &sm.full[s], pf);
+                issue_tile(p, L, lo, hi, sm.st[s], &sm.full[s], pf);
+                lo = nlo;
+                hi = nhi;
             }
         }
         return;
