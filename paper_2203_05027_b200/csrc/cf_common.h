@@ -114,7 +114,8 @@ struct cf_plan {
     // jagged-diagonal copies of the CSR panels (rj_*) and of the CSC (cj_*) read by the passes
     cf::DevBuf<int32_t> rj_idx, cj_idx;
     cf::DevBuf<double> rj_val, cj_val;
-    cf::DevBuf<uint16_t> rj_perm, cj_perm, rj_joff, cj_joff;
+    cf::DevBuf<uint8_t> rj_perm, cj_perm;
+    cf::DevBuf<uint16_t> rj_joff, cj_joff;
     int64_t row_tiles = 0, col_tiles = 0;
     // row-pass column panels: the CSR is stored panel-major (segment = panel*m + row)
     // so each row-pass launch gathers only one panel's slice of x (L2-resident)

@@ -79,23 +79,19 @@ using pass::Smem;
 using pass::Stage;
 
 // ---------------------------------------------------------------- pass policies
-// Staged vectors are indexed by segment: for a row panel p the segments are
-// p*m + i, so vector bases are shifted by -seg_off.
+// A policy supplies the gathered operand, the per-segment epilogue vectors
+// (loaded in natural order straight from global memory) and the epilogue.
+using pass::Vals;
+
 struct Layout {
     const double* g_;
-    int32_t nvec_ = 0;
-    bool carry_ = false;
-    const double* vb_[pass::kPVecs] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     static constexpr bool kGroupEpilogue = false;
     static constexpr int kUnroll = pass::kUnroll;   // gathers in flight per thread
     __device__ __forceinline__ const double* gvec() const { return g_; }
-    __device__ __forceinline__ int nvec() const { return nvec_; }
-    __device__ __forceinline__ const double* vec(int v) const { return vb_[v]; }
-    __device__ __forceinline__ bool carry_in() const { return carry_; }
-    const double* carry_src_ = nullptr;   // global base of the carried partial (last staged vector)
-    __device__ __forceinline__ const double* carry_src() const { return carry_src_; }
+    __device__ __forceinline__ bool carry_in() const { return false; }
+    __device__ __forceinline__ double carry(const Vals&) const { return 0.0; }
     __device__ __forceinline__ void check(double, int, double) {}
-    __device__ __forceinline__ void group(Smem&, Stage&, int, int, int, const double* const*) {}
+    __device__ __forceinline__ void group(Smem&, int, int, int) {}
     __device__ __forceinline__ void finish(Smem&) {}
 };
 
@@ -106,7 +102,11 @@ struct Layout {
 struct RowIter : Layout {
     int64_t seg_off;       // p * m
     bool last;             // last panel: ADMM update
-    double* carry;         // partial A x between panels (= the plan's ax buffer)
+    bool has_carry;        // panel > 0: the sum continues from carry[i]
+    double* carry_buf;     // partial A x between panels (= the plan's ax buffer)
+    const double* b;
+    const double* fu;
+    const double* db;
     double* lam;
     double* h;
     double* br;            // optional: b - r
@@ -114,13 +114,28 @@ struct RowIter : Layout {
     const double* rcorr;   // optional: warm-start U eps / mu
     double mu;
     pass::MuDiv div;
-    __device__ __forceinline__ void segment(Smem&, Stage&, int, int s0, int q, int, double axi, const double* const* vb) {
+    __device__ __forceinline__ bool carry_in() const { return has_carry; }
+    __device__ __forceinline__ double carry(const Vals& v) const { return v.v[4]; }
+    __device__ __forceinline__ Vals load(int s) const {
+        const uint64_t pf = pass::pol_first();
+        const int64_t i = s - seg_off;
+        Vals v{};
+        if (last) {
+            v.v[0] = pass::ld_first(b + i, pf);
+            v.v[1] = pass::ld_first(lam + i, pf);
+            v.v[2] = pass::ld_first(fu + i, pf);
+            v.v[3] = pass::ld_first(db + i, pf);
+        }
+        if (has_carry) v.v[4] = pass::ld_first(carry_buf + i, pf);
+        return v;
+    }
+    __device__ __forceinline__ void segment(Smem&, int, int s0, int q, int, double axi, const Vals& v) {
         const int64_t i = s0 + q - seg_off;
         if (!last) {
-            carry[i] = axi;
+            carry_buf[i] = axi;
             return;
         }
-        const double bi = vb[0][q], li = vb[1][q], fui = vb[2][q], dbi = vb[3][q];
+        const double bi = v.v[0], li = v.v[1], fui = v.v[2], dbi = v.v[3];
         double si = dbi + axi;                  // (U t)_i with t = a b + x
         if (rcorr) si = si - rcorr[i];
         const double r = fui * si;              // r = U y+ = fu (U t)
@@ -138,8 +153,16 @@ struct RowIter : Layout {
 // y = A x (apply_U . apply_Vt, uv.py:106-131), panel by panel with y as the carry.
 struct RowSpmv : Layout {
     int64_t seg_off;
+    bool has_carry;
     double* y;
-    __device__ __forceinline__ void segment(Smem&, Stage&, int, int s0, int q, int, double acc, const double* const*) {
+    __device__ __forceinline__ bool carry_in() const { return has_carry; }
+    __device__ __forceinline__ double carry(const Vals& v) const { return v.v[4]; }
+    __device__ __forceinline__ Vals load(int s) const {
+        Vals v{};
+        if (has_carry) v.v[4] = y[s - seg_off];
+        return v;
+    }
+    __device__ __forceinline__ void segment(Smem&, int, int s0, int q, int, double acc, const Vals&) {
         y[s0 + q - seg_off] = acc;
     }
 };
@@ -147,17 +170,35 @@ struct RowSpmv : Layout {
 // x = A^T y (apply_V . apply_Ut)
 struct ColSpmv : Layout {
     double* y;
-    __device__ __forceinline__ void segment(Smem&, Stage&, int, int s0, int q, int, double acc, const double* const*) {
+    __device__ __forceinline__ Vals load(int) const { return Vals{}; }
+    __device__ __forceinline__ void segment(Smem&, int, int s0, int q, int, double acc, const Vals&) {
         y[s0 + q] = acc;
+    }
+};
+
+// Column-pass epilogue vectors: x, z, delta, c of column j.
+struct ColVecs : Layout {
+    const double* x_in;
+    const double* z_in;
+    const double* d_in;
+    const double* c;
+    __device__ __forceinline__ Vals load(int j) const {
+        const uint64_t pf = pass::pol_first();
+        Vals v{};
+        v.v[0] = pass::ld_first(x_in + j, pf);
+        v.v[1] = pass::ld_first(z_in + j, pf);
+        v.v[2] = pass::ld_first(d_in + j, pf);
+        v.v[3] = pass::ld_first(c + j, pf);
+        return v;
     }
 };
 
 // Column pass of the iteration: x_update (solver.py:168-176) in the reduced form
 // V(y + gamma/mu) = cnt*x + A^T h, then z = Proj_K(x+ - delta/mu), delta update.
 // CONES=false: all blocks of size 1 (cones.py:108-109 shortcut), fused per column.
-// CONES=true : x+ and w per column, then (group epilogue) one thread per cone.
+// CONES=true : x+, w, delta per column to shared memory, then (group epilogue) one thread per cone.
 template <bool CONES>
-struct ColIter : Layout {
+struct ColIter : ColVecs {
     static constexpr bool kGroupEpilogue = CONES;
     double* x;
     double* z;
@@ -170,10 +211,10 @@ struct ColIter : Layout {
     double* wbuf;
     double mu;
     pass::MuDiv div;
-    __device__ __forceinline__ void segment(Smem& sm, Stage&, int, int s0, int q, int cnt, double ath, const double* const* vb) {
+    __device__ __forceinline__ void segment(Smem& sm, int, int s0, int q, int cnt, double ath, const Vals& vv) {
         const int j = s0 + q;
         const double fv = cnt < pass::kFvTab ? sm.fvtab[cnt] : 1.0 / (1.0 + (double)cnt);   // uv.py:82
-        const double xj = vb[0][q], zj = vb[1][q], dj = vb[2][q], cj = vb[3][q];
+        const double xj = vv.v[0], zj = vv.v[1], dj = vv.v[2], cj = vv.v[3];
         const double dm = div(dj);
         double v = vterm ? vterm[j] : __dadd_rn(__dmul_rn((double)cnt, xj), ath);
         if (ccorr) v = v - ccorr[j];
@@ -186,16 +227,19 @@ struct ColIter : Layout {
             pass::st_hint(z + j, zp, pass::pol_first());
             pass::st_hint(delta + j, dp, pass::pol_first());
         } else {
-            sm.cscr[pass::group_id()][0][q] = xp;
-            sm.cscr[pass::group_id()][1][q] = w;
+            const int gi = pass::group_id();
+            sm.cscr[gi][0][q] = xp;
+            sm.cscr[gi][1][q] = w;
+            sm.cscr[gi][2][q] = dj;
         }
     }
-    __device__ __forceinline__ void group(Smem& sm, Stage&, int tile, int s0, int nseg, const double* const* vb) {
+    __device__ __forceinline__ void group(Smem& sm, int tile, int s0, int nseg) {
         const int gi = pass::group_id();
         const double* sxp = sm.cscr[gi][0];
         const double* sw = sm.cscr[gi][1];
-        double* sdn = sm.cscr[gi][2];
-        double* szp = sm.acc[gi];
+        const double* sd = sm.cscr[gi][2];
+        double* sdn = sm.cscr[gi][3];
+        double* szp = sm.wacc[gi];   // the warp transposes of this tile are done
         const int t = pass::group_tid();
         const int big = tile_big[tile];
         if (big >= 0) {  // piece of a cone wider than a tile: k_big_cone projects it
@@ -209,7 +253,7 @@ struct ColIter : Layout {
         for (int c = q0 + t; c < q1; c += kComputeThreads) {
             const int off = cone_ptr[c] - s0, size = cone_ptr[c + 1] - cone_ptr[c];
             project_block_dev(sw + off, size, szp + off);
-            for (int u = 0; u < size; ++u) sdn[off + u] = vb[2][off + u] + mu * (szp[off + u] - sxp[off + u]);
+            for (int u = 0; u < size; ++u) sdn[off + u] = sd[off + u] + mu * (szp[off + u] - sxp[off + u]);
         }
         pass::group_sync();
         for (int q = t; q < nseg; q += kComputeThreads) {
@@ -224,16 +268,16 @@ struct ColIter : Layout {
 // dual = atl + c, stat = dual - delta, pobj = c.x, cone_gap = max|x - z| and the
 // finiteness of x, z, delta and of the implicit y_k = x_j + a_k (b_i - r_i),
 // gamma_k = -a_k lam_i. Per-thread partials are reduced once per CTA (finish).
-struct ColReport : Layout {
+struct ColReport : ColVecs {
     static constexpr int kUnroll = 4;   // 8 report accumulators per thread: keep register pressure low
     const double* br;      // may be null
-    double* part;          // [kReportFieldsCol][gridDim.x]
+    double* part;          // [kReportFieldsCol][kGroups][gridDim.x]
     double d2, dmx, s2, smx, amx, cx, cg, nf;
     __device__ __forceinline__ void check(double a, int i, double lam_i) {
         if (!isfinite(a * lam_i) || (br && !isfinite(a * br[i]))) nf = 1.0;
     }
-    __device__ __forceinline__ void segment(Smem&, Stage&, int, int, int q, int, double atl, const double* const* vb) {
-        const double xj = vb[0][q], zj = vb[1][q], dj = vb[2][q], cj = vb[3][q];
+    __device__ __forceinline__ void segment(Smem&, int, int, int, int, double atl, const Vals& vv) {
+        const double xj = vv.v[0], zj = vv.v[1], dj = vv.v[2], cj = vv.v[3];
         const double dual = atl + cj;
         const double stat = dual - dj;
         d2 = d2 + dual * dual;
@@ -249,6 +293,7 @@ struct ColReport : Layout {
         const int G = gridDim.x;
         const double vals[8] = {d2, dmx, s2, smx, amx, cx, cg, nf};
         const bool is_sum[8] = {true, false, true, false, false, true, false, false};
+#pragma unroll
         for (int f = 0; f < 8; ++f) {
             const double v = is_sum[f] ? pass::group_reduce(vals[f], sm.red[pass::group_id()], SumOp())
                                        : pass::group_reduce(vals[f], sm.red[pass::group_id()], MaxOp());
@@ -551,11 +596,10 @@ template <bool CONES>
 ColIter<CONES> col_iter(cf_plan* p, const IterOpts& opt) {
     ColIter<CONES> c{};
     c.g_ = p->h.p;
-    c.nvec_ = 4;
-    c.vb_[0] = p->x.p;
-    c.vb_[1] = p->z.p;
-    c.vb_[2] = p->delta.p;
-    c.vb_[3] = p->c.p;
+    c.x_in = p->x.p;
+    c.z_in = p->z.p;
+    c.d_in = p->delta.p;
+    c.c = p->c.p;
     c.x = p->x.p;
     c.z = p->z.p;
     c.delta = p->delta.p;
@@ -617,21 +661,11 @@ int launch_iteration(cf_plan* p, const IterOpts& opt, const int32_t* done, int64
         r.g_ = p->x.p;
         r.seg_off = (int64_t)pn * m;
         r.last = (pn == p->n_panels - 1);
-        r.carry = p->ax.p;
-        int nv = 0;
-        if (r.last) {
-            r.vb_[0] = p->b.p - r.seg_off;
-            r.vb_[1] = p->lam.p - r.seg_off;
-            r.vb_[2] = p->fu.p - r.seg_off;
-            r.vb_[3] = p->db.p - r.seg_off;
-            nv = 4;
-        }
-        if (pn > 0) {
-            r.vb_[nv++] = p->ax.p - r.seg_off;
-            r.carry_src_ = p->ax.p - r.seg_off;
-            r.carry_ = true;
-        }
-        r.nvec_ = nv;
+        r.has_carry = pn > 0;
+        r.carry_buf = p->ax.p;
+        r.b = p->b.p;
+        r.fu = p->fu.p;
+        r.db = p->db.p;
         r.lam = p->lam.p;
         r.h = p->h.p;
         r.mu = opt.mu;
@@ -669,13 +703,8 @@ int launch_spmv_rows(cf_plan* p, const double* x, double* y) {
         RowSpmv r{};
         r.g_ = x;
         r.seg_off = (int64_t)pn * m;
+        r.has_carry = pn > 0;
         r.y = y;
-        if (pn > 0) {
-            r.vb_[0] = y - r.seg_off;
-            r.carry_src_ = y - r.seg_off;
-            r.nvec_ = 1;
-            r.carry_ = true;
-        }
         CF_TRY(launch_pass(r, row_jds(p), row_panel_tiles(p, pn), nullptr, p->stream));
     }
     return CF_OK;
@@ -714,11 +743,10 @@ int launch_report(cf_plan* p, double mu, bool ax_ready, const cf_config* cfg, in
         ColReport c{};
         c.d2 = c.dmx = c.s2 = c.smx = c.amx = c.cx = c.cg = c.nf = 0.0;
         c.g_ = p->lam.p;
-        c.nvec_ = 4;
-        c.vb_[0] = p->x.p;
-        c.vb_[1] = p->z.p;
-        c.vb_[2] = p->delta.p;
-        c.vb_[3] = p->c.p;
+        c.x_in = p->x.p;
+        c.z_in = p->z.p;
+        c.d_in = p->delta.p;
+        c.c = p->c.p;
         c.br = p->br_valid ? p->br.p : nullptr;
         c.part = p->part_col.p;
         CF_TRY(launch_pass(c, col_jds(p), col_tiles(p), done, p->stream, &g_col));

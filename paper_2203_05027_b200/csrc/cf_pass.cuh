@@ -1,27 +1,33 @@
-// Persistent, TMA-pipelined, jagged-diagonal tile engine for the sparse passes (sm_100a).
+// Persistent, TMA-pipelined, warp-local jagged-diagonal tile engine for the sparse passes (sm_100a).
 //
 // A pass walks one compressed layout (CSR panels for the row pass, CSC for the
 // column pass) tile by tile. A tile is a run of <= kPSeg segments (rows or
 // columns) with <= kPCap nonzeros, cut on the host (cf_setup.cu), or one
-// segment longer than kPCap ("long tile"). Inside a normal tile the nonzeros
-// are stored in JAGGED-DIAGONAL order (built once by k_build_jds): the tile's
-// segments are ranked by length (descending, stable), slot j holds segment
-// perm[j], and the k-th nonzero of slot j sits at joff[k] + j. So
-//   * thread j owns one segment: it gathers g[idx] for its nonzeros (8
+// segment longer than kMaxDiag ("long tile", streamed in chunks).
+//
+// Inside a normal tile every WARP BLOCK of 32 consecutive segments is stored
+// in jagged-diagonal order (k_build_jds): the block's segments are ranked by
+// length (descending, stable), rank r holds local segment perm[r], and the
+// k-th nonzero of rank r sits at joff_w[k] + r. So
+//   * lane r owns one segment: it gathers g[idx] for its nonzeros (kUnroll
 //     independent loads in flight) and sums the products SEQUENTIALLY in
 //     canonical order — np.bincount's order (uv.py:10-12), bit-identical;
-//   * a warp reads idx/val for 32 segments at consecutive shared-memory
-//     addresses (conflict-free), the k loop bound is warp-uniform and lanes
-//     drop out in length order (no product buffer, no reduction phase).
+//   * a warp reads idx/val of 32 segments at consecutive shared-memory
+//     addresses (conflict-free); lanes drop out in length order;
+//   * the rank -> natural-order transpose of the sums stays inside the warp, so
+//     the epilogue runs in natural segment order with no CTA barrier: its
+//     vectors are loaded straight from global memory (coalesced, issued at
+//     tile start so they arrive during the gathers) and its stores coalesce.
 // The L1TEX pipe's ~1 random sector per SM-cycle (the gathers) is then the
-// only hot resource besides HBM.
+// dominant consumer of the only hot on-chip resource.
 //
-// Warp roles: 1 producer warp issues cp.async.bulk (TMA 1D) of a future
-// tile's idx/val/perm/joff and its epilogue vectors into a kStages ring
-// (full[s] mbarrier, L2 evict-first hint on every streamed byte); kPSeg/32
-// compute warps consume (empty[s] when done). Compute warps progress through
-// tiles independently unless the policy needs a per-tile group barrier
-// (cones) or the tile is long (chunked through the stage by all of them).
+// Warp roles: per compute group (kPSeg threads) one producer warp issues
+// cp.async.bulk (TMA 1D) copies of a future tile's idx/val/perm/joff into the
+// group's slots of a kStages ring (full[s] mbarrier, L2 evict-first hint on
+// every streamed byte); the group's warps consume (empty[s] when done).
+// Groups alternate tiles; a group needs a barrier only for cone epilogues and
+// long tiles. The ring is kept small on purpose: shared memory beyond ~150 KB
+// per SM starves the L1 that the outstanding gathers need (profiles/r01_probes.md).
 #pragma once
 
 #include <cmath>
@@ -39,7 +45,7 @@ namespace pass {
 #define CF_GROUPS 2
 #endif
 #ifndef CF_UNROLL
-#define CF_UNROLL 12
+#define CF_UNROLL 20
 #endif
 #ifndef CF_PCAP
 #define CF_PCAP 2048
@@ -47,24 +53,24 @@ namespace pass {
 constexpr int kPCap = CF_PCAP;     // nonzeros per staged tile
 constexpr int kPSeg = 256;         // segments per tile (== threads of a compute group)
 constexpr int kMaxDiag = 256;      // longest segment inside a normal tile (longer ones get their own tile)
-constexpr int kStages = CF_STAGES; // ring depth
+constexpr int kStages = CF_STAGES; // ring depth (all groups)
 constexpr int kGroups = CF_GROUPS; // compute groups; group g consumes the CTA's tiles i = g, g+kGroups, ...
 constexpr int kUnroll = CF_UNROLL; // independent gathers in flight per thread
 constexpr int kComputeWarps = kPSeg / 32;      // per group
 constexpr int kComputeThreads = kPSeg;         // per group
 constexpr int kPThreads = kGroups * (kComputeThreads + 32);   // + one producer warp per group
-constexpr int kPVecs = 5;          // epilogue vectors staged per tile (incl. the panel carry)
+constexpr int kJoffHdr = 2 * kComputeWarps;    // per-warp {start, maxlen} header of a tile's joff
+constexpr int kJoffMax = kJoffHdr + kComputeWarps * (kMaxDiag + 1);
 constexpr int kFvTab = 256;
 static_assert(kStages % kGroups == 0, "a ring slot must be reused by the same compute group (mbarrier parity)");
 
 struct alignas(16) Stage {
     int32_t meta[4];                    // s0, nseg, k0, len (written by the producer)
-    int32_t meta2[4];                   // maxlen (0 = long tile), first joff entry
+    int32_t meta2[4];                   // joff length (0 = long tile), first joff entry
     int32_t idx[kPCap + 8];
     double val[kPCap + 4];
-    uint16_t perm[kPSeg + 16];
-    uint16_t joff[kMaxDiag + 16];
-    double vec[kPVecs][kPSeg + 4];
+    uint8_t perm[kPSeg + 16];
+    uint16_t joff[kJoffMax + 16];
 };
 
 struct Smem {
@@ -72,9 +78,9 @@ struct Smem {
     alignas(8) uint64_t full[kStages];
     alignas(8) uint64_t empty[kStages];
     double fvtab[kFvTab];               // 1/(1+cnt) for small column counts (uv.py:82)
-    double acc[kGroups][kPSeg];         // segment sums of the current tile, natural order
-    int32_t cnt[kGroups][kPSeg];        // segment lengths
-    double cscr[kGroups][3][kPSeg];     // cone epilogue: x+, w, delta+
+    double wacc[kGroups][kPSeg];        // rank -> natural transpose of the sums (warp-private slices)
+    int32_t wcnt[kGroups][kPSeg];
+    double cscr[kGroups][4][kPSeg];     // cone epilogue: x+, w, delta, delta+
     double red[kGroups][32];
 };
 
@@ -92,6 +98,11 @@ __host__ inline MuDiv make_mudiv(double mu) {
     MuDiv d{mu, 1.0 / mu, fr == 0.5 && e > -1000 && e < 1000};
     return d;
 }
+
+// Epilogue vectors of one segment, loaded by the policy (natural order, coalesced).
+struct Vals {
+    double v[5];
+};
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -137,6 +148,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+
 // compute group of the calling thread and its thread index inside the group
 __device__ __forceinline__ int group_id() { return (int)threadIdx.x / kComputeThreads; }
 __device__ __forceinline__ int group_tid() { return (int)threadIdx.x % kComputeThreads; }
@@ -167,6 +179,7 @@ __device__ __forceinline__ double ld_gather(const double* p, uint64_t pol) {
     asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
     return v;
 }
+// streamed once: no L1 allocation, L2 evict-first
 __device__ __forceinline__ double ld_first(const double* p, uint64_t pol) {
     double v;
     asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
@@ -200,64 +213,56 @@ __device__ __forceinline__ void copy_span(void* dst, const T* first, int64_t cou
     if (bytes) bulk_g2s(dst, (const void*)((uintptr_t)first & ~(uintptr_t)15u), bytes, bar, pol);
 }
 
-// Tile table: tb[t] = {first segment, first nonzero, first joff entry, maxlen (0 = long tile)};
+// Tile table: tb[t] = {first segment, first nonzero, first joff entry, joff length (0 = long tile)};
 // tile t spans [tb[t].x, tb[t+1].x) segments and [tb[t].y, tb[t+1].y) nonzeros.
 struct Tiles {
     const int4* tb;
     int32_t n_tiles;
 };
 
-// The JDS layout of a pass: idx/val in jagged-diagonal order inside every
-// normal tile (canonical order inside long tiles), perm (slot -> local
-// segment, indexed by segment position) and joff (per-tile diagonal starts).
+// The JDS layout of a pass: idx/val in warp-local jagged-diagonal order inside
+// every normal tile (canonical order inside long tiles); perm (rank -> local
+// segment of the warp block, one byte per segment position); joff per tile =
+// {start, maxlen} per warp block, then every block's diagonal starts
+// (tile-relative nonzero offsets).
 struct Jds {
     const int32_t* idx;
     const double* val;
-    const uint16_t* perm;
+    const uint8_t* perm;
     const uint16_t* joff;
 };
 
 // ---------------------------------------------------------------- the engine
 // P (the pass policy) provides (device):
-//   int nvec() const; const double* vec(int v) const  staged epilogue vectors, indexed by segment
-//   bool carry_in() const                              acc starts from staged vec[nvec()-1]
-//   const double* gvec() const                         gathered operand
-//   static constexpr bool kGroupEpilogue               epilogue needs all segments of the tile at once
-//   void check(double a, int j, double g)              per-nonzero hook (report finiteness)
-//   void segment(Smem&, Stage&, int tile, int s0, int q, int cnt, double acc, const double* const* vecb)
-//                                                      thread-level epilogue of local segment q
-//   void group(Smem&, Stage&, int tile, int s0, int nseg, const double* const* vecb)
-//                                                      (kGroupEpilogue) after group_sync
-//   void finish(Smem&)                                 compute threads, after the last tile
-template <class P>
-__device__ __forceinline__ void issue_tile(const P& p, const Jds& L, int4 lo, int4 hi, Stage& st, uint64_t* bar,
-                                           uint64_t pol) {
-    const int s0 = lo.x, nseg = hi.x - lo.x, k0 = lo.y, len = hi.y - lo.y, j0 = lo.z, maxlen = lo.w;
+//   const double* gvec() const                 gathered operand
+//   Vals load(int s) const                     epilogue vectors of segment s (global index, natural order)
+//   bool carry_in() const; double carry(const Vals&) const   starting value of a segment's sum
+//   static constexpr int kUnroll               gathers in flight per thread
+//   static constexpr bool kGroupEpilogue       epilogue needs all segments of the tile at once (cones)
+//   void check(double a, int j, double g)      per-nonzero hook (report finiteness)
+//   void segment(Smem&, int tile, int s0, int q, int cnt, double acc, const Vals&)
+//                                              epilogue of local segment q (natural order)
+//   void group(Smem&, int tile, int s0, int nseg)   (kGroupEpilogue) after a group barrier
+//   void finish(Smem&)                         compute threads, after the last tile
+__device__ __forceinline__ void issue_tile(const Jds& L, int4 lo, int4 hi, Stage& st, uint64_t* bar, uint64_t pol) {
+    const int s0 = lo.x, nseg = hi.x - lo.x, k0 = lo.y, len = hi.y - lo.y, j0 = lo.z, jn = lo.w;
     st.meta[0] = s0;
     st.meta[1] = nseg;
     st.meta[2] = k0;
     st.meta[3] = len;
-    st.meta2[0] = maxlen;
+    st.meta2[0] = jn;
     st.meta2[1] = j0;
-    const int nv = p.nvec();
-    uint32_t total = 0;
-    if (maxlen > 0) {
-        total += span_bytes(L.idx + k0, len) + span_bytes(L.val + k0, len);
-        total += span_bytes(L.perm + s0, nseg) + span_bytes(L.joff + j0, maxlen + 1);
+    if (jn == 0) {  // long tile: nothing staged (streamed by the consumers)
+        mbar_expect_tx(bar, 0);
+        return;
     }
-#pragma unroll
-    for (int v = 0; v < kPVecs; ++v)
-        if (v < nv) total += span_bytes(p.vec(v) + s0, nseg);
+    const uint32_t total = span_bytes(L.idx + k0, len) + span_bytes(L.val + k0, len) +
+                           span_bytes(L.perm + s0, nseg) + span_bytes(L.joff + j0, jn);
     mbar_expect_tx(bar, total);
-    if (maxlen > 0) {
-        copy_span(st.idx, L.idx + k0, len, bar, pol);
-        copy_span(st.val, L.val + k0, len, bar, pol);
-        copy_span(st.perm, L.perm + s0, nseg, bar, pol);
-        copy_span(st.joff, L.joff + j0, maxlen + 1, bar, pol);
-    }
-#pragma unroll
-    for (int v = 0; v < kPVecs; ++v)
-        if (v < nv) copy_span(st.vec[v], p.vec(v) + s0, nseg, bar, pol);
+    copy_span(st.idx, L.idx + k0, len, bar, pol);
+    copy_span(st.val, L.val + k0, len, bar, pol);
+    copy_span(st.perm, L.perm + s0, nseg, bar, pol);
+    copy_span(st.joff, L.joff + j0, jn, bar, pol);
 }
 
 template <class P>
@@ -270,7 +275,6 @@ __global__ void __launch_bounds__(kPThreads, 1) k_pass(const P p0, const Jds L, 
     const int my = (T.n_tiles > (int)blockIdx.x) ? (T.n_tiles - (int)blockIdx.x + G - 1) / G : 0;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int c = threadIdx.x; c < kFvTab; c += blockDim.x) sm.fvtab[c] = 1.0 / (1.0 + (double)c);
-    (void)warp;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&sm.full[s], 1);
@@ -281,13 +285,11 @@ __global__ void __launch_bounds__(kPThreads, 1) k_pass(const P p0, const Jds L, 
     __syncthreads();
 
     if (warp >= kGroups * kComputeWarps) {
-        // ------------------------------------------------ producers: warp kGroups*kComputeWarps + g feeds
-        // group g, whose tiles i = g, g+kGroups, ... use ring slots i % kStages (slot ≡ g mod kGroups)
+        // ------------------------------------------------ producers: warp kGroups*kComputeWarps + g feeds group g
         const int pg = warp - kGroups * kComputeWarps;
         if (lane == 0) {
             const uint64_t pf = pol_first();
-            // the tile-table entries of the next tile are loaded before waiting for its slot,
-            // so the copies start the moment the slot frees
+            // the next tile's table entries are loaded before waiting for its slot
             int4 lo = make_int4(0, 0, 0, 0), hi = lo;
             if (pg < my) {
                 lo = T.tb[blockIdx.x + pg * G];
@@ -304,7 +306,7 @@ __global__ void __launch_bounds__(kPThreads, 1) k_pass(const P p0, const Jds L, 
                     mbar_wait(&sm.empty[s], (uint32_t)(((i / kStages) - 1) & 1));
                     fence_proxy_async();
                 }
-                issue_tile(p, L, lo, hi, sm.st[s], &sm.full[s], pf);
+                issue_tile(L, lo, hi, sm.st[s], &sm.full[s], pf);
                 lo = nlo;
                 hi = nhi;
             }
@@ -316,44 +318,45 @@ __global__ void __launch_bounds__(kPThreads, 1) k_pass(const P p0, const Jds L, 
     const uint64_t pl = pol_last(), pf = pol_first();
     const double* __restrict__ g = p.gvec();
     const int grp = group_id();
-    const int j = group_tid();   // slot within the tile
-    const int gw = j >> 5;       // warp within the group
+    const int gt = group_tid();
+    const int gw = gt >> 5;      // warp within the group = warp block of the tile
+    double* wacc = sm.wacc[grp] + gw * 32;
+    int32_t* wcnt = sm.wcnt[grp] + gw * 32;
     for (int i = grp; i < my; i += kGroups) {
         const int s = i % kStages;
         Stage& st = sm.st[s];
         mbar_wait(&sm.full[s], (uint32_t)((i / kStages) & 1));
         const int s0 = st.meta[0], nseg = st.meta[1], k0 = st.meta[2], len = st.meta[3];
-        const int maxlen = st.meta2[0];
-        const int nv = p.nvec();
-        const double* vecb[kPVecs];
-#pragma unroll
-        for (int v = 0; v < kPVecs; ++v) vecb[v] = v < nv ? st.vec[v] + lead_of(p.vec(v) + s0) : nullptr;
-        // the carried partial is always the last staged vector (p.carry_src() = its global base)
-        const double* carry = p.carry_in() ? st.vec[nv - 1] + lead_of(p.carry_src() + s0) : nullptr;
+        const int jn = st.meta2[0];
         const int tile = (int)blockIdx.x + i * G;
-        if (maxlen > 0) {
-            const int32_t* ib = st.idx + lead_of(L.idx + k0);
-            const double* vb = st.val + lead_of(L.val + k0);
-            const uint16_t* pb = st.perm + lead_of(L.perm + s0);
-            const uint16_t* jb = st.joff + lead_of(L.joff + st.meta2[1]);
-            if (gw * 32 < nseg) {
-                const bool active = j < nseg;
-                const int q = active ? (int)pb[j] : 0;
-                double acc = (active && carry) ? carry[q] : 0.0;
+        if (jn > 0) {
+            const int nb = min(32, nseg - gw * 32);   // segments of this warp block
+            if (nb > 0) {
+                const int32_t* ib = st.idx + lead_of(L.idx + k0);
+                const double* vb = st.val + lead_of(L.val + k0);
+                const uint8_t* pb = st.perm + lead_of(L.perm + s0) + gw * 32;
+                const uint16_t* jh = st.joff + lead_of(L.joff + st.meta2[1]);
+                const uint16_t* jb = jh + jh[2 * gw];   // this block's diagonal starts
+                const int mlen = jh[2 * gw + 1];
+                const bool nat = lane < nb;             // natural segment gw*32 + lane exists
+                const Vals vv = nat ? p.load(s0 + gw * 32 + lane) : Vals{};
+                const int r = lane;                     // rank within the block
+                const int q = nat ? (int)pb[r] : 0;     // local segment (within the block) of rank r
+                const double c0 = p.carry_in() ? p.carry(vv) : 0.0;
+                double acc = __shfl_sync(0xffffffffu, c0, q);
                 int cnt = 0;
-                // lanes drop out in length order; the warp stops when its lane 0 is done
                 constexpr int U = P::kUnroll;
-                for (int k = 0; k < maxlen; k += U) {
+                for (int k = 0; k < mlen; k += U) {
                     int e[U];
                     bool ok[U];
                     bool any = false;
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         const int kk = k + u;
-                        const int a = kk < maxlen ? (int)jb[kk] : 0;
-                        const int b = kk < maxlen ? (int)jb[kk + 1] : 0;
-                        ok[u] = active && (b - a) > j;
-                        e[u] = a + j;
+                        const int a = kk < mlen ? (int)jb[kk] : 0;
+                        const int b = kk < mlen ? (int)jb[kk + 1] : 0;
+                        ok[u] = nat && (b - a) > r;
+                        e[u] = a + r;
                         any |= ok[u];
                     }
                     if (!__any_sync(0xffffffffu, any)) break;
@@ -374,27 +377,28 @@ __global__ void __launch_bounds__(kPThreads, 1) k_pass(const P p0, const Jds L, 
                             ++cnt;
                         }
                 }
-                if (active) {
-                    if (P::kGroupEpilogue) {
-                        sm.acc[grp][q] = acc;
-                        sm.cnt[grp][q] = cnt;
-                    } else {
-                        p.segment(sm, st, tile, s0, q, cnt, acc, vecb);   // slot order, no barrier
-                    }
+                // rank -> natural order inside the warp
+                if (nat) {
+                    wacc[q] = acc;
+                    wcnt[q] = cnt;
                 }
+                __syncwarp();
+                if (nat) p.segment(sm, tile, s0, gw * 32 + lane, wcnt[lane], wacc[lane], vv);
+                __syncwarp();
             }
         } else {
             // long tile: one segment [k0, k0+len), canonical order, chunked through the stage
             double* buf = st.val;
-            double* lacc = sm.acc[grp];
-            if (j == 0) {
-                lacc[0] = carry ? carry[0] : 0.0;
-                sm.cnt[grp][0] = len;
+            double* lacc = sm.wacc[grp];
+            Vals vv{};
+            if (gt == 0) {
+                vv = p.load(s0);
+                lacc[0] = p.carry_in() ? p.carry(vv) : 0.0;
             }
             group_sync();
             for (int c0 = 0; c0 < len; c0 += kPCap) {
                 const int cl = min(kPCap, len - c0);
-                for (int e = j; e < cl; e += kComputeThreads) {
+                for (int e = gt; e < cl; e += kComputeThreads) {
                     const int jj = ld_first(L.idx + k0 + c0 + e, pf);
                     const double a = ld_first(L.val + k0 + c0 + e, pf);
                     const double gj = ld_gather(g + jj, pl);
@@ -402,24 +406,20 @@ __global__ void __launch_bounds__(kPThreads, 1) k_pass(const P p0, const Jds L, 
                     buf[e] = __dmul_rn(a, gj);
                 }
                 group_sync();
-                if (j == 0) {
+                if (gt == 0) {
                     double acc = lacc[0];
                     for (int e = 0; e < cl; ++e) acc = __dadd_rn(acc, buf[e]);
                     lacc[0] = acc;
                 }
                 group_sync();
             }
-            if (!P::kGroupEpilogue && j == 0) p.segment(sm, st, tile, s0, 0, len, lacc[0], vecb);
+            if (gt == 0) p.segment(sm, tile, s0, 0, len, lacc[0], vv);
             group_sync();
         }
         if (P::kGroupEpilogue) {
-            // cones: every column of the tile first (natural order), then one thread per cone
             group_sync();
-            for (int q = j; q < nseg; q += kComputeThreads)
-                p.segment(sm, st, tile, s0, q, sm.cnt[grp][q], sm.acc[grp][q], vecb);
-            group_sync();
-            p.group(sm, st, tile, s0, nseg, vecb);
-            group_sync();   // sm.acc/cnt/cscr of this group are rewritten by its next tile
+            p.group(sm, tile, s0, nseg);
+            group_sync();   // cone scratch of this group is rewritten by its next tile
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[s]);

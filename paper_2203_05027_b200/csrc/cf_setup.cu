@@ -126,20 +126,26 @@ inline int bits_for(uint64_t maxval) {
     return b;
 }
 
-// Jagged-diagonal layout of one tile (see cf_pass.cuh): segments ranked by
-// length (descending, stable), perm[rank] = local segment, the k-th nonzero
-// of rank j at k0 + joff[k] + j. A long tile (maxlen == 0) is copied as is.
-__global__ void __launch_bounds__(256) k_build_jds(const int32_t* ptr, const int32_t* isrc, const double* vsrc,
-                                                   const int4* tb, int32_t* idst, double* vdst, uint16_t* perm,
-                                                   uint16_t* joff) {
-    __shared__ int len[kTileSeg];
-    __shared__ int rnk[kTileSeg];
-    __shared__ int width[kTileDiag + 1];
-    __shared__ int jo[kTileDiag + 2];
+// Warp-local jagged-diagonal layout of one tile (see cf_pass.cuh). Warp w
+// handles the block of segments [32w, 32w+32): ranks them by length
+// (descending, stable), writes perm[rank] = local segment (one byte per
+// segment position), the block's diagonal starts jo_w[k] (tile-relative) after
+// a per-warp {start, maxlen} header, and scatters the k-th nonzero of rank r to
+// k0 + jo_w[k] + r. A long tile (joff length 0) is copied as is.
+constexpr int kJoffHdr = 2 * (kTileSeg / 32);
+
+__global__ void __launch_bounds__(kTileSeg) k_build_jds(const int32_t* ptr, const int32_t* isrc,
+                                                        const double* vsrc, const int4* tb, int32_t* idst,
+                                                        double* vdst, uint8_t* perm, uint16_t* joff) {
+    constexpr int kW = kTileSeg / 32;
+    __shared__ int lens[kTileSeg];
+    __shared__ int bsum[kW], bmax[kW];
+    __shared__ int boff[kW + 1], bstart[kW + 1];
+    __shared__ int jo[kW][kTileDiag + 2];
     const int t = blockIdx.x;
     const int4 lo = tb[t], hi = tb[t + 1];
-    const int s0 = lo.x, nseg = hi.x - lo.x, k0 = lo.y, k1 = hi.y, j0 = lo.z, maxlen = lo.w;
-    if (maxlen == 0) {
+    const int s0 = lo.x, nseg = hi.x - lo.x, k0 = lo.y, k1 = hi.y, j0 = lo.z, jn = lo.w;
+    if (jn == 0) {
         for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
             idst[k] = isrc[k];
             vdst[k] = vsrc[k];
@@ -147,33 +153,64 @@ __global__ void __launch_bounds__(256) k_build_jds(const int32_t* ptr, const int
         if (threadIdx.x == 0) perm[s0] = 0;
         return;
     }
-    for (int q = threadIdx.x; q < nseg; q += blockDim.x) len[q] = ptr[s0 + q + 1] - ptr[s0 + q];
-    __syncthreads();
-    for (int q = threadIdx.x; q < nseg; q += blockDim.x) {
-        int r = 0;
-        const int lq = len[q];
-        for (int q2 = 0; q2 < nseg; ++q2) r += (len[q2] > lq) || (len[q2] == lq && q2 < q);
-        rnk[q] = r;
-        perm[s0 + r] = (uint16_t)q;
+    const int w = threadIdx.x >> 5, r = threadIdx.x & 31;
+    const int q = threadIdx.x;
+    const bool valid = q < nseg;
+    const int len = valid ? ptr[s0 + q + 1] - ptr[s0 + q] : -1;
+    lens[q] = len;
+    // rank inside the warp block: longer first, ties in segment order
+    int rank = 0;
+    for (int r2 = 0; r2 < 32; ++r2) {
+        const int l2 = __shfl_sync(0xffffffffu, len, r2);
+        rank += (l2 > len) || (l2 == len && r2 < r);
     }
-    for (int k = threadIdx.x; k < maxlen; k += blockDim.x) {
-        int w = 0;
-        for (int q = 0; q < nseg; ++q) w += len[q] > k;
-        width[k] = w;
+    if (valid) perm[s0 + q] = 0;  // (overwritten below; keeps the byte defined)
+    __syncwarp();
+    if (valid) perm[s0 + w * 32 + rank] = (uint8_t)r;
+    int sum = valid ? len : 0, mx = valid ? len : 0;
+    for (int off = 16; off > 0; off >>= 1) {
+        sum += __shfl_xor_sync(0xffffffffu, sum, off);
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    }
+    if (r == 0) {
+        bsum[w] = sum;
+        bmax[w] = mx;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        jo[0] = 0;
-        for (int k = 0; k < maxlen; ++k) jo[k + 1] = jo[k] + width[k];
+        boff[0] = 0;
+        bstart[0] = kJoffHdr;
+        for (int b = 0; b < kW; ++b) {
+            const bool nonempty = b * 32 < nseg;
+            boff[b + 1] = boff[b] + (nonempty ? bsum[b] : 0);
+            bstart[b + 1] = bstart[b] + (nonempty ? bmax[b] + 1 : 0);
+            joff[j0 + 2 * b] = (uint16_t)(nonempty ? bstart[b] : 0);
+            joff[j0 + 2 * b + 1] = (uint16_t)(nonempty ? bmax[b] : 0);
+        }
     }
     __syncthreads();
-    for (int k = threadIdx.x; k <= maxlen; k += blockDim.x) joff[j0 + k] = (uint16_t)jo[k];
-    for (int q = threadIdx.x; q < nseg; q += blockDim.x) {
-        const int src0 = ptr[s0 + q], r = rnk[q];
-        for (int kk = 0; kk < len[q]; ++kk) {
-            const int dst = k0 + jo[kk] + r;
-            idst[dst] = isrc[src0 + kk];
-            vdst[dst] = vsrc[src0 + kk];
+    if (w * 32 < nseg) {
+        const int mlen = bmax[w];
+        // width of diagonal k = number of segments of the block longer than k
+        for (int k = r; k < mlen; k += 32) {
+            int wd = 0;
+            for (int r2 = 0; r2 < 32; ++r2) wd += lens[w * 32 + r2] > k;
+            jo[w][k + 1] = wd;
+        }
+        __syncwarp();
+        if (r == 0) {
+            jo[w][0] = boff[w];
+            for (int k = 0; k < mlen; ++k) jo[w][k + 1] += jo[w][k];
+        }
+        __syncwarp();
+        for (int k = r; k <= mlen; k += 32) joff[j0 + bstart[w] + k] = (uint16_t)jo[w][k];
+        if (valid) {
+            const int src0 = ptr[s0 + q];
+            for (int kk = 0; kk < len; ++kk) {
+                const int dst = k0 + jo[w][kk] + rank;
+                idst[dst] = isrc[src0 + kk];
+                vdst[dst] = vsrc[src0 + kk];
+            }
         }
     }
 }
@@ -195,7 +232,7 @@ void tile_starts(const std::vector<int32_t>& ptr, int64_t s_begin, int64_t s_end
     }
 }
 
-// tile table {s0, k0, joff start, maxlen} from tile starts (+ the final end segment)
+// tile table {s0, k0, joff start, joff length (0 = long tile)} from tile starts (+ the end segment)
 void tile_table(const std::vector<int32_t>& ptr, const std::vector<int64_t>& starts, int64_t s_end,
                 std::vector<int4>& tb, int64_t& joff_total) {
     tb.clear();
@@ -203,20 +240,24 @@ void tile_table(const std::vector<int32_t>& ptr, const std::vector<int64_t>& sta
     for (size_t t = 0; t < starts.size(); ++t) {
         const int64_t s0 = starts[t], s1 = (t + 1 < starts.size()) ? starts[t + 1] : s_end;
         const int64_t nnz = ptr[s1] - ptr[s0];
-        int maxlen = 0;
-        if (!(s1 - s0 == 1 && (nnz > kTileNnz || nnz > kTileDiag))) {
-            for (int64_t q = s0; q < s1; ++q) maxlen = std::max<int>(maxlen, ptr[q + 1] - ptr[q]);
-            maxlen = std::max(maxlen, 1);
+        int64_t jn = 0;
+        if (!(s1 - s0 == 1 && nnz > kTileDiag)) {
+            jn = kJoffHdr;
+            for (int64_t b0 = s0; b0 < s1; b0 += 32) {
+                int64_t mx = 0;
+                for (int64_t q = b0; q < std::min(s1, b0 + 32); ++q) mx = std::max<int64_t>(mx, ptr[q + 1] - ptr[q]);
+                jn += mx + 1;
+            }
         }
-        tb.push_back(make_int4((int)s0, ptr[s0], (int)joff_total, maxlen));
-        if (maxlen > 0) joff_total += maxlen + 1;
+        tb.push_back(make_int4((int)s0, ptr[s0], (int)joff_total, (int)jn));
+        joff_total += jn;
     }
     tb.push_back(make_int4((int)s_end, ptr[s_end], (int)joff_total, 0));
 }
 
 int build_jds(cf_plan* p, const int32_t* ptr, const int32_t* isrc, const double* vsrc, const std::vector<int4>& tb,
               int64_t nseg_total, int64_t joff_total, DevBuf<int4>& dtb, DevBuf<int32_t>& idst,
-              DevBuf<double>& vdst, DevBuf<uint16_t>& perm, DevBuf<uint16_t>& joff) {
+              DevBuf<double>& vdst, DevBuf<uint8_t>& perm, DevBuf<uint16_t>& joff) {
     CF_TRY(dtb.alloc(tb.size()));
     CF_CUDA(cudaMemcpyAsync(dtb.p, tb.data(), tb.size() * sizeof(int4), cudaMemcpyHostToDevice, p->stream));
     CF_TRY(idst.alloc(p->o));
@@ -225,7 +266,8 @@ int build_jds(cf_plan* p, const int32_t* ptr, const int32_t* isrc, const double*
     CF_TRY(joff.alloc(joff_total));
     const int64_t ntiles = (int64_t)tb.size() - 1;
     if (ntiles > 0) {
-        k_build_jds<<<(unsigned)ntiles, 256, 0, p->stream>>>(ptr, isrc, vsrc, dtb.p, idst.p, vdst.p, perm.p, joff.p);
+        k_build_jds<<<(unsigned)ntiles, kTileSeg, 0, p->stream>>>(ptr, isrc, vsrc, dtb.p, idst.p, vdst.p, perm.p,
+                                                                   joff.p);
         CF_LAUNCHED();
     }
     return CF_OK;
