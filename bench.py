@@ -54,6 +54,8 @@ CONFIGS = {
                workload="C3: synthetic SOCP m=2,000,000 n=4,000,000 o=40,000,000, 1,000,000 K4 cones fp64"),
     "c1": dict(m=1000, n=2000, density=0.01, cone_kind="lp",
                workload="C1: synthetic sparse LP m=1,000 n=2,000 o=20,000 fp64"),
+    "c4": dict(m=100, n=200, density=0.05, cone_kind="lp", batch=4096,
+               workload="C4: batch of 4096 independent sparse LPs m=100 n=200 o=1,000 (5%) fp64, seeds 0..4095"),
 }
 CPU_SAMPLE_SCALE = 20  # the CPU baseline runs a 1/20-scale instance of the same structure
 
@@ -345,6 +347,61 @@ def run_ours(args, spec, rank, world, local_rank):
     return 0
 
 
+def run_batch(args, spec, rank, world):
+    """C4: solve_batch over 4096 generated problems; value = problem-iterations/s of the batch kernel."""
+    import numpy as np
+
+    from paper_2203_05027_b200 import GenSpec, SolverConfig, generate, solve_batch
+
+    P = spec["batch"]
+    probs = [generate(GenSpec(spec["m"], spec["n"], spec["density"], spec["cone_kind"], seed=s)) for s in range(P)]
+    cfg = SolverConfig(eps_prim=args.eps, eps_dual=args.eps, eps_gap=args.eps)
+    solve_batch(probs[:64], SolverConfig(max_iters=100), trace=False)   # warm-up
+    tim = {}
+    t0 = time.perf_counter()
+    res = solve_batch(probs, cfg, trace=False, timing=tim)
+    t1 = time.perf_counter()
+    iters = np.array([r.report.iter for r in res])
+    total = int(iters.sum())
+    value = total / (tim["kernel_ms"] / 1000.0)
+    statuses = {}
+    for r in res:
+        statuses[r.report.status] = statuses.get(r.report.status, 0) + 1
+    cpu = None
+    if not args.skip_cpu:
+        import oracle
+
+        ts, its = 0.0, 0
+        t_start = time.perf_counter()
+        for s in range(P):
+            tt = time.perf_counter()
+            _, _, tr, _ = oracle.solve(probs[s], cfg, max_wall_s=args.cpu_budget)
+            ts += time.perf_counter() - tt
+            its += tr[-1]["iter"]
+            if time.perf_counter() - t_start > args.cpu_budget:
+                break
+        cpu = {"value": its / ts, "unit": "problem-iterations/s", "cores": 1, "kind": "port",
+               "sample": f"oracle port solving problems 0..{s} of the batch to eps={args.eps} (or the budget) "
+                         f"one after another: {its} iterations in {ts:.1f} s"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "problem-iterations/s", "n_gpus": world, "steps": 1,
+        "warmup": args.warmup, "ms_per_step": tim["kernel_ms"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator, seeds 0..4095)",
+        "config": {"workload": spec["workload"], "problems": P, "parallelism": "one CTA per problem"},
+        "gpu_launches": 1,
+        "time_to_tol": {"seconds": tim["kernel_ms"] / 1000.0, "iters_total": total, "iters_median": float(np.median(iters)),
+                        "iters_max": int(iters.max()), "statuses": statuses, "eps": args.eps},
+        "e2e": {"value": total / (t1 - t0), "unit": "problem-iterations/s", "seconds": t1 - t0,
+                "h2d_bytes_per_step": int(sum(24 * p.A.nnz + 8 * (p.m + p.n) for p in probs)),
+                "d2h_bytes_per_step": int(sum(8 * (p.m + p.n) for p in probs)),
+                "step": "one solve_batch(4096 problems) from host numpy buffers"},
+        "cpu_baseline": cpu,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -375,6 +432,8 @@ def main():
         torch.cuda.set_device(local_rank)
         tdist.init_process_group("nccl")
     try:
+        if "batch" in spec:
+            return run_batch(args, spec, rank, world)
         return run_ours(args, spec, rank, world, local_rank)
     finally:
         if world > 1:

@@ -166,6 +166,26 @@ int cf_apply_At(cf_plan* plan, const double* y_dev, double* x_dev);
 /* project_product (cones.py:103-110) of a device n-vector onto the plan's cone. */
 int cf_project(cf_plan* plan, const double* w_dev, double* out_dev);
 
+/* ---------------------------------------------------------------- batch
+ * cf_batch_solve: many independent problems, each solved like cf_plan_solve
+ * (the reference's batch mechanism is a process pool over solve(),
+ * bench.py:96-106). The problems are passed as ONE block-diagonal problem:
+ * problem p owns rows [row_off[p], row_off[p+1]) and columns
+ * [col_off[p], col_off[p+1]) (host arrays of P+1, row_off[0] = col_off[0] = 0);
+ * rows/cols/vals (o triplets, any order), b, c and the cone blocks are the
+ * concatenation (no cone may cross a problem boundary). cfgs: one cf_config per
+ * problem (its norm-dependent bounds from that problem's b, c). Outputs (host):
+ * x_out (N), lam_out (M), final_reports / n_reports (P), and optionally the
+ * first trace_cap reports of every problem in trace (P*trace_cap; NULL if 0).
+ * One CTA per problem keeps it in shared memory; a problem that does not fit
+ * returns CF_EINVAL. elapsed_ms: device time of the solve kernel. */
+int cf_batch_solve(int64_t n_problems, const int64_t* row_off, const int64_t* col_off, int64_t o,
+                   const int64_t* rows, const int64_t* cols, const double* vals,
+                   const double* b, const double* c, int64_t n_blocks, const int64_t* block_sizes,
+                   const cf_config* cfgs, double* x_out, double* lam_out,
+                   cf_report* final_reports, int32_t* n_reports, cf_report* trace, int64_t trace_cap,
+                   cf_problem_checks* checks, double* elapsed_ms);
+
 /* ---------------------------------------------------------------- timing
  * CUDA-event time of the last cf_plan_iterate / cf_plan_solve loop (ms),
  * kernel launches issued by it, and the event time of row/col passes when

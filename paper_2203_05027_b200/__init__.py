@@ -14,6 +14,7 @@ from .api import (
     SolverState,
     check_termination,
     solve,
+    solve_batch,
 )
 from .engine import DevicePlan
 from .instances import GeneratedInstance, GenSpec, generate, generate_witnessed, shape_for_nnz
@@ -38,5 +39,6 @@ __all__ = [
     "generate_witnessed",
     "shape_for_nnz",
     "solve",
+    "solve_batch",
     "validate",
 ]

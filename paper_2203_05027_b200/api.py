@@ -30,6 +30,7 @@ from .engine import DevicePlan, ProblemRejected, config_struct
 from .problem import cone_sizes_array, validate
 
 __all__ = [
+    "solve_batch",
     "SolverConfig",
     "SolverState",
     "IterationReport",
@@ -226,3 +227,91 @@ def solve(p, cfg: SolverConfig | None = None, init: SolverState | None = None) -
         return run_plan(plan, p, cfg)
     finally:
         plan.close()
+
+
+def solve_batch(problems, cfg: SolverConfig | None = None, trace: bool = True, timing: dict | None = None) -> list:
+    """Solve many independent problems at once: ``[solve(p, cfg) for p in problems]``.
+
+    The reference batches with a process pool over ``solve`` (bench.py:96-106);
+    here every problem is solved by one CTA that keeps it in shared memory
+    (csrc/cf_batch.cu, SURVEY config C4), with per-problem termination. Each
+    result is the SolveResult ``solve(p, cfg)`` returns (same iterates,
+    statuses and iteration counts; ``trace=False`` keeps only the final report).
+    Problems too large for one CTA's shared memory raise ValueError (use solve).
+    ``timing``, if given, receives the device time of the solve kernel.
+    """
+    import ctypes
+
+    from . import _lib
+    from ._lib import CfChecks, CfReport, check, lib
+    from .engine import config_struct, report_to_dict
+
+    cfg = cfg or SolverConfig()
+    problems = list(problems)
+    P = len(problems)
+    if P == 0:
+        return []
+    for i, p in enumerate(problems):
+        if not _host_shapes_ok(p):
+            rep = validate(p)
+            raise ValueError(f"problem {i}: invalid problem: " + "; ".join(rep.violations[:3]))
+    ms = np.array([p.A.num_rows for p in problems], dtype=np.int64)
+    ns = np.array([p.A.num_cols for p in problems], dtype=np.int64)
+    row_off = np.concatenate(([0], np.cumsum(ms))).astype(np.int64)
+    col_off = np.concatenate(([0], np.cumsum(ns))).astype(np.int64)
+    rows = np.concatenate([np.asarray(p.A.rows, np.int64) + row_off[i] for i, p in enumerate(problems)])
+    cols = np.concatenate([np.asarray(p.A.cols, np.int64) + col_off[i] for i, p in enumerate(problems)])
+    vals = np.concatenate([np.asarray(p.A.vals, np.float64) for p in problems])
+    b = np.concatenate([np.asarray(p.b, np.float64) for p in problems])
+    c = np.concatenate([np.asarray(p.c, np.float64) for p in problems])
+    sizes = np.concatenate([cone_sizes_array(p.cones) for p in problems]).astype(np.int64)
+    bn = [norms(p.b) for p in problems]
+    cn = [norms(p.c) for p in problems]
+    cfgs = (_lib.CfConfig * P)(*[config_struct(cfg, bn[i], cn[i]) for i in range(P)])
+    M, N = int(row_off[-1]), int(col_off[-1])
+    x = np.empty(N)
+    lam = np.empty(M)
+    finals = (CfReport * P)()
+    nrep = np.zeros(P, dtype=np.int32)
+    cap = -(-int(cfg.max_iters) // int(cfg.check_every)) if trace else 0
+    if trace and P * cap * ctypes.sizeof(CfReport) > (4 << 30):
+        raise ValueError("solve_batch: the full traces would need more than 4 GiB; pass trace=False")
+    tr = (CfReport * max(P * cap, 1))()
+    chk = CfChecks()
+    el = ctypes.c_double()
+
+    def ptr(a):
+        return ctypes.c_void_p(a.ctypes.data) if a.size else ctypes.c_void_p(0)
+
+    rc = lib().cf_batch_solve(P, ptr(row_off), ptr(col_off), int(vals.size), ptr(rows), ptr(cols), ptr(vals),
+                              ptr(b), ptr(c), int(sizes.size), ptr(sizes), cfgs, ptr(x), ptr(lam), finals,
+                              ptr(nrep), tr if cap else None, cap, ctypes.byref(chk), ctypes.byref(el))
+    if rc == _lib.CF_EPROBLEM:
+        for i, p in enumerate(problems):
+            rep = validate(p)
+            if not rep.ok:
+                raise ValueError(f"problem {i}: invalid problem: " + "; ".join(rep.violations[:3]))
+    check(rc, "cf_batch_solve")
+    if timing is not None:
+        timing["kernel_ms"] = el.value
+    out = []
+    for i, p in enumerate(problems):
+        def host_report(d):
+            rep = _to_report(d)
+            status = _decide(rep, cfg, bn[i], cn[i])
+            if status == "running" and rep.iter == cfg.max_iters:
+                status = "max_iters"
+            if status != d["status"]:
+                raise RuntimeError(f"problem {i}: device termination ({d['status']}) disagrees with "
+                                   f"check_termination ({status}) at iteration {rep.iter}")
+            return replace(rep, status=status)
+
+        final = host_report(report_to_dict(finals[i]))
+        if cap:
+            k = int(nrep[i])
+            reps = tuple(host_report(report_to_dict(tr[i * cap + j])) for j in range(k))
+        else:
+            reps = (final,)
+        out.append(SolveResult(x=x[col_off[i]:col_off[i + 1]].copy(), lam=lam[row_off[i]:row_off[i + 1]].copy(),
+                               report=final, trace=reps))
+    return out

@@ -1,0 +1,432 @@
+// Batched solver (SURVEY §2 "Batched solver", config C4): many independent small
+// problems, each solved by ONE CTA that keeps the problem's CSR + CSC copy and all
+// iterates in shared memory and runs the whole loop of solve() (solver.py:309-334)
+// with per-problem termination. Persistent CTAs pull problems from an atomic queue,
+// so a problem that needs 100k iterations does not hold up the others.
+//
+// The batch is set up as ONE block-diagonal problem through the plan's device
+// setup (validate + canonical sort + CSR), so problem p owns rows
+// [row_off[p], row_off[p+1]) and columns [col_off[p], col_off[p+1]) and its CSR
+// and CSC slices are contiguous. Arithmetic is that of the plan's passes:
+// sequential canonical-order sums (bit-identical to np.bincount), the same
+// epilogue expressions, the same report assembly and termination test
+// (cf_report.cuh). The reference's batch mechanism is a process pool over
+// solve() (bench.py:96-106); solve_batch() returns what [solve(p) for p in ps]
+// returns.
+#include <algorithm>
+#include <cmath>
+
+#include "cf_common.h"
+#include "cf_report.cuh"
+
+namespace cf {
+namespace {
+
+constexpr int kBT = 256;   // threads per problem CTA
+
+struct BatchArgs {
+    int32_t P;
+    const int64_t* row_off;   // P+1
+    const int64_t* col_off;   // P+1
+    const int64_t* cone_off;  // P+1 first cone of each problem (cones mode)
+    const int32_t* rowptr;
+    const int32_t* colidx;
+    const double* valr;
+    const int32_t* colptr;
+    const int32_t* rowidx;
+    const double* valc;
+    const double* b;
+    const double* c;
+    const double* fu;
+    const double* db;
+    const int32_t* cone_ptr;
+    int32_t cones;            // 0: all blocks of size 1
+    const cf_config* cfg;     // per problem
+    double* x_out;
+    double* lam_out;
+    cf_report* trace;         // [P][trace_cap]
+    int64_t trace_cap;
+    int32_t* n_reports;       // [P]
+    cf_report* final_report;  // [P]
+    int32_t* queue;
+    int32_t cap_m, cap_n, cap_o, cap_k;   // smem capacities (rows, cols, nonzeros, cones)
+};
+
+__device__ __forceinline__ double nanmax_b(double a, double b) { return (a > b || a != a) ? a : b; }
+
+template <bool MAX>
+__device__ double block_reduce_b(double v, double* sh) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const double o = __shfl_xor_sync(0xffffffffu, v, off);
+        v = MAX ? nanmax_b(v, o) : v + o;
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        v = (l < kBT / 32) ? sh[l] : 0.0;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const double o = __shfl_xor_sync(0xffffffffu, v, off);
+            v = MAX ? nanmax_b(v, o) : v + o;
+        }
+    }
+    return v;   // valid in thread 0
+}
+
+__device__ __forceinline__ void project_block_b(const double* w, int q, double* out) {
+    const double w0 = w[0];
+    double ssq = 0.0;
+    for (int t = 1; t < q; ++t) ssq = __dadd_rn(ssq, __dmul_rn(w[t], w[t]));
+    const double alpha = sqrt(ssq);
+    if (alpha <= -w0) {
+        for (int t = 0; t < q; ++t) out[t] = 0.0;
+    } else if (alpha <= w0) {
+        for (int t = 0; t < q; ++t) out[t] = w[t];
+    } else {
+        const double factor = w0 / (2.0 * alpha);
+        for (int t = 1; t < q; ++t) out[t] = __dadd_rn(__dmul_rn(0.5, w[t]), __dmul_rn(factor, w[t]));
+        out[0] = __dadd_rn(__dmul_rn(0.5, w0), __dmul_rn(0.5, alpha));
+    }
+}
+
+__global__ void __launch_bounds__(kBT) k_batch(const BatchArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int CM = a.cap_m, CN = a.cap_n, CO = a.cap_o;
+    // shared-memory carve-up (doubles first)
+    double* valr = reinterpret_cast<double*>(smem);
+    double* valc = valr + CO;
+    double* b = valc + CO;
+    double* fu = b + CM;
+    double* db = fu + CM;
+    double* lam = db + CM;
+    double* h = lam + CM;
+    double* br = h + CM;
+    double* ax = br + CM;
+    double* c = ax + CM;
+    double* x = c + CN;
+    double* z = x + CN;
+    double* dl = z + CN;
+    double* wv = dl + CN;     // cones: x+ - delta/mu, then z+
+    double* red = wv + CN;    // 32
+    int32_t* colidx = reinterpret_cast<int32_t*>(red + 32);
+    int32_t* rowidx = colidx + CO;
+    int32_t* rowptr = rowidx + CO;
+    int32_t* colptr = rowptr + CM + 1;
+    int32_t* cptr = colptr + CN + 1;   // cone offsets (local), cap_k + 1
+    __shared__ int32_t s_prob, s_status;
+    const int t = threadIdx.x;
+
+    for (;;) {
+        if (t == 0) s_prob = atomicAdd(a.queue, 1);
+        __syncthreads();
+        const int pid = s_prob;
+        if (pid >= a.P) break;
+        const int64_t r0 = a.row_off[pid], c0 = a.col_off[pid];
+        const int m = (int)(a.row_off[pid + 1] - r0), n = (int)(a.col_off[pid + 1] - c0);
+        const int64_t kr0 = a.rowptr[r0], kc0 = a.colptr[c0];
+        const int o = (int)(a.colptr[c0 + n] - kc0);
+        const cf_config cfg = a.cfg[pid];
+        const double mu = cfg.mu;
+        // ---- load the problem (canonical CSC, CSR, vectors) and a cold start (solver.py:309)
+        for (int i = t; i <= m; i += kBT) rowptr[i] = (int32_t)(a.rowptr[r0 + i] - kr0);
+        for (int j = t; j <= n; j += kBT) colptr[j] = (int32_t)(a.colptr[c0 + j] - kc0);
+        for (int k = t; k < o; k += kBT) {
+            colidx[k] = (int32_t)(a.colidx[kr0 + k] - c0);
+            valr[k] = a.valr[kr0 + k];
+            rowidx[k] = (int32_t)(a.rowidx[kc0 + k] - r0);
+            valc[k] = a.valc[kc0 + k];
+        }
+        for (int i = t; i < m; i += kBT) {
+            b[i] = a.b[r0 + i];
+            fu[i] = a.fu[r0 + i];
+            db[i] = a.db[r0 + i];
+            lam[i] = 0.0;
+            h[i] = 0.0;
+            br[i] = 0.0;
+        }
+        for (int j = t; j < n; j += kBT) {
+            c[j] = a.c[c0 + j];
+            x[j] = 0.0;
+            z[j] = 0.0;
+            dl[j] = 0.0;
+        }
+        int nk = 0;
+        if (a.cones) {
+            const int64_t q0 = a.cone_off[pid];
+            nk = (int)(a.cone_off[pid + 1] - q0);
+            for (int q = t; q <= nk; q += kBT) cptr[q] = (int32_t)(a.cone_ptr[q0 + q] - c0);
+        }
+        if (t == 0) s_status = CF_STATUS_RUNNING;
+        __syncthreads();
+        int nrep = 0;
+        cf_report last{};
+        for (int64_t k = 1; k <= cfg.max_iters; ++k) {
+            const bool report = (k % cfg.check_every == 0) || (k == cfg.max_iters);
+            // ---- column pass: x_update, z_update, delta update (solver.py:168-176,186-188,196)
+            for (int j = t; j < n; j += kBT) {
+                const int p0 = colptr[j], p1 = colptr[j + 1];
+                double ath = 0.0;
+                for (int q = p0; q < p1; ++q) ath = __dadd_rn(ath, __dmul_rn(valc[q], h[rowidx[q]]));
+                const int cnt = p1 - p0;
+                const double fv = 1.0 / (1.0 + (double)cnt);
+                const double xj = x[j], zj = z[j], dj = dl[j], cj = c[j];
+                const double dm = dj / mu;
+                const double v = __dadd_rn(__dmul_rn((double)cnt, xj), ath);
+                const double xp = fv * (((v + zj) + dm) - cj / mu);
+                const double w = xp - dm;
+                x[j] = xp;
+                if (!a.cones) {
+                    const double zp = w > 0.0 ? w : 0.0;
+                    z[j] = zp;
+                    dl[j] = dj + mu * (zp - xp);
+                } else {
+                    wv[j] = w;
+                }
+            }
+            if (a.cones) {
+                __syncthreads();
+                for (int q = t; q < nk; q += kBT) {
+                    const int off = cptr[q], size = cptr[q + 1] - off;
+                    project_block_b(wv + off, size, z + off);
+                    for (int u = 0; u < size; ++u) dl[off + u] = dl[off + u] + mu * (z[off + u] - x[off + u]);
+                }
+            }
+            __syncthreads();
+            // ---- row pass: y_update + lam/gamma of dual_update (solver.py:179-183,194-195)
+            for (int i = t; i < m; i += kBT) {
+                const int p0 = rowptr[i], p1 = rowptr[i + 1];
+                double axi = 0.0;
+                for (int q = p0; q < p1; ++q) axi = __dadd_rn(axi, __dmul_rn(valr[q], x[colidx[q]]));
+                const double bi = b[i];
+                const double r = fu[i] * (db[i] + axi);
+                const double ln = lam[i] + mu * (r - bi);
+                const double bmr = bi - r;
+                lam[i] = ln;
+                h[i] = bmr - ln / mu;
+                if (report) {
+                    br[i] = bmr;
+                    ax[i] = axi;
+                }
+            }
+            __syncthreads();
+            if (!report) continue;
+            // ---- compute_report (solver.py:206-242)
+            double prim2 = 0.0, primi = 0.0, axm = 0.0, blam = 0.0, nfr = 0.0;
+            for (int i = t; i < m; i += kBT) {
+                const double pr = ax[i] - b[i];
+                prim2 = prim2 + pr * pr;
+                primi = nanmax_b(primi, fabs(pr));
+                axm = nanmax_b(axm, fabs(ax[i]));
+                blam = blam + b[i] * lam[i];
+                if (!isfinite(lam[i])) nfr = 1.0;
+            }
+            double d2 = 0.0, dmx = 0.0, s2 = 0.0, smx = 0.0, amx = 0.0, cx = 0.0, cg = 0.0, nfc = 0.0;
+            for (int j = t; j < n; j += kBT) {
+                double atl = 0.0;
+                for (int q = colptr[j]; q < colptr[j + 1]; ++q) {
+                    const int i = rowidx[q];
+                    const double pa = __dmul_rn(valc[q], lam[i]);
+                    if (!isfinite(pa) || !isfinite(valc[q] * br[i])) nfc = 1.0;
+                    atl = __dadd_rn(atl, pa);
+                }
+                const double dual = atl + c[j];
+                const double stat = dual - dl[j];
+                d2 = d2 + dual * dual;
+                dmx = nanmax_b(dmx, fabs(dual));
+                s2 = s2 + stat * stat;
+                smx = nanmax_b(smx, fabs(stat));
+                amx = nanmax_b(amx, fabs(atl));
+                cx = cx + c[j] * x[j];
+                cg = nanmax_b(cg, fabs(x[j] - z[j]));
+                if (!isfinite(x[j]) || !isfinite(z[j]) || !isfinite(dl[j])) nfc = 1.0;
+            }
+            ReportFields f;
+            f.prim2 = block_reduce_b<false>(prim2, red);
+            f.prim_inf = block_reduce_b<true>(primi, red);
+            f.ax_inf = block_reduce_b<true>(axm, red);
+            f.blam = block_reduce_b<false>(blam, red);
+            f.nf_row = block_reduce_b<true>(nfr, red);
+            f.dual2 = block_reduce_b<false>(d2, red);
+            f.dual_inf = block_reduce_b<true>(dmx, red);
+            f.stat2 = block_reduce_b<false>(s2, red);
+            f.stat_inf = block_reduce_b<true>(smx, red);
+            f.atl_inf = block_reduce_b<true>(amx, red);
+            f.pobj = block_reduce_b<false>(cx, red);
+            f.cone_gap = block_reduce_b<true>(cg, red);
+            f.nf_col = block_reduce_b<true>(nfc, red);
+            if (t == 0) {
+                cf_report r = assemble_report(f, k, false);
+                r.status = decide_status(r, cfg, k);
+                if (nrep < a.trace_cap) a.trace[(int64_t)pid * a.trace_cap + nrep] = r;
+                ++nrep;
+                last = r;
+                s_status = r.status;
+            }
+            __syncthreads();
+            if (s_status != CF_STATUS_RUNNING) break;
+        }
+        // ---- SolveResult (solver.py:329-334)
+        for (int j = t; j < n; j += kBT) a.x_out[c0 + j] = x[j];
+        for (int i = t; i < m; i += kBT) a.lam_out[r0 + i] = lam[i];
+        if (t == 0) {
+            a.final_report[pid] = last;
+            a.n_reports[pid] = nrep;
+        }
+        __syncthreads();
+    }
+}
+
+size_t batch_smem(int cm, int cn, int co, int ck) {
+    return sizeof(double) * (size_t)(2 * co + 7 * cm + 5 * cn + 32) +
+           sizeof(int32_t) * (size_t)(2 * co + cm + 1 + cn + 1 + ck + 1) + 16;
+}
+
+}  // namespace
+}  // namespace cf
+
+using namespace cf;
+
+extern "C" int cf_batch_solve(int64_t n_problems, const int64_t* row_off, const int64_t* col_off, int64_t o,
+                              const int64_t* rows, const int64_t* cols, const double* vals, const double* b,
+                              const double* c, int64_t n_blocks, const int64_t* block_sizes,
+                              const cf_config* cfgs, double* x_out, double* lam_out, cf_report* final_reports,
+                              int32_t* n_reports, cf_report* trace, int64_t trace_cap, cf_problem_checks* checks,
+                              double* elapsed_ms) {
+    if (n_problems < 1 || !row_off || !col_off || !cfgs || !x_out || !lam_out || !final_reports || !n_reports ||
+        trace_cap < 0 || (trace_cap > 0 && !trace)) {
+        set_error("cf_batch_solve: bad arguments");
+        return CF_EINVAL;
+    }
+    const int64_t P = n_problems, M = row_off[P], N = col_off[P];
+    if (row_off[0] != 0 || col_off[0] != 0 || P >= INT32_MAX) {
+        set_error("cf_batch_solve: offsets must start at 0");
+        return CF_EINVAL;
+    }
+    int cap_m = 0, cap_n = 0;
+    for (int64_t p = 0; p < P; ++p) {
+        if (row_off[p + 1] < row_off[p] || col_off[p + 1] < col_off[p]) {
+            set_error("cf_batch_solve: offsets must be non-decreasing");
+            return CF_EINVAL;
+        }
+        cap_m = std::max<int>(cap_m, (int)(row_off[p + 1] - row_off[p]));
+        cap_n = std::max<int>(cap_n, (int)(col_off[p + 1] - col_off[p]));
+        if (cfgs[p].max_iters < 1 || cfgs[p].check_every < 1 || !(cfgs[p].mu > 0)) {
+            set_error("cf_batch_solve: invalid config of problem " + std::to_string(p));
+            return CF_EINVAL;
+        }
+    }
+    // one block-diagonal plan: device validate + canonical CSC + CSR (single panel, no pass tiles)
+    cf_plan* plan = nullptr;
+    int rc = cf_plan_create_mode(M, N, o, rows, cols, vals, b, c, n_blocks, block_sizes, 0, nullptr, checks,
+                                 /*batch_mode=*/1, &plan);
+    if (rc != CF_OK) return rc;
+    struct Guard {
+        cf_plan* p;
+        ~Guard() { cf_plan_destroy(p); }
+    } guard{plan};
+    cudaStream_t st = plan->stream;
+    // per-problem nonzeros and cones
+    std::vector<int32_t> cp(N + 1);
+    CF_CUDA(cudaMemcpyAsync(cp.data(), plan->colptr.p, (N + 1) * 4, cudaMemcpyDeviceToHost, st));
+    CF_CUDA(cudaStreamSynchronize(st));
+    int cap_o = 0;
+    for (int64_t p = 0; p < P; ++p) cap_o = std::max<int>(cap_o, cp[col_off[p + 1]] - cp[col_off[p]]);
+    std::vector<int64_t> cone_off(P + 1, 0);
+    int cap_k = 0;
+    if (!plan->all_unit) {
+        std::vector<int64_t> starts(n_blocks + 1, 0);
+        for (int64_t q = 0; q < n_blocks; ++q) starts[q + 1] = starts[q] + block_sizes[q];
+        for (int64_t p = 0; p <= P; ++p) {
+            const auto it = std::lower_bound(starts.begin(), starts.end(), col_off[p]);
+            if (it == starts.end() || *it != col_off[p]) {
+                set_error("cf_batch_solve: a cone block crosses the boundary of problem " + std::to_string(p));
+                return CF_EINVAL;
+            }
+            cone_off[p] = it - starts.begin();
+        }
+        for (int64_t p = 0; p < P; ++p) cap_k = std::max<int>(cap_k, (int)(cone_off[p + 1] - cone_off[p]));
+    }
+    const size_t smem = batch_smem(cap_m, cap_n, cap_o, cap_k);
+    int dev = 0, max_smem = 0, sms = 0;
+    CF_CUDA(cudaGetDevice(&dev));
+    CF_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    CF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (smem > (size_t)max_smem) {
+        set_error("cf_batch_solve: the largest problem needs " + std::to_string(smem) +
+                  " bytes of shared memory (> " + std::to_string(max_smem) + "); solve it with cf_plan_solve");
+        return CF_EINVAL;
+    }
+    CF_CUDA(cudaFuncSetAttribute(k_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_batch, kBT, smem));
+    const int grid = (int)std::min<int64_t>(P, (int64_t)std::max(per_sm, 1) * sms);
+    // device-side arguments and outputs
+    DevBuf<int64_t> d_roff, d_coff, d_koff;
+    DevBuf<cf_config> d_cfg;
+    DevBuf<double> d_x, d_lam;
+    DevBuf<cf_report> d_final, d_trace;
+    DevBuf<int32_t> d_nrep, d_queue;
+    CF_TRY(d_roff.alloc(P + 1));
+    CF_TRY(d_coff.alloc(P + 1));
+    CF_TRY(d_koff.alloc(P + 1));
+    CF_TRY(d_cfg.alloc(P));
+    CF_TRY(d_x.alloc(N));
+    CF_TRY(d_lam.alloc(M));
+    CF_TRY(d_final.alloc(P));
+    CF_TRY(d_trace.alloc(std::max<int64_t>(1, P * trace_cap)));
+    CF_TRY(d_nrep.alloc(P));
+    CF_TRY(d_queue.alloc(1));
+    CF_CUDA(cudaMemcpyAsync(d_roff.p, row_off, (P + 1) * 8, cudaMemcpyHostToDevice, st));
+    CF_CUDA(cudaMemcpyAsync(d_coff.p, col_off, (P + 1) * 8, cudaMemcpyHostToDevice, st));
+    CF_CUDA(cudaMemcpyAsync(d_koff.p, cone_off.data(), (P + 1) * 8, cudaMemcpyHostToDevice, st));
+    CF_CUDA(cudaMemcpyAsync(d_cfg.p, cfgs, P * sizeof(cf_config), cudaMemcpyHostToDevice, st));
+    CF_CUDA(cudaMemsetAsync(d_queue.p, 0, 4, st));
+    BatchArgs a{};
+    a.P = (int32_t)P;
+    a.row_off = d_roff.p;
+    a.col_off = d_coff.p;
+    a.cone_off = d_koff.p;
+    a.rowptr = plan->rowptr.p;
+    a.colidx = plan->colidx.p;
+    a.valr = plan->valr.p;
+    a.colptr = plan->colptr.p;
+    a.rowidx = plan->rowidx.p;
+    a.valc = plan->valc.p;
+    a.b = plan->b.p;
+    a.c = plan->c.p;
+    a.fu = plan->fu.p;
+    a.db = plan->db.p;
+    a.cone_ptr = plan->cone_ptr.p;
+    a.cones = plan->all_unit ? 0 : 1;
+    a.cfg = d_cfg.p;
+    a.x_out = d_x.p;
+    a.lam_out = d_lam.p;
+    a.trace = d_trace.p;
+    a.trace_cap = trace_cap;
+    a.n_reports = d_nrep.p;
+    a.final_report = d_final.p;
+    a.queue = d_queue.p;
+    a.cap_m = cap_m;
+    a.cap_n = cap_n;
+    a.cap_o = cap_o;
+    a.cap_k = cap_k;
+    CF_CUDA(cudaEventRecord(plan->ev0, st));
+    k_batch<<<grid, kBT, smem, st>>>(a);
+    CF_LAUNCHED();
+    CF_CUDA(cudaEventRecord(plan->ev1, st));
+    CF_CUDA(cudaEventSynchronize(plan->ev1));
+    float ms = 0.f;
+    CF_CUDA(cudaEventElapsedTime(&ms, plan->ev0, plan->ev1));
+    if (elapsed_ms) *elapsed_ms = ms;
+    CF_CUDA(cudaMemcpyAsync(x_out, d_x.p, N * 8, cudaMemcpyDeviceToHost, st));
+    CF_CUDA(cudaMemcpyAsync(lam_out, d_lam.p, M * 8, cudaMemcpyDeviceToHost, st));
+    CF_CUDA(cudaMemcpyAsync(final_reports, d_final.p, P * sizeof(cf_report), cudaMemcpyDeviceToHost, st));
+    CF_CUDA(cudaMemcpyAsync(n_reports, d_nrep.p, P * 4, cudaMemcpyDeviceToHost, st));
+    if (trace_cap > 0)
+        CF_CUDA(cudaMemcpyAsync(trace, d_trace.p, P * trace_cap * sizeof(cf_report), cudaMemcpyDeviceToHost, st));
+    CF_CUDA(cudaStreamSynchronize(st));
+    return CF_OK;
+}

@@ -87,6 +87,7 @@ struct DevBuf {
 // reduced two-pass iteration.
 struct cf_plan {
     int64_t m = 0, n = 0, o = 0;
+    bool batch_mode = false;        // built for cf_batch_solve: one CSR panel, no pass tiles
     cudaStream_t stream = nullptr;
     bool own_stream = false;
 
@@ -155,6 +156,12 @@ struct cf_plan {
 };
 
 namespace cf {
+
+// plan creation with an optional batch mode (cf_setup.cu)
+int cf_plan_create_mode(int64_t m, int64_t n, int64_t o, const int64_t* rows, const int64_t* cols, const double* vals,
+                        const double* b, const double* c, int64_t n_blocks, const int64_t* block_sizes,
+                        int inputs_on_device, void* stream, cf_problem_checks* checks, int batch_mode,
+                        cf_plan** out);
 
 // ---------------------------------------------------------------- launch wrappers (cf_kernels.cu)
 struct IterOpts {

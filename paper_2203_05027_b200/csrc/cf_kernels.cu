@@ -22,6 +22,7 @@
 
 #include "cf_common.h"
 #include "cf_pass.cuh"
+#include "cf_report.cuh"
 
 namespace cf {
 namespace {
@@ -423,42 +424,9 @@ __global__ void __launch_bounds__(1024) k_finalize(const FinalizeArgs a) {
     f[11] = reduce_partials(a.part_col + 6 * a.g_col, a.g_col, sh, mx);
     f[12] = reduce_partials(a.part_col + 7 * a.g_col, a.g_col, sh, mx);
     if (threadIdx.x != 0) return;
-    cf_report r;
-    r.iter = a.k;
-    r.prim_res_inf = f[1];
-    r.prim_res_2 = sqrt(f[0]);
-    r.dual_res_inf = f[6];
-    r.dual_res_2 = sqrt(f[5]);
-    r.stat_res_inf = f[8];
-    r.stat_res_2 = sqrt(f[7]);
-    r.ax_inf = f[2];
-    r.atl_inf = f[9];
-    r.cone_gap = f[11];
-    r.pobj = f[10];
-    const double blam = f[3];
-    r.dobj = -blam;
-    r.gap = r.pobj + blam;
-    r.nonfinite = (f[4] > 0.0 || f[12] > 0.0 || (a.nf_flag && *a.nf_flag)) ? 1 : 0;
-    int status = r.nonfinite ? CF_STATUS_DIVERGED : CF_STATUS_RUNNING;
-    if (a.check && status == CF_STATUS_RUNNING) {
-        const cf_config& c = a.cfg;
-        bool ok;
-        if (c.term_mode == CF_TERM_OSQP) {
-            // Python max(a, b) returns a unless b > a
-            const double mp = (c.b_inf > r.ax_inf) ? c.b_inf : r.ax_inf;
-            const double md = (c.c_inf > r.atl_inf) ? c.c_inf : r.atl_inf;
-            const double ep = c.eps_abs + c.eps_rel * mp;
-            const double ed = c.eps_abs + c.eps_rel * md;
-            ok = (r.prim_res_inf < ep) && (r.stat_res_inf < ed);
-        } else if (c.term_mode == CF_TERM_SCS) {
-            ok = (r.prim_res_2 <= c.scs_prim_bound) && (r.stat_res_2 <= c.scs_dual_bound) &&
-                 (fabs(r.gap) <= c.eps_gap * ((1.0 + fabs(r.pobj)) + fabs(r.dobj)));
-        } else {
-            ok = (r.prim_res_2 < c.target_prim_res) && (fabs(r.gap) < c.target_gap);
-        }
-        status = ok ? CF_STATUS_SOLVED : CF_STATUS_RUNNING;
-        if (status == CF_STATUS_RUNNING && a.k == c.max_iters) status = CF_STATUS_MAX_ITERS;
-    }
+    const ReportFields rf{f[0], f[1], f[2], f[3], f[4], f[5], f[6], f[7], f[8], f[9], f[10], f[11], f[12]};
+    cf_report r = assemble_report(rf, a.k, a.nf_flag && *a.nf_flag);
+    int status = a.check ? decide_status(r, a.cfg, a.k) : r.status;
     r.status = status;
     *a.slot = r;
     if (a.done && status != CF_STATUS_RUNNING) *a.done = 1;

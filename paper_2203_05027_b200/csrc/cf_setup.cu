@@ -460,6 +460,7 @@ int build(cf_plan* p, const int64_t* rows, const int64_t* cols, const double* va
         if (panels < 1) panels = 1;
         if (panels > 64) panels = 64;
         if ((int64_t)panels * m >= (int64_t)INT32_MAX) panels = 1;  // tile segment ids are int32
+        if (p->batch_mode) panels = 1;                                // the batched kernel reads plain CSR
         p->n_panels = panels;
         p->panel_cols = std::max<int64_t>(1, (n + panels - 1) / panels);
     }
@@ -545,7 +546,15 @@ int build(cf_plan* p, const int64_t* rows, const int64_t* cols, const double* va
     for (int64_t q = 0; q < nb; ++q) maxsize = std::max(maxsize, sizes[q]);
     p->all_unit = (nb == 0 || maxsize == 1);
     clk.mark("row diag");
-    CF_TRY(build_tiles(p, sizes, nb));
+    if (!p->batch_mode) {
+        CF_TRY(build_tiles(p, sizes, nb));
+    } else if (!p->all_unit) {
+        std::vector<int32_t> cone_ptr(nb + 1, 0);
+        for (int64_t q = 0; q < nb; ++q) cone_ptr[q + 1] = cone_ptr[q] + (int32_t)sizes[q];
+        CF_TRY(p->cone_ptr.alloc(nb + 1));
+        CF_CUDA(cudaMemcpyAsync(p->cone_ptr.p, cone_ptr.data(), (nb + 1) * 4, cudaMemcpyHostToDevice, st));
+        CF_CUDA(cudaStreamSynchronize(st));
+    }
     clk.mark("tiles + jds");
 
     // ---- iterate state (SolverState.zeros, solver.py:118-127) and report buffers
@@ -588,6 +597,14 @@ extern "C" int cf_plan_create(int64_t m, int64_t n, int64_t o, const int64_t* ro
                               const double* vals, const double* b, const double* c, int64_t n_blocks,
                               const int64_t* block_sizes, int inputs_on_device, void* stream,
                               cf_problem_checks* checks, cf_plan** out) {
+    return cf::cf_plan_create_mode(m, n, o, rows, cols, vals, b, c, n_blocks, block_sizes, inputs_on_device, stream,
+                                   checks, 0, out);
+}
+
+int cf::cf_plan_create_mode(int64_t m, int64_t n, int64_t o, const int64_t* rows, const int64_t* cols,
+                            const double* vals, const double* b, const double* c, int64_t n_blocks,
+                            const int64_t* block_sizes, int inputs_on_device, void* stream,
+                            cf_problem_checks* checks, int batch_mode, cf_plan** out) {
     using namespace cf;
     if (!out) {
         set_error("cf_plan_create: out is NULL");
@@ -631,6 +648,7 @@ extern "C" int cf_plan_create(int64_t m, int64_t n, int64_t o, const int64_t* ro
     p->m = m;
     p->n = n;
     p->o = o;
+    p->batch_mode = batch_mode != 0;
     if (stream) {
         p->stream = (cudaStream_t)stream;
     } else {

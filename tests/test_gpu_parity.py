@@ -338,3 +338,31 @@ def test_row_panels_bit_identical(monkeypatch):
     ref = solve(q, cfg)
     np.testing.assert_array_equal(res.x, ref.x)
     assert res.trace == ref.trace
+
+
+def test_solve_batch_matches_solve():
+    """Batched solver (C4): every problem's result equals solve(p) (same iterates, statuses, counts)."""
+    from paper_2203_05027_b200 import GenSpec, SolverConfig, generate, solve, solve_batch
+
+    specs = [GenSpec(30, 60, 0.05, "lp", seed=s) for s in range(6)] + \
+            [GenSpec(20, 48, 0.08, "socp4", seed=s) for s in range(3)] + [GenSpec(5, 9, 0.4, "lp", seed=99)]
+    probs = [generate(s) for s in specs]
+    cfg = SolverConfig(eps_prim=1e-4, eps_dual=1e-4, eps_gap=1e-4, max_iters=5000)
+    batch = solve_batch(probs, cfg)
+    for p, rb in zip(probs, batch):
+        rs = solve(p, cfg)
+        assert rb.report.status == rs.report.status and rb.report.iter == rs.report.iter
+        np.testing.assert_array_equal(rb.x, rs.x)       # same sequential arithmetic as the plan passes
+        np.testing.assert_array_equal(rb.lam, rs.lam)
+        assert len(rb.trace) == len(rs.trace)
+        for a, b in zip(rb.trace, rs.trace):
+            assert a.status == b.status and a.iter == b.iter
+            for fld in REPORT_FIELDS[1:]:
+                assert _scalar_rel(getattr(a, fld), getattr(b, fld)) <= 1e-12
+    # against the oracle too (C4 shape: 100 x 200, 5 %)
+    q = generate(GenSpec(100, 200, 0.05, "lp", seed=3))
+    cfg2 = SolverConfig(max_iters=3000)
+    rb = solve_batch([q], cfg2)[0]
+    ox, olam, otrace, _ = oracle.solve(q, cfg2)
+    assert rb.report.status == otrace[-1]["status"] and rb.report.iter == otrace[-1]["iter"]
+    assert rel_err(rb.x, ox) <= 1e-8 and rel_err(rb.lam, olam) <= 1e-8
