@@ -186,6 +186,43 @@ int cf_batch_solve(int64_t n_problems, const int64_t* row_off, const int64_t* co
                    cf_report* final_reports, int32_t* n_reports, cf_report* trace, int64_t trace_cap,
                    cf_problem_checks* checks, double* elapsed_ms);
 
+/* ---------------------------------------------------------------- row-sharded building blocks
+ * Used by paper_2203_05027_b200/sharded.py (config C5: A's rows split over
+ * ranks, one exchange per iteration). A rank's plan holds its row block and ALL
+ * columns; per iteration the driver runs
+ *   cf_apply_At(h) -> reduce-scatter -> cf_column_update on the rank's column
+ *   slice -> all-gather x into the plan's x -> cf_plan_row_step.
+ * Reports: cf_plan_row_parts + (cf_apply_At(lam) -> reduce-scatter ->
+ * cf_column_parts), all-reduced, then the host assembles compute_report. */
+#define CF_VEC_X 0
+#define CF_VEC_Z 1
+#define CF_VEC_DELTA 2
+#define CF_VEC_LAM 3
+#define CF_VEC_H 4
+#define CF_VEC_AX 5
+#define CF_VEC_B 6
+#define CF_VEC_C 7
+/* device pointer and length of one of the plan's vectors */
+int cf_plan_vector(cf_plan* plan, int which, double** ptr, int64_t* len);
+/* per-column nonzero counts of the plan (n doubles, device) */
+int cf_plan_column_counts(cf_plan* plan, double* cnt_dev);
+/* the row pass of one iteration (y_update + lam/gamma updates, solver.py:179-183,194-195)
+ * with the plan's current x; report=1 also keeps A x for cf_plan_row_parts */
+int cf_plan_row_step(cf_plan* plan, double mu, int report);
+/* row part of compute_report over the plan's rows: out = {sum (Ax-b)^2, max|Ax-b|,
+ * max|Ax|, sum b*lam, nonfinite(lam)} (host array of 5) */
+int cf_plan_row_parts(cf_plan* plan, double* out5);
+/* x_update + z_update + delta update (solver.py:168-176,186-188,196) on a column slice
+ * from the reduced A^T h: all device arrays of n; cone_ptr (device, n_blocks+1,
+ * slice-local offsets) or NULL for the orthant; vterm (optional) replaces cnt*x + ath. */
+int cf_column_update(int64_t n, const double* ath, const double* cnt, const double* c, double* x,
+                     double* z, double* delta, double mu, int64_t n_blocks, const int32_t* cone_ptr,
+                     void* stream);
+/* column part of compute_report on a slice from the reduced A^T lam: out = {sum dual^2,
+ * max|dual|, sum stat^2, max|stat|, max|A^T lam|, sum c*x, max|x-z|, nonfinite} (host, 8) */
+int cf_column_parts(int64_t n, const double* atl, const double* c, const double* x, const double* z,
+                    const double* delta, double* out8, void* stream);
+
 /* ---------------------------------------------------------------- timing
  * CUDA-event time of the last cf_plan_iterate / cf_plan_solve loop (ms),
  * kernel launches issued by it, and the event time of row/col passes when

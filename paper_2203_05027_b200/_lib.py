@@ -103,6 +103,12 @@ SIGNATURES = {
     "cf_apply_At": (c_int, [_P, _P, _P]),
     "cf_project": (c_int, [_P, _P, _P]),
     "cf_plan_last_timing": (c_int, [_P, _D, _I64, _D, _D, _I64]),
+    "cf_plan_vector": (c_int, [_P, c_int, POINTER(c_void_p), _I64]),
+    "cf_plan_column_counts": (c_int, [_P, _P]),
+    "cf_plan_row_step": (c_int, [_P, c_double, c_int]),
+    "cf_plan_row_parts": (c_int, [_P, _P]),
+    "cf_column_update": (c_int, [c_int64, _P, _P, _P, _P, _P, _P, c_double, c_int64, _P, _P]),
+    "cf_column_parts": (c_int, [c_int64, _P, _P, _P, _P, _P, _P, _P]),
     "cf_batch_solve": (c_int, [c_int64, _P, _P, c_int64, _P, _P, _P, _P, _P, c_int64, _P, _P, _P, _P, _P, _P, _P,
                                c_int64, POINTER(CfChecks), _D]),
     "cf_plan_set_profiling": (c_int, [_P, c_int]),

@@ -383,6 +383,72 @@ int cf_project(cf_plan* p, const double* w_dev, double* out_dev) {
     return CF_OK;
 }
 
+int cf_plan_vector(cf_plan* p, int which, double** ptr, int64_t* len) {
+    CF_TRY(check_plan(p, "cf_plan_vector"));
+    if (!ptr || !len) {
+        set_error("cf_plan_vector: NULL output");
+        return CF_EINVAL;
+    }
+    switch (which) {
+        case CF_VEC_X: *ptr = p->x.p; *len = p->n; break;
+        case CF_VEC_Z: *ptr = p->z.p; *len = p->n; break;
+        case CF_VEC_DELTA: *ptr = p->delta.p; *len = p->n; break;
+        case CF_VEC_LAM: *ptr = p->lam.p; *len = p->m; break;
+        case CF_VEC_H: *ptr = p->h.p; *len = p->m; break;
+        case CF_VEC_AX: *ptr = p->ax.p; *len = p->m; break;
+        case CF_VEC_B: *ptr = p->b.p; *len = p->m; break;
+        case CF_VEC_C: *ptr = p->c.p; *len = p->n; break;
+        default: set_error("cf_plan_vector: unknown vector"); return CF_EINVAL;
+    }
+    return CF_OK;
+}
+
+int cf_plan_column_counts(cf_plan* p, double* cnt_dev) {
+    CF_TRY(check_plan(p, "cf_plan_column_counts"));
+    CF_TRY(launch_counts(p, cnt_dev));
+    CF_CUDA(cudaStreamSynchronize(p->stream));
+    return CF_OK;
+}
+
+int cf_plan_row_step(cf_plan* p, double mu, int report) {
+    CF_TRY(check_plan(p, "cf_plan_row_step"));
+    CF_TRY(check_mu(mu, "cf_plan_row_step"));
+    // the row half of launch_iteration: the column update already happened on the slices
+    IterOpts opt;
+    opt.mu = mu;
+    opt.report = report != 0;
+    CF_TRY(launch_row_only(p, opt));
+    p->br_valid = opt.report || p->keep_br;
+    return CF_OK;
+}
+
+int cf_plan_row_parts(cf_plan* p, double* out5) {
+    CF_TRY(check_plan(p, "cf_plan_row_parts"));
+    DevBuf<double> d;
+    CF_TRY(d.alloc(5));
+    CF_TRY(launch_row_parts(p, d.p));
+    CF_CUDA(cudaMemcpyAsync(out5, d.p, 5 * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+    CF_CUDA(cudaStreamSynchronize(p->stream));
+    return CF_OK;
+}
+
+int cf_column_update(int64_t n, const double* ath, const double* cnt, const double* c, double* x, double* z,
+                     double* delta, double mu, int64_t n_blocks, const int32_t* cone_ptr, void* stream) {
+    CF_TRY(check_mu(mu, "cf_column_update"));
+    CF_TRY(launch_col_update(n, ath, cnt, c, x, z, delta, mu, n_blocks, cone_ptr, (cudaStream_t)stream));
+    return CF_OK;
+}
+
+int cf_column_parts(int64_t n, const double* atl, const double* c, const double* x, const double* z,
+                    const double* delta, double* out8, void* stream) {
+    DevBuf<double> d;
+    CF_TRY(d.alloc(8));
+    CF_TRY(launch_col_parts(n, atl, c, x, z, delta, d.p, (cudaStream_t)stream));
+    CF_CUDA(cudaMemcpyAsync(out8, d.p, 8 * sizeof(double), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    CF_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    return CF_OK;
+}
+
 int cf_plan_last_timing(const cf_plan* p, double* loop_ms, int64_t* launches, double* row_pass_ms,
                         double* col_pass_ms, int64_t* timed_iters) {
     CF_TRY(check_plan(p, "cf_plan_last_timing"));

@@ -171,6 +171,8 @@ struct IterOpts {
     const double* ccorr = nullptr;
     const double* rcorr = nullptr;
 };
+// the row pass of one iteration (all column panels)
+int launch_row_only(cf_plan* p, const IterOpts& opt, const int32_t* done = nullptr, int64_t* launches = nullptr);
 // one iteration (col pass + cones + row pass); returns kernel launches issued via *launches
 int launch_iteration(cf_plan* p, const IterOpts& opt, const int32_t* done, int64_t* launches);
 // y = A x (rows), x = A^T y (cols)
@@ -185,6 +187,13 @@ int launch_warm_start(cf_plan* p, double mu);
 // setup helpers
 int launch_row_diag(cf_plan* p);
 int max_col_report_ctas();
+// row-sharded building blocks
+int launch_col_update(int64_t n, const double* ath, const double* cnt, const double* c, double* x, double* z,
+                      double* delta, double mu, int64_t n_blocks, const int32_t* cone_ptr, cudaStream_t st);
+int launch_col_parts(int64_t n, const double* atl, const double* c, const double* x, const double* z,
+                     const double* delta, double* out8_dev, cudaStream_t st);
+int launch_row_parts(cf_plan* p, double* out5_dev);
+int launch_counts(cf_plan* p, double* cnt);
 // profiling: reset before a loop, fold the recorded per-pass event times after its final sync
 void prof_reset(cf_plan* p);
 void prof_collect(cf_plan* p);

@@ -585,6 +585,33 @@ ColIter<CONES> col_iter(cf_plan* p, const IterOpts& opt) {
 }  // namespace
 
 // ---------------------------------------------------------------- launch wrappers
+int launch_row_only(cf_plan* p, const IterOpts& opt, const int32_t* done, int64_t* launches) {
+    int64_t nl = 0;
+    const int64_t m = p->m;
+    for (int pn = 0; pn < p->n_panels && m > 0; ++pn) {
+        RowIter r{};
+        r.g_ = p->x.p;
+        r.seg_off = (int64_t)pn * m;
+        r.last = (pn == p->n_panels - 1);
+        r.has_carry = pn > 0;
+        r.carry_buf = p->ax.p;
+        r.b = p->b.p;
+        r.fu = p->fu.p;
+        r.db = p->db.p;
+        r.lam = p->lam.p;
+        r.h = p->h.p;
+        r.mu = opt.mu;
+        r.div = pass::make_mudiv(opt.mu);
+        r.rcorr = opt.rcorr;
+        r.br = (opt.report || p->keep_br) ? p->br.p : nullptr;
+        r.ax = opt.report ? p->ax.p : nullptr;
+        CF_TRY(launch_pass(r, row_jds(p), row_panel_tiles(p, pn), done, p->stream));
+        ++nl;
+    }
+    if (launches) *launches += nl;
+    return CF_OK;
+}
+
 int launch_iteration(cf_plan* p, const IterOpts& opt, const int32_t* done, int64_t* launches) {
     int64_t nl = 0;
     cudaEvent_t e_a = nullptr, e_b = nullptr, e_c = nullptr;
@@ -623,27 +650,7 @@ int launch_iteration(cf_plan* p, const IterOpts& opt, const int32_t* done, int64
         }
     }
     if (p->profiling) CF_CUDA(cudaEventRecord(e_b, p->stream));
-    const int64_t m = p->m;
-    for (int pn = 0; pn < p->n_panels && m > 0; ++pn) {
-        RowIter r{};
-        r.g_ = p->x.p;
-        r.seg_off = (int64_t)pn * m;
-        r.last = (pn == p->n_panels - 1);
-        r.has_carry = pn > 0;
-        r.carry_buf = p->ax.p;
-        r.b = p->b.p;
-        r.fu = p->fu.p;
-        r.db = p->db.p;
-        r.lam = p->lam.p;
-        r.h = p->h.p;
-        r.mu = opt.mu;
-        r.div = pass::make_mudiv(opt.mu);
-        r.rcorr = opt.rcorr;
-        r.br = (opt.report || p->keep_br) ? p->br.p : nullptr;
-        r.ax = opt.report ? p->ax.p : nullptr;
-        CF_TRY(launch_pass(r, row_jds(p), row_panel_tiles(p, pn), done, p->stream));
-        ++nl;
-    }
+    CF_TRY(launch_row_only(p, opt, done, &nl));
     if (p->profiling) CF_CUDA(cudaEventRecord(e_c, p->stream));
     if (launches) *launches += nl;
     return CF_OK;
@@ -793,5 +800,129 @@ int launch_row_diag(cf_plan* p) {
 }
 
 int max_col_report_ctas() { return persistent_grid<ColReport>(1 << 30); }
+
+// ---------------------------------------------------------------- row-sharded building blocks
+namespace {
+__global__ void k_col_update(int64_t n, const double* ath, const double* cnt, const double* c, double* x, double* z,
+                             double* delta, double mu, int64_t n_blocks, const int32_t* cone_ptr, double* wbuf) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        const double cj = cnt[j];
+        const double fv = 1.0 / (1.0 + cj);
+        const double xj = x[j], zj = z[j], dj = delta[j];
+        const double dm = dj / mu;
+        const double v = __dadd_rn(__dmul_rn(cj, xj), ath[j]);
+        const double xp = fv * (((v + zj) + dm) - c[j] / mu);
+        const double w = xp - dm;
+        x[j] = xp;
+        if (!cone_ptr) {
+            const double zp = w > 0.0 ? w : 0.0;
+            z[j] = zp;
+            delta[j] = dj + mu * (zp - xp);
+        } else {
+            wbuf[j] = w;
+        }
+    }
+}
+__global__ void k_cone_update(int64_t n_blocks, const int32_t* cone_ptr, const double* wbuf, const double* x,
+                              double* z, double* delta, double mu) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n_blocks;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int off = cone_ptr[q], size = cone_ptr[q + 1] - off;
+        project_block_dev(wbuf + off, size, z + off);
+        for (int u = 0; u < size; ++u) delta[off + u] = delta[off + u] + mu * (z[off + u] - x[off + u]);
+    }
+}
+__global__ void k_col_parts(int64_t n, const double* atl, const double* c, const double* x, const double* z,
+                            const double* delta, double* part) {
+    __shared__ double sh[32];
+    double d2 = 0.0, dmx = 0.0, s2 = 0.0, smx = 0.0, amx = 0.0, cx = 0.0, cg = 0.0, nf = 0.0;
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+        const double dual = atl[j] + c[j];
+        const double stat = dual - delta[j];
+        d2 = d2 + dual * dual;
+        dmx = nanmax(dmx, fabs(dual));
+        s2 = s2 + stat * stat;
+        smx = nanmax(smx, fabs(stat));
+        amx = nanmax(amx, fabs(atl[j]));
+        cx = cx + c[j] * x[j];
+        cg = nanmax(cg, fabs(x[j] - z[j]));
+        if (!isfinite(x[j]) || !isfinite(z[j]) || !isfinite(delta[j]) || !isfinite(atl[j])) nf = 1.0;
+    }
+    const double vals[8] = {d2, dmx, s2, smx, amx, cx, cg, nf};
+    const bool is_sum[8] = {true, false, true, false, false, true, false, false};
+    for (int f = 0; f < 8; ++f) {
+        const double v = is_sum[f] ? block_reduce(vals[f], sh, SumOp()) : block_reduce(vals[f], sh, MaxOp());
+        if (threadIdx.x == 0) part[f] = v;
+    }
+}
+__global__ void k_row_parts_final(const double* part_row, int G, double* out) {
+    __shared__ double sh[32];
+    const SumOp sum;
+    const MaxOp mx;
+    const double f0 = reduce_partials(part_row + 0 * G, G, sh, sum);
+    const double f1 = reduce_partials(part_row + 1 * G, G, sh, mx);
+    const double f2 = reduce_partials(part_row + 2 * G, G, sh, mx);
+    const double f3 = reduce_partials(part_row + 3 * G, G, sh, sum);
+    const double f4 = reduce_partials(part_row + 4 * G, G, sh, mx);
+    if (threadIdx.x == 0) {
+        out[0] = f0;
+        out[1] = f1;
+        out[2] = f2;
+        out[3] = f3;
+        out[4] = f4;
+    }
+}
+__global__ void k_counts(const int32_t* colptr, int64_t n, double* cnt) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+        cnt[j] = (double)(colptr[j + 1] - colptr[j]);
+}
+}  // namespace
+
+int launch_col_update(int64_t n, const double* ath, const double* cnt, const double* c, double* x, double* z,
+                      double* delta, double mu, int64_t n_blocks, const int32_t* cone_ptr, cudaStream_t st) {
+    if (n == 0) return CF_OK;
+    DevBuf<double> w;
+    if (cone_ptr) CF_TRY(w.alloc(n));
+    k_col_update<<<grid_for(n, 256), 256, 0, st>>>(n, ath, cnt, c, x, z, delta, mu, n_blocks, cone_ptr, w.p);
+    CF_LAUNCHED();
+    if (cone_ptr) {
+        k_cone_update<<<grid_for(n_blocks, 128), 128, 0, st>>>(n_blocks, cone_ptr, w.p, x, z, delta, mu);
+        CF_LAUNCHED();
+        CF_CUDA(cudaStreamSynchronize(st));  // w is released at return
+    }
+    return CF_OK;
+}
+
+int launch_col_parts(int64_t n, const double* atl, const double* c, const double* x, const double* z,
+                     const double* delta, double* out8_dev, cudaStream_t st) {
+    k_col_parts<<<1, 1024, 0, st>>>(n, atl, c, x, z, delta, out8_dev);
+    CF_LAUNCHED();
+    return CF_OK;
+}
+
+int launch_row_parts(cf_plan* p, double* out5_dev) {
+    if (p->m == 0) {
+        CF_CUDA(cudaMemsetAsync(out5_dev, 0, 5 * sizeof(double), p->stream));
+        return CF_OK;
+    }
+    RowReportArgs a{};
+    a.ax = p->ax.p;
+    a.b = p->b.p;
+    a.lam = p->lam.p;
+    a.part = p->part_row.p;
+    a.m = (int32_t)p->m;
+    k_row_report<<<p->row_report_ctas, kThreads, 0, p->stream>>>(a);
+    CF_LAUNCHED();
+    k_row_parts_final<<<1, 1024, 0, p->stream>>>(p->part_row.p, p->row_report_ctas, out5_dev);
+    CF_LAUNCHED();
+    return CF_OK;
+}
+
+int launch_counts(cf_plan* p, double* cnt) {
+    if (p->n == 0) return CF_OK;
+    k_counts<<<grid_for(p->n, 256), 256, 0, p->stream>>>(p->colptr.p, p->n, cnt);
+    CF_LAUNCHED();
+    return CF_OK;
+}
 
 }  // namespace cf

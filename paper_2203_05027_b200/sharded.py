@@ -1,0 +1,283 @@
+"""Row-sharded solve over several GPUs.
+
+A's rows are split over the ranks of a torch.distributed process group
+(balanced by nonzeros); every rank also owns a contiguous slice of the
+columns (cone-aligned). One iteration of solver.py:313-317 in the reduced
+two-pass form becomes
+
+    partial = A_r^T h_r                      column pass over the local rows (all n columns)
+    ath_s   = reduce-scatter(partial, sum)   the exchange step (NCCL over NVLink)
+    x_s, z_s, delta_s <- column update        x_update / z_update / delta update on the slice,
+                                              with GLOBAL column counts (uv.py:82)
+    x       = all-gather(x_s)
+    lam_r, h_r <- row pass(x)                 y_update + dual updates of the local rows
+
+and every check_every iterations the report parts (row part local, A^T lam via
+a second reduce-scatter) are all-reduced and check_termination decides on every
+rank identically. Rows never move; the only collectives carry n-vectors.
+
+The compute of a rank is a *backend* (``CudaRankBackend``: libcfb200 kernels
+through the C ABI; the CPU tests use a numpy backend with the same interface
+on the gloo backend). Parity: the sums over rows of A^T h are split per rank,
+so iterates agree with ``solve`` to rounding (not bit for bit).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import replace
+
+import numpy as np
+
+from .api import IterationReport, SolveResult, SolverConfig, _decide, norms
+from .problem import ConeSpec, ProblemInstance, TripletMatrix, cone_sizes_array
+
+__all__ = ["solve_sharded", "partition", "CudaRankBackend", "assemble_report"]
+
+# report parts: row = {sum prim^2, max|prim|, max|Ax|, sum b.lam, nonfinite};
+# column = {sum dual^2, max|dual|, sum stat^2, max|stat|, max|A^T lam|, sum c.x, cone_gap, nonfinite}
+
+
+def partition(p, world: int):
+    """Row blocks balanced by nonzeros and cone-aligned column slices of equal-ish size.
+
+    Returns (row_cuts[world+1], col_cuts[world+1])."""
+    m, n = int(p.A.num_rows), int(p.A.num_cols)
+    counts = np.bincount(np.asarray(p.A.rows, dtype=np.int64), minlength=m)
+    cum = np.concatenate(([0], np.cumsum(counts)))
+    total = cum[-1]
+    row_cuts = [0]
+    for r in range(1, world):
+        row_cuts.append(int(np.searchsorted(cum, r * total / world, side="left")))
+    row_cuts.append(m)
+    row_cuts = list(np.maximum.accumulate(np.minimum(row_cuts, m)))
+    sizes = cone_sizes_array(p.cones)
+    starts = np.concatenate(([0], np.cumsum(sizes))) if sizes.size else np.array([0, n])
+    col_cuts = [0]
+    for r in range(1, world):
+        k = int(np.searchsorted(starts, r * n / world, side="left"))
+        col_cuts.append(int(starts[min(k, len(starts) - 1)]))
+    col_cuts.append(n)
+    col_cuts = list(np.maximum.accumulate(np.minimum(col_cuts, n)))
+    return [int(v) for v in row_cuts], [int(v) for v in col_cuts]
+
+
+def local_problem(p, r0: int, r1: int):
+    """The rank's rows [r0, r1) renumbered from 0, all columns (cones do not matter to the row block)."""
+    rows = np.asarray(p.A.rows, dtype=np.int64)
+    sel = (rows >= r0) & (rows < r1)
+    a = TripletMatrix(r1 - r0, p.A.num_cols, rows[sel] - r0, np.asarray(p.A.cols)[sel], np.asarray(p.A.vals)[sel])
+    return ProblemInstance(a, np.asarray(p.b)[r0:r1], np.asarray(p.c), ConeSpec.orthant(p.A.num_cols))
+
+
+def assemble_report(k: int, f: list) -> IterationReport:
+    """compute_report's final assembly (solver.py:219-242) from the reduced parts."""
+    prim2, prim_inf, ax_inf, blam, nf_row, dual2, dual_inf, stat2, stat_inf, atl_inf, pobj, cone_gap, nf_col = f
+    return IterationReport(
+        iter=k, prim_res_inf=prim_inf, prim_res_2=math.sqrt(prim2), dual_res_inf=dual_inf,
+        dual_res_2=math.sqrt(dual2), stat_res_inf=stat_inf, stat_res_2=math.sqrt(stat2), ax_inf=ax_inf,
+        atl_inf=atl_inf, cone_gap=cone_gap, pobj=pobj, dobj=-blam, gap=pobj + blam,
+        status="diverged" if (nf_row > 0 or nf_col > 0) else "running",
+    )
+
+
+class _DevArray:
+    """Zero-copy torch view of a device buffer owned by a cf_plan."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False), "version": 3,
+                                         "strides": None}
+
+
+class CudaRankBackend:
+    """One rank on its GPU: a plan over its row block (all columns) + its column slice state."""
+
+    def __init__(self, lp, col_lo: int, col_hi: int, cone_ptr_slice, global_counts_slice_fn):
+        import ctypes
+
+        import torch
+
+        from . import _lib
+        from .engine import DevicePlan
+
+        self.torch = torch
+        self.lib = _lib.lib()
+        self.stream = torch.cuda.current_stream()
+        self.plan = DevicePlan.from_problem(lp, stream=self.stream.cuda_stream)
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        self.n, self.m = lp.A.num_cols, lp.A.num_rows
+        self.lo, self.hi = col_lo, col_hi
+
+        def view(which):
+            ptr, ln = ctypes.c_void_p(), ctypes.c_int64()
+            _lib.check(self.lib.cf_plan_vector(self.plan.handle, which, ctypes.byref(ptr), ctypes.byref(ln)))
+            return torch.as_tensor(_DevArray(ptr.value or 0, ln.value), device=self.device) if ln.value else \
+                torch.zeros(0, dtype=torch.float64, device=self.device)
+
+        self.x_full, self.lam, self.h = view(0), view(3), view(4)
+        self.partial = torch.zeros(self.n, dtype=torch.float64, device=self.device)
+        ns = col_hi - col_lo
+        self.xs = torch.zeros(ns, dtype=torch.float64, device=self.device)
+        self.zs = torch.zeros_like(self.xs)
+        self.ds = torch.zeros_like(self.xs)
+        self.cs = torch.as_tensor(np.array(np.asarray(lp.c)[col_lo:col_hi]), dtype=torch.float64, device=self.device)
+        cnt = torch.zeros(self.n, dtype=torch.float64, device=self.device)
+        _lib.check(self.lib.cf_plan_column_counts(self.plan.handle, ctypes.c_void_p(cnt.data_ptr())))
+        self.local_counts = cnt
+        self.cnt_s = None   # set by the driver after the all-reduce of the counts
+        self.cone_ptr = None if cone_ptr_slice is None else torch.as_tensor(cone_ptr_slice, dtype=torch.int32,
+                                                                            device=self.device)
+        self.n_blocks = 0 if cone_ptr_slice is None else len(cone_ptr_slice) - 1
+
+    def _p(self, t):
+        import ctypes
+
+        return ctypes.c_void_p(t.data_ptr()) if t.numel() else ctypes.c_void_p(0)
+
+    def partial_At(self, which: str):
+        vec = self.h if which == "h" else self.lam
+        if self.m == 0:
+            self.partial.zero_()
+        else:
+            self.plan.apply_At(vec.data_ptr(), self.partial.data_ptr())
+        return self.partial
+
+    def column_update(self, ath_s, mu: float):
+        from . import _lib
+
+        _lib.check(self.lib.cf_column_update(self.xs.numel(), self._p(ath_s), self._p(self.cnt_s), self._p(self.cs),
+                                             self._p(self.xs), self._p(self.zs), self._p(self.ds), float(mu),
+                                             self.n_blocks, self._p(self.cone_ptr) if self.cone_ptr is not None
+                                             else None, self.stream.cuda_stream))
+
+    def x_slice(self):
+        return self.xs
+
+    def set_x(self, x_full):
+        self.x_full.copy_(x_full)
+
+    def row_step(self, mu: float, report: bool):
+        from . import _lib
+
+        _lib.check(self.lib.cf_plan_row_step(self.plan.handle, float(mu), 1 if report else 0))
+
+    def row_parts(self):
+        from . import _lib
+
+        out = np.zeros(5)
+        _lib.check(self.lib.cf_plan_row_parts(self.plan.handle, self._np(out)))
+        return out
+
+    def col_parts(self, atl_s):
+        from . import _lib
+
+        out = np.zeros(8)
+        _lib.check(self.lib.cf_column_parts(self.xs.numel(), self._p(atl_s), self._p(self.cs), self._p(self.xs),
+                                            self._p(self.zs), self._p(self.ds), self._np(out),
+                                            self.stream.cuda_stream))
+        return out
+
+    @staticmethod
+    def _np(a):
+        import ctypes
+
+        return ctypes.c_void_p(a.ctypes.data)
+
+    def lam_local(self):
+        return self.lam
+
+    def close(self):
+        self.plan.close()
+
+
+def _cone_ptr_slice(p, lo: int, hi: int):
+    sizes = cone_sizes_array(p.cones)
+    if sizes.size == 0 or int(sizes.max()) == 1:
+        return None
+    starts = np.concatenate(([0], np.cumsum(sizes)))
+    q0, q1 = np.searchsorted(starts, lo), np.searchsorted(starts, hi)
+    return (starts[q0:q1 + 1] - lo).astype(np.int32)
+
+
+def solve_sharded(p, cfg: SolverConfig | None = None, group=None, backend_factory=None) -> SolveResult:
+    """solve() with A's rows split over the ranks of ``group`` (every rank passes the same problem).
+
+    Cold start only. Returns the same SolveResult on every rank."""
+    import torch
+    import torch.distributed as dist
+
+    cfg = cfg or SolverConfig()
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    row_cuts, col_cuts = partition(p, world)
+    r0, r1 = row_cuts[rank], row_cuts[rank + 1]
+    lo, hi = col_cuts[rank], col_cuts[rank + 1]
+    lp = local_problem(p, r0, r1)
+    factory = backend_factory or CudaRankBackend
+    be = factory(lp, lo, hi, _cone_ptr_slice(p, lo, hi), None)
+    torch_dev = be.device
+    n, m = int(p.A.num_cols), int(p.A.num_rows)
+    S = max(col_cuts[r + 1] - col_cuts[r] for r in range(world))
+    Mx = max(row_cuts[r + 1] - row_cuts[r] for r in range(world))
+    # padded layout of an n-vector: slice r at [r*S, r*S + len_r)
+    pad_idx = torch.cat([torch.arange(col_cuts[r], col_cuts[r + 1], dtype=torch.int64) - col_cuts[r] + r * S
+                         for r in range(world)]).to(torch_dev)
+    nccl = dist.get_backend(group) == "nccl"
+
+    def reduce_scatter(vec):
+        padded = torch.zeros(world * S, dtype=torch.float64, device=torch_dev)
+        padded[pad_idx] = vec
+        if nccl:
+            out = torch.empty(S, dtype=torch.float64, device=torch_dev)
+            dist.reduce_scatter_tensor(out, padded, op=dist.ReduceOp.SUM, group=group)
+        else:
+            dist.all_reduce(padded, op=dist.ReduceOp.SUM, group=group)
+            out = padded[rank * S:(rank + 1) * S].clone()
+        return out[:hi - lo]
+
+    def all_gather(slice_vec, width, cuts):
+        padded = torch.zeros(width, dtype=torch.float64, device=torch_dev)
+        padded[:slice_vec.numel()] = slice_vec
+        parts = [torch.empty(width, dtype=torch.float64, device=torch_dev) for _ in range(world)]
+        dist.all_gather(parts, padded, group=group)
+        return torch.cat([parts[r][:cuts[r + 1] - cuts[r]] for r in range(world)])
+
+    # global column counts (uv.py:82 uses counts over ALL rows)
+    be.cnt_s = reduce_scatter(be.local_counts).contiguous()
+    b_norms, c_norms = norms(p.b), norms(p.c)
+    trace = []
+    x_full = None
+    for k in range(1, cfg.max_iters + 1):
+        ath = reduce_scatter(be.partial_At("h")).contiguous()
+        be.column_update(ath, cfg.mu)
+        x_full = all_gather(be.x_slice(), S, col_cuts)
+        be.set_x(x_full)
+        report = (k % cfg.check_every == 0) or (k == cfg.max_iters)
+        be.row_step(cfg.mu, report)
+        if not report:
+            continue
+        rp = torch.as_tensor(be.row_parts(), dtype=torch.float64, device=torch_dev)
+        atl = reduce_scatter(be.partial_At("lam")).contiguous()
+        cp = torch.as_tensor(be.col_parts(atl), dtype=torch.float64, device=torch_dev)
+        sums = torch.stack([rp[0], rp[3], cp[0], cp[2], cp[5]])
+        maxs = torch.stack([rp[1], rp[2], rp[4], cp[1], cp[3], cp[4], cp[6], cp[7]])
+        nan = torch.isnan(maxs).to(torch.float64)
+        dist.all_reduce(sums, op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(maxs, op=dist.ReduceOp.MAX, group=group)
+        dist.all_reduce(nan, op=dist.ReduceOp.MAX, group=group)
+        maxs = torch.where(nan > 0, torch.full_like(maxs, float("nan")), maxs)
+        s, mx = sums.tolist(), maxs.tolist()
+        f = [s[0], mx[0], mx[1], s[1], mx[2], s[2], mx[3], s[3], mx[4], mx[5], s[4], mx[6], mx[7]]
+        rep = assemble_report(k, f)
+        status = _decide(rep, cfg, b_norms, c_norms)
+        if status == "running" and k == cfg.max_iters:
+            status = "max_iters"
+        trace.append(replace(rep, status=status))
+        if status != "running":
+            break
+    lam = all_gather(be.lam_local(), Mx, row_cuts)
+    x = x_full.detach().cpu().numpy().copy()
+    lam = lam.detach().cpu().numpy().copy()
+    if hasattr(be, "close"):
+        be.close()
+    return SolveResult(x=x, lam=lam, report=trace[-1], trace=tuple(trace))
