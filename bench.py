@@ -54,6 +54,8 @@ CONFIGS = {
                workload="C3: synthetic SOCP m=2,000,000 n=4,000,000 o=40,000,000, 1,000,000 K4 cones fp64"),
     "c1": dict(m=1000, n=2000, density=0.01, cone_kind="lp",
                workload="C1: synthetic sparse LP m=1,000 n=2,000 o=20,000 fp64"),
+    "c5": dict(m=50_000_000, n=100_000_000, density=2e-7, cone_kind="lp", sharded=True,
+               workload="C5: row-sharded synthetic sparse LP m=50,000,000 n=100,000,000 o=1,000,000,000 fp64"),
     "c4": dict(m=100, n=200, density=0.05, cone_kind="lp", batch=4096,
                workload="C4: batch of 4096 independent sparse LPs m=100 n=200 o=1,000 (5%) fp64, seeds 0..4095"),
 }
@@ -347,6 +349,72 @@ def run_ours(args, spec, rank, world, local_rank):
     return 0
 
 
+def run_sharded_bench(args, spec, rank, world, local_rank):
+    """C5: rows of one instance split over the ranks (strong scaling), NCCL reduce-scatter + all-gather."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2203_05027_b200 import SolverConfig
+    from paper_2203_05027_b200.devgen import generate_device_shard
+    from paper_2203_05027_b200.sharded import CudaRankBackend, run_sharded
+
+    torch.cuda.set_device(local_rank)
+    own_group = False
+    if world == 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        dist.init_process_group("nccl", rank=0, world_size=1)
+        own_group = True
+    scale = args.c5_scale
+    m, n = int(spec["m"] * scale), int(spec["n"] * scale)
+    stream = torch.cuda.current_stream()
+    plan, row_cuts, col_cuts, c_slice, bn, cn, cones = generate_device_shard(
+        m, n, spec["density"] / scale, spec["cone_kind"], args.seed, rank, world, stream=stream.cuda_stream)
+    be = CudaRankBackend.from_plan(plan, col_cuts[rank], col_cuts[rank + 1], c_slice, cones)
+    o_local = plan.o
+    o_t = torch.tensor([float(o_local)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(o_t)
+    warm = SolverConfig(max_iters=max(args.warmup, 1), check_every=25, eps_prim=0.0, eps_dual=0.0, eps_gap=0.0)
+    run_sharded(be, row_cuts, col_cuts, warm, bn, cn, gather_result=False)
+    # fresh state for the timed run
+    be.close()
+    del be
+    plan, row_cuts, col_cuts, c_slice, bn, cn, cones = generate_device_shard(
+        m, n, spec["density"] / scale, spec["cone_kind"], args.seed, rank, world, stream=stream.cuda_stream)
+    be = CudaRankBackend.from_plan(plan, col_cuts[rank], col_cuts[rank + 1], c_slice, cones)
+    cfg = SolverConfig(max_iters=args.steps, check_every=25, eps_prim=0.0, eps_dual=0.0, eps_gap=0.0)
+    dist.barrier()
+    torch.cuda.synchronize()
+    tim = {}
+    run_sharded(be, row_cuts, col_cuts, cfg, bn, cn, timing=tim, gather_result=False)
+    torch.cuda.synchronize()
+    ms = torch.tensor([tim["loop_ms"]], dtype=torch.float64, device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms)
+    value = args.steps / (ms / 1000.0)
+    o_total = int(o_t.item())
+    row_b, col_b = algorithmic_bytes(m, n, o_total)
+    peak, src = hbm_peak()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (per-rank GPU generator, reference recipe)",
+            "config": {"workload": spec["workload"] if scale == 1.0 else f"C5 structure scaled by {scale}: m={m} n={n}",
+                       "m": m, "n": n, "o": o_total, "parallelism": f"row-sharded x{world} (NCCL reduce-scatter + all-gather)"},
+            # per iteration: partial A^T h, column update, row pass (per panel); + report kernels every 25
+            "gpu_launches": args.steps * 4 + (args.steps // 25) * 5,
+            "iteration_roofline": {"bytes_per_iteration_total": row_b + col_b,
+                                   "achieved_per_gpu_GBs": (row_b + col_b) / world / (ms / args.steps / 1000) / 1e9,
+                                   "peak": peak, "peak_source": src},
+        }
+        print(json.dumps(line), flush=True)
+    be.close()
+    if own_group:
+        dist.destroy_process_group()
+    return 0
+
+
 def run_batch(args, spec, rank, world):
     """C4: solve_batch over 4096 generated problems; value = problem-iterations/s of the batch kernel."""
     import numpy as np
@@ -416,6 +484,7 @@ def main():
     ap.add_argument("--skip-ttt", action="store_true")
     ap.add_argument("--e2e-max-iters", type=int, default=0)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--c5-scale", type=float, default=1.0, help="shrink C5 (m, n) by this factor (same nnz/row)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
@@ -434,6 +503,8 @@ def main():
     try:
         if "batch" in spec:
             return run_batch(args, spec, rank, world)
+        if spec.get("sharded"):
+            return run_sharded_bench(args, spec, rank, world, local_rank)
         return run_ours(args, spec, rank, world, local_rank)
     finally:
         if world > 1:

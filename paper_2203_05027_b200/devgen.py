@@ -20,7 +20,7 @@ import numpy as np
 
 from .engine import DevicePlan
 
-__all__ = ["DeviceInstance", "generate_device", "c2_spec", "c3_spec", "to_host_problem"]
+__all__ = ["DeviceInstance", "generate_device", "generate_device_shard", "c2_spec", "c3_spec", "to_host_problem"]
 
 
 @dataclass
@@ -124,3 +124,88 @@ def to_host_problem(inst: DeviceInstance):
 
     a = TripletMatrix(inst.m, inst.n, inst.rows.cpu().numpy(), inst.cols.cpu().numpy(), inst.vals.cpu().numpy())
     return ProblemInstance(a, inst.b.cpu().numpy(), inst.c.cpu().numpy(), ConeSpec(inst.block_sizes))
+
+
+def generate_device_shard(m: int, n: int, density: float, cone_kind: str, seed: int, rank: int, world: int,
+                          group=None, stream: int | None = None):
+    """Rank ``rank``'s row block of a row-sharded instance (C5), built on its GPU only.
+
+    Rows [m*rank/world, m*(rank+1)/world) get their share of the nonzeros
+    (uniform positions, N(0,1) values); the primal witness x and the dual slack
+    draw are shared (same seed on every rank) so b_local = A_local Proj_K(x) and
+    c = Proj_K(s) - sum_r A_r^T lam_r (an all-reduce) reproduce the generator
+    recipe of generate.py:103-140 for the whole matrix. Returns
+    (plan, row_cuts, col_cuts, c_slice tensor, b_norms, c_norms)."""
+    import math
+
+    import torch
+    import torch.distributed as dist
+
+    dev = torch.device("cuda")
+    r0, r1 = m * rank // world, m * (rank + 1) // world
+    ml = r1 - r0
+    o = int(round(ml * n * density))
+    g_local = torch.Generator(device=dev)
+    g_local.manual_seed(int(seed) * 1000003 + rank)
+    g_shared = torch.Generator(device=dev)
+    g_shared.manual_seed(int(seed))
+    pos = _distinct_positions(torch, g_local, ml * n, o, dev)
+    rows, cols = pos // n, pos % n
+    del pos
+    vals = torch.randn(o, generator=g_local, device=dev, dtype=torch.float64)
+    vals[vals == 0.0] = 1.0
+    if cone_kind == "lp":
+        sizes = np.ones(n, dtype=np.int64)
+        unit = 1
+    else:
+        sizes = np.full(n // 4, 4, dtype=np.int64)
+        unit = 4
+    b = torch.zeros(ml, dtype=torch.float64, device=dev)
+    c = torch.zeros(n, dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
+    # the local plan's own column pass is never used (the driver updates column slices), so the
+    # orthant is enough here; the cones enter through the slice update
+    plan = DevicePlan.from_device(ml, n, o, rows.data_ptr(), cols.data_ptr(), vals.data_ptr(), b.data_ptr(),
+                                  c.data_ptr(), np.ones(n, dtype=np.int64), stream=stream)
+    del rows, cols, vals
+    xdot = torch.randn(n, generator=g_shared, device=dev, dtype=torch.float64)
+    xf = _project(torch, xdot, unit)
+    plan.apply_A(xf.data_ptr(), b.data_ptr())
+    lam = torch.randn(ml, generator=g_local, device=dev, dtype=torch.float64)
+    atl = torch.empty(n, dtype=torch.float64, device=dev)
+    plan.apply_At(lam.data_ptr(), atl.data_ptr())
+    dist.all_reduce(atl, op=dist.ReduceOp.SUM, group=group)
+    s = _project(torch, torch.randn(n, generator=g_shared, device=dev, dtype=torch.float64), unit)
+    c.copy_(s - atl)
+    torch.cuda.synchronize()
+    plan.set_rhs(b.data_ptr(), c.data_ptr(), on_device=True)
+    row_cuts = [m * r // world for r in range(world + 1)]
+    step = -(-n // world)
+    step = -(-step // unit) * unit
+    col_cuts = [min(n, r * step) for r in range(world)] + [n]
+    lo, hi = col_cuts[rank], col_cuts[rank + 1]
+    # global norms of b (distributed) and c (replicated): ||.||_inf and ||.||_2 as solver.py:200-203
+    bb = torch.stack([b.abs().max() if ml else torch.zeros((), device=dev, dtype=torch.float64), (b * b).sum()])
+    dist.all_reduce(bb[:1], op=dist.ReduceOp.MAX, group=group)
+    sq = bb[1:].clone()
+    dist.all_reduce(sq, op=dist.ReduceOp.SUM, group=group)
+    b_norms = (float(bb[0]), math.sqrt(float(sq)))
+    c_norms = (float(c.abs().max()), math.sqrt(float((c * c).sum())))
+    cone_slice = None if unit == 1 else (np.arange(lo, hi + 1, 4) - lo).astype(np.int32)
+    return plan, row_cuts, col_cuts, c[lo:hi].clone(), b_norms, c_norms, cone_slice
+
+
+def _project(torch, w, unit):
+    if unit == 1:
+        return torch.clamp(w, min=0.0) + 0.0
+    v = w.view(-1, unit)
+    head, tail = v[:, 0], v[:, 1:]
+    alpha = torch.sqrt((tail * tail).sum(1))
+    out = torch.zeros_like(v)
+    keep = alpha <= head
+    scale = ~(alpha <= -head) & ~keep
+    out[keep] = v[keep]
+    f = head[scale] / (2.0 * alpha[scale])
+    out[scale, 1:] = 0.5 * tail[scale] + f[:, None] * tail[scale]
+    out[scale, 0] = 0.5 * head[scale] + 0.5 * alpha[scale]
+    return out.view(-1)

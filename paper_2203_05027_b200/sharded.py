@@ -32,7 +32,7 @@ import numpy as np
 from .api import IterationReport, SolveResult, SolverConfig, _decide, norms
 from .problem import ConeSpec, ProblemInstance, TripletMatrix, cone_sizes_array
 
-__all__ = ["solve_sharded", "partition", "CudaRankBackend", "assemble_report"]
+__all__ = ["solve_sharded", "run_sharded", "partition", "CudaRankBackend", "assemble_report"]
 
 # report parts: row = {sum prim^2, max|prim|, max|Ax|, sum b.lam, nonfinite};
 # column = {sum dual^2, max|dual|, sum stat^2, max|stat|, max|A^T lam|, sum c.x, cone_gap, nonfinite}
@@ -92,7 +92,8 @@ class _DevArray:
 class CudaRankBackend:
     """One rank on its GPU: a plan over its row block (all columns) + its column slice state."""
 
-    def __init__(self, lp, col_lo: int, col_hi: int, cone_ptr_slice, global_counts_slice_fn):
+    def __init__(self, lp, col_lo: int, col_hi: int, cone_ptr_slice, global_counts_slice_fn, plan=None,
+                 c_slice=None):
         import ctypes
 
         import torch
@@ -103,9 +104,9 @@ class CudaRankBackend:
         self.torch = torch
         self.lib = _lib.lib()
         self.stream = torch.cuda.current_stream()
-        self.plan = DevicePlan.from_problem(lp, stream=self.stream.cuda_stream)
+        self.plan = plan if plan is not None else DevicePlan.from_problem(lp, stream=self.stream.cuda_stream)
         self.device = torch.device("cuda", torch.cuda.current_device())
-        self.n, self.m = lp.A.num_cols, lp.A.num_rows
+        self.n, self.m = self.plan.n, self.plan.m
         self.lo, self.hi = col_lo, col_hi
 
         def view(which):
@@ -120,7 +121,11 @@ class CudaRankBackend:
         self.xs = torch.zeros(ns, dtype=torch.float64, device=self.device)
         self.zs = torch.zeros_like(self.xs)
         self.ds = torch.zeros_like(self.xs)
-        self.cs = torch.as_tensor(np.array(np.asarray(lp.c)[col_lo:col_hi]), dtype=torch.float64, device=self.device)
+        if c_slice is not None:
+            self.cs = c_slice
+        else:
+            self.cs = torch.as_tensor(np.array(np.asarray(lp.c)[col_lo:col_hi]), dtype=torch.float64,
+                                      device=self.device)
         cnt = torch.zeros(self.n, dtype=torch.float64, device=self.device)
         _lib.check(self.lib.cf_plan_column_counts(self.plan.handle, ctypes.c_void_p(cnt.data_ptr())))
         self.local_counts = cnt
@@ -141,6 +146,11 @@ class CudaRankBackend:
         else:
             self.plan.apply_At(vec.data_ptr(), self.partial.data_ptr())
         return self.partial
+
+    @classmethod
+    def from_plan(cls, plan, col_lo: int, col_hi: int, c_slice, cone_ptr_slice=None):
+        """A rank backend over a plan already built on the device (devgen.generate_device_shard)."""
+        return cls(None, col_lo, col_hi, cone_ptr_slice, None, plan=plan, c_slice=c_slice)
 
     def column_update(self, ath_s, mu: float):
         from . import _lib
@@ -203,7 +213,6 @@ def solve_sharded(p, cfg: SolverConfig | None = None, group=None, backend_factor
     """solve() with A's rows split over the ranks of ``group`` (every rank passes the same problem).
 
     Cold start only. Returns the same SolveResult on every rank."""
-    import torch
     import torch.distributed as dist
 
     cfg = cfg or SolverConfig()
@@ -215,49 +224,81 @@ def solve_sharded(p, cfg: SolverConfig | None = None, group=None, backend_factor
     lp = local_problem(p, r0, r1)
     factory = backend_factory or CudaRankBackend
     be = factory(lp, lo, hi, _cone_ptr_slice(p, lo, hi), None)
+    try:
+        return run_sharded(be, row_cuts, col_cuts, cfg, norms(p.b), norms(p.c), group)
+    finally:
+        if hasattr(be, "close"):
+            be.close()
+
+
+def run_sharded(be, row_cuts, col_cuts, cfg, b_norms, c_norms, group=None, timing=None,
+                gather_result: bool = True) -> SolveResult:
+    """The sharded loop on an existing rank backend (row/column cuts shared by all ranks).
+
+    ``timing``: if a dict, receives the CUDA-event time of the loop on this rank (ms)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    lo, hi = col_cuts[rank], col_cuts[rank + 1]
     torch_dev = be.device
-    n, m = int(p.A.num_cols), int(p.A.num_rows)
+    n = col_cuts[-1]
     S = max(col_cuts[r + 1] - col_cuts[r] for r in range(world))
     Mx = max(row_cuts[r + 1] - row_cuts[r] for r in range(world))
-    # padded layout of an n-vector: slice r at [r*S, r*S + len_r)
-    pad_idx = torch.cat([torch.arange(col_cuts[r], col_cuts[r + 1], dtype=torch.int64) - col_cuts[r] + r * S
-                         for r in range(world)]).to(torch_dev)
+    contiguous = all(col_cuts[r] == r * S for r in range(world))
     nccl = dist.get_backend(group) == "nccl"
+    padded = torch.zeros(world * S, dtype=torch.float64, device=torch_dev)
+    rs_out = torch.empty(S, dtype=torch.float64, device=torch_dev)
+    ag_out = torch.empty(world * S, dtype=torch.float64, device=torch_dev)
+    xs_pad = torch.zeros(S, dtype=torch.float64, device=torch_dev)
+    pad_idx = None
+    if not contiguous:
+        # slice r at [r*S, r*S + len_r) of the padded layout
+        pad_idx = torch.cat([torch.arange(col_cuts[r], col_cuts[r + 1], dtype=torch.int64) - col_cuts[r] + r * S
+                             for r in range(world)]).to(torch_dev)
 
     def reduce_scatter(vec):
-        padded = torch.zeros(world * S, dtype=torch.float64, device=torch_dev)
-        padded[pad_idx] = vec
+        if contiguous:
+            padded[:n].copy_(vec)
+        else:
+            padded[pad_idx] = vec
         if nccl:
-            out = torch.empty(S, dtype=torch.float64, device=torch_dev)
-            dist.reduce_scatter_tensor(out, padded, op=dist.ReduceOp.SUM, group=group)
+            dist.reduce_scatter_tensor(rs_out, padded, op=dist.ReduceOp.SUM, group=group)
+            out = rs_out
         else:
             dist.all_reduce(padded, op=dist.ReduceOp.SUM, group=group)
-            out = padded[rank * S:(rank + 1) * S].clone()
-        return out[:hi - lo]
+            out = padded[rank * S:(rank + 1) * S]
+        return out[:hi - lo].contiguous()
 
-    def all_gather(slice_vec, width, cuts):
-        padded = torch.zeros(width, dtype=torch.float64, device=torch_dev)
-        padded[:slice_vec.numel()] = slice_vec
-        parts = [torch.empty(width, dtype=torch.float64, device=torch_dev) for _ in range(world)]
-        dist.all_gather(parts, padded, group=group)
-        return torch.cat([parts[r][:cuts[r + 1] - cuts[r]] for r in range(world)])
+    def gather_x(slice_vec):
+        xs_pad[:slice_vec.numel()] = slice_vec
+        if nccl:
+            dist.all_gather_into_tensor(ag_out, xs_pad, group=group)
+        else:
+            parts = list(ag_out.chunk(world))
+            dist.all_gather(parts, xs_pad, group=group)
+            ag_out.copy_(torch.cat(parts))
+        return ag_out[:n] if contiguous else ag_out[pad_idx]
 
     # global column counts (uv.py:82 uses counts over ALL rows)
-    be.cnt_s = reduce_scatter(be.local_counts).contiguous()
-    b_norms, c_norms = norms(p.b), norms(p.c)
+    be.cnt_s = reduce_scatter(be.local_counts).clone()
     trace = []
     x_full = None
+    if timing is not None and torch_dev.type == "cuda":
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
     for k in range(1, cfg.max_iters + 1):
-        ath = reduce_scatter(be.partial_At("h")).contiguous()
+        ath = reduce_scatter(be.partial_At("h"))
         be.column_update(ath, cfg.mu)
-        x_full = all_gather(be.x_slice(), S, col_cuts)
+        x_full = gather_x(be.x_slice())
         be.set_x(x_full)
         report = (k % cfg.check_every == 0) or (k == cfg.max_iters)
         be.row_step(cfg.mu, report)
         if not report:
             continue
         rp = torch.as_tensor(be.row_parts(), dtype=torch.float64, device=torch_dev)
-        atl = reduce_scatter(be.partial_At("lam")).contiguous()
+        atl = reduce_scatter(be.partial_At("lam"))
         cp = torch.as_tensor(be.col_parts(atl), dtype=torch.float64, device=torch_dev)
         sums = torch.stack([rp[0], rp[3], cp[0], cp[2], cp[5]])
         maxs = torch.stack([rp[1], rp[2], rp[4], cp[1], cp[3], cp[4], cp[6], cp[7]])
@@ -275,9 +316,18 @@ def solve_sharded(p, cfg: SolverConfig | None = None, group=None, backend_factor
         trace.append(replace(rep, status=status))
         if status != "running":
             break
-    lam = all_gather(be.lam_local(), Mx, row_cuts)
-    x = x_full.detach().cpu().numpy().copy()
-    lam = lam.detach().cpu().numpy().copy()
-    if hasattr(be, "close"):
-        be.close()
-    return SolveResult(x=x, lam=lam, report=trace[-1], trace=tuple(trace))
+    if timing is not None and torch_dev.type == "cuda":
+        e1.record()
+        e1.synchronize()
+        timing["loop_ms"] = e0.elapsed_time(e1)
+        timing["iters"] = trace[-1].iter
+    if not gather_result:
+        return SolveResult(x=None, lam=None, report=trace[-1], trace=tuple(trace))
+    lam_pad = torch.zeros(Mx, dtype=torch.float64, device=torch_dev)
+    lam_local = be.lam_local()
+    lam_pad[:lam_local.numel()] = lam_local
+    parts = [torch.empty(Mx, dtype=torch.float64, device=torch_dev) for _ in range(world)]
+    dist.all_gather(parts, lam_pad, group=group)
+    lam = torch.cat([parts[r][:row_cuts[r + 1] - row_cuts[r]] for r in range(world)])
+    return SolveResult(x=x_full.detach().cpu().numpy().copy(), lam=lam.detach().cpu().numpy().copy(),
+                       report=trace[-1], trace=tuple(trace))
