@@ -100,7 +100,7 @@ struct cf_plan {
     cf::DevBuf<int32_t> csr2csc;  // canonical position of each CSR entry
 
     // problem vectors and cached diagonals (fu_diag uv.py:81; d*b for the row pass)
-    cf::DevBuf<double> b, c, fu, db;
+    cf::DevBuf<double> b, c, fu, db, amax;
 
     // cones (cones.py:39-59) and column tiling
     bool all_unit = true;

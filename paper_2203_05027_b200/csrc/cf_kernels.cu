@@ -267,16 +267,12 @@ struct ColIter : ColVecs {
 
 // Column part of compute_report (solver.py:208-225): atl = A^T lam (bincount order),
 // dual = atl + c, stat = dual - delta, pobj = c.x, cone_gap = max|x - z| and the
-// finiteness of x, z, delta and of the implicit y_k = x_j + a_k (b_i - r_i),
-// gamma_k = -a_k lam_i. Per-thread partials are reduced once per CTA (finish).
+// finiteness of x, z, delta (the implicit y and gamma are checked per row by
+// k_row_report). Per-thread partials are reduced once per CTA (finish).
 struct ColReport : ColVecs {
-    static constexpr int kUnroll = 4;   // 8 report accumulators per thread: keep register pressure low
-    const double* br;      // may be null
+    static constexpr int kUnroll = 12;   // 8 report accumulators per thread: a little less in flight
     double* part;          // [kReportFieldsCol][kGroups][gridDim.x]
     double d2, dmx, s2, smx, amx, cx, cg, nf;
-    __device__ __forceinline__ void check(double a, int i, double lam_i) {
-        if (!isfinite(a * lam_i) || (br && !isfinite(a * br[i]))) nf = 1.0;
-    }
     __device__ __forceinline__ void segment(Smem&, int, int, int, int, double atl, const Vals& vv) {
         const double xj = vv.v[0], zj = vv.v[1], dj = vv.v[2], cj = vv.v[3];
         const double dual = atl + cj;
@@ -353,6 +349,8 @@ struct RowReportArgs {
     const double* ax;
     const double* b;
     const double* lam;
+    const double* br;     // b - r of the report iteration (y_k = x_j + a_k br_i), may be null
+    const double* amax;   // max |a_k| of each row
     double* part;    // [kReportFieldsRow][gridDim.x]
     int32_t m;
     const int32_t* done;
@@ -364,6 +362,10 @@ __global__ void __launch_bounds__(kThreads) k_row_report(const RowReportArgs a) 
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.m; i += gridDim.x * blockDim.x) {
         const double axi = a.ax[i], bi = a.b[i], li = a.lam[i];
         const double pr = axi - bi;
+        // implicit gamma_k = -a_k lam_i and the a_k (b_i - r_i) part of y_k: all finite iff
+        // their largest magnitude is
+        const double am = a.amax[i];
+        if (!finite(am * li) || (a.br && !finite(am * a.br[i]))) nf = 1.0;
         s2 = s2 + pr * pr;
         mx = nanmax(mx, fabs(pr));
         axm = nanmax(axm, fabs(axi));
@@ -503,16 +505,22 @@ __global__ void k_warm_rows(const int32_t* rowptr, const double* valr, const int
 }
 
 // fu_i = 1/(1 + sum a^2) (uv.py:81, bincount order = CSR order), db_i = d_i b_i
+// also amax_i = max_k |a_k| of row i: a_k*v is finite for every k of row i iff amax_i*v is
+// (the report's exact row-level test of the implicit y and gamma, solver.py:208-211)
 __global__ void k_row_diag(const int32_t* rowptr, const double* valr, const double* b, double* fu, double* db,
-                           int64_t m, int32_t panels) {
+                           double* amax, int64_t m, int32_t panels) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
-        double d = 0.0;
+        double d = 0.0, am = 0.0;
         for (int32_t pn = 0; pn < panels; ++pn) {
             const int64_t seg = pn * m + i;
-            for (int p = rowptr[seg]; p < rowptr[seg + 1]; ++p) d = d + valr[p] * valr[p];
+            for (int p = rowptr[seg]; p < rowptr[seg + 1]; ++p) {
+                d = d + valr[p] * valr[p];
+                am = fmax(am, fabs(valr[p]));
+            }
         }
         fu[i] = 1.0 / (1.0 + d);
         db[i] = d * b[i];
+        amax[i] = am;
     }
 }
 
@@ -706,6 +714,8 @@ int launch_report(cf_plan* p, double mu, bool ax_ready, const cf_config* cfg, in
         a.ax = p->ax.p;
         a.b = p->b.p;
         a.lam = p->lam.p;
+        a.br = p->br_valid ? p->br.p : nullptr;
+        a.amax = p->amax.p;
         a.part = p->part_row.p;
         a.m = (int32_t)p->m;
         a.done = done;
@@ -722,7 +732,6 @@ int launch_report(cf_plan* p, double mu, bool ax_ready, const cf_config* cfg, in
         c.z_in = p->z.p;
         c.d_in = p->delta.p;
         c.c = p->c.p;
-        c.br = p->br_valid ? p->br.p : nullptr;
         c.part = p->part_col.p;
         CF_TRY(launch_pass(c, col_jds(p), col_tiles(p), done, p->stream, &g_col));
         g_col *= pass::kGroups;  // one partial per (field, group, CTA)
@@ -793,8 +802,8 @@ int launch_warm_start(cf_plan* p, double mu) {
 
 int launch_row_diag(cf_plan* p) {
     if (p->m == 0) return CF_OK;
-    k_row_diag<<<grid_for(p->m, 128), 128, 0, p->stream>>>(p->rowptr.p, p->valr.p, p->b.p, p->fu.p, p->db.p, p->m,
-                                                          p->n_panels);
+    k_row_diag<<<grid_for(p->m, 128), 128, 0, p->stream>>>(p->rowptr.p, p->valr.p, p->b.p, p->fu.p, p->db.p,
+                                                          p->amax.p, p->m, p->n_panels);
     CF_LAUNCHED();
     return CF_OK;
 }
@@ -909,6 +918,8 @@ int launch_row_parts(cf_plan* p, double* out5_dev) {
     a.ax = p->ax.p;
     a.b = p->b.p;
     a.lam = p->lam.p;
+    a.br = p->br_valid ? p->br.p : nullptr;
+    a.amax = p->amax.p;
     a.part = p->part_row.p;
     a.m = (int32_t)p->m;
     k_row_report<<<p->row_report_ctas, kThreads, 0, p->stream>>>(a);
