@@ -15,10 +15,13 @@ namespace cf {
 // ---------------------------------------------------------------- geometry
 constexpr int kThreads = 256;     // threads of the simple (non-pass) kernels
 #ifndef CF_PCAP
-#define CF_PCAP 2048
+#define CF_PCAP 3072
+#endif
+#ifndef CF_PSEG
+#define CF_PSEG 256
 #endif
 constexpr int kTileNnz = CF_PCAP;  // nonzeros per tile (= pass::kPCap)
-constexpr int kTileSeg = 256;     // rows / columns per tile (= pass::kPSeg)
+constexpr int kTileSeg = CF_PSEG;  // rows / columns per tile (= pass::kPSeg)
 constexpr int kTileDiag = 256;    // longest segment inside a multi-segment tile (= pass::kMaxDiag)
 constexpr int kSmallCone = 256;   // cones up to this size are projected inside the column tile
 constexpr int kReportFieldsRow = 5;

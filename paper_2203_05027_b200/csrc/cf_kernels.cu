@@ -74,6 +74,7 @@ __device__ __forceinline__ void project_block_dev(const double* w, int q, double
     }
 }
 
+static_assert(kTileSeg == pass::kPSeg && kTileNnz == pass::kPCap, "host tile cutter and pass engine disagree");
 using pass::kComputeThreads;
 using pass::kPSeg;
 using pass::Smem;
