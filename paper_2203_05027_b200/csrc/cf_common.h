@@ -23,7 +23,7 @@ constexpr int kThreads = 256;     // threads of the simple (non-pass) kernels
 constexpr int kTileNnz = CF_PCAP;  // nonzeros per tile (= pass::kPCap)
 constexpr int kTileSeg = CF_PSEG;  // rows / columns per tile (= pass::kPSeg)
 constexpr int kTileDiag = 256;    // longest segment inside a multi-segment tile (= pass::kMaxDiag)
-constexpr int kSmallCone = 256;   // cones up to this size are projected inside the column tile
+constexpr int kSmallCone = kTileSeg;  // cones up to this size are projected inside the column tile
 constexpr int kReportFieldsRow = 5;
 constexpr int kReportFieldsCol = 8;
 constexpr int kMaxGroups = 4;     // upper bound of pass::kGroups (partial buffer sizing)
@@ -114,12 +114,11 @@ struct cf_plan {
     cf::DevBuf<int32_t> tile_big;      // big-cone id of a tile, -1 otherwise
     cf::DevBuf<int32_t> big_cone;      // cone index of each big cone
     int64_t n_big = 0;
-    cf::DevBuf<int4> row_tb, col_tb;   // tile table {first segment, first nonzero, first joff, maxlen}
+    cf::DevBuf<int4> row_tb, col_tb;   // tile table {first segment, first nonzero, normal (1) / long (0), 0}
     // jagged-diagonal copies of the CSR panels (rj_*) and of the CSC (cj_*) read by the passes
     cf::DevBuf<int32_t> rj_idx, cj_idx;
     cf::DevBuf<double> rj_val, cj_val;
-    cf::DevBuf<uint8_t> rj_perm, cj_perm;
-    cf::DevBuf<uint16_t> rj_joff, cj_joff;
+    cf::DevBuf<uint32_t> rj_pl, cj_pl;  // per segment position: perm (rank -> segment) | length << 5 | block start << 14
     int64_t row_tiles = 0, col_tiles = 0;
     // row-pass column panels: the CSR is stored panel-major (segment = panel*m + row)
     // so each row-pass launch gathers only one panel's slice of x (L2-resident)

@@ -78,7 +78,6 @@ static_assert(kTileSeg == pass::kPSeg && kTileNnz == pass::kPCap, "host tile cut
 using pass::kComputeThreads;
 using pass::kPSeg;
 using pass::Smem;
-using pass::Stage;
 
 // ---------------------------------------------------------------- pass policies
 // A policy supplies the gathered operand, the per-segment epilogue vectors
@@ -89,9 +88,12 @@ struct Layout {
     const double* g_;
     static constexpr bool kGroupEpilogue = false;
     static constexpr int kUnroll = pass::kUnroll;   // gathers in flight per thread
+    static constexpr int kMinBlocks = pass::kMinBlocks;
     __device__ __forceinline__ const double* gvec() const { return g_; }
+    static constexpr int kVals = 0;
+    __device__ __forceinline__ void load_async(int, double*) const {}
     __device__ __forceinline__ bool carry_in() const { return false; }
-    __device__ __forceinline__ double carry(const Vals&) const { return 0.0; }
+    __device__ __forceinline__ double carry(int) const { return 0.0; }
     __device__ __forceinline__ void check(double, int, double) {}
     __device__ __forceinline__ void group(Smem&, int, int, int) {}
     __device__ __forceinline__ void finish(Smem&) {}
@@ -116,20 +118,19 @@ struct RowIter : Layout {
     const double* rcorr;   // optional: warm-start U eps / mu
     double mu;
     pass::MuDiv div;
+    static constexpr int kVals = 4;   // b, lam, fu, d*b (last panel only)
     __device__ __forceinline__ bool carry_in() const { return has_carry; }
-    __device__ __forceinline__ double carry(const Vals& v) const { return v.v[4]; }
-    __device__ __forceinline__ Vals load(int s) const {
+    __device__ __forceinline__ double carry(int s) const {
+        return pass::ld_first(carry_buf + (s - seg_off), pass::pol_first());
+    }
+    __device__ __forceinline__ void load_async(int s, double* slot) const {
+        if (!last) return;
         const uint64_t pf = pass::pol_first();
         const int64_t i = s - seg_off;
-        Vals v{};
-        if (last) {
-            v.v[0] = pass::ld_first(b + i, pf);
-            v.v[1] = pass::ld_first(lam + i, pf);
-            v.v[2] = pass::ld_first(fu + i, pf);
-            v.v[3] = pass::ld_first(db + i, pf);
-        }
-        if (has_carry) v.v[4] = pass::ld_first(carry_buf + i, pf);
-        return v;
+        pass::cp_async8(slot, b + i, pf);
+        pass::cp_async8(slot + 32, lam + i, pf);
+        pass::cp_async8(slot + 64, fu + i, pf);
+        pass::cp_async8(slot + 96, db + i, pf);
     }
     __device__ __forceinline__ void segment(Smem&, int, int s0, int q, int, double axi, const Vals& v) {
         const int64_t i = s0 + q - seg_off;
@@ -158,12 +159,7 @@ struct RowSpmv : Layout {
     bool has_carry;
     double* y;
     __device__ __forceinline__ bool carry_in() const { return has_carry; }
-    __device__ __forceinline__ double carry(const Vals& v) const { return v.v[4]; }
-    __device__ __forceinline__ Vals load(int s) const {
-        Vals v{};
-        if (has_carry) v.v[4] = y[s - seg_off];
-        return v;
-    }
+    __device__ __forceinline__ double carry(int s) const { return y[s - seg_off]; }
     __device__ __forceinline__ void segment(Smem&, int, int s0, int q, int, double acc, const Vals&) {
         y[s0 + q - seg_off] = acc;
     }
@@ -172,7 +168,6 @@ struct RowSpmv : Layout {
 // x = A^T y (apply_V . apply_Ut)
 struct ColSpmv : Layout {
     double* y;
-    __device__ __forceinline__ Vals load(int) const { return Vals{}; }
     __device__ __forceinline__ void segment(Smem&, int, int s0, int q, int, double acc, const Vals&) {
         y[s0 + q] = acc;
     }
@@ -184,14 +179,13 @@ struct ColVecs : Layout {
     const double* z_in;
     const double* d_in;
     const double* c;
-    __device__ __forceinline__ Vals load(int j) const {
+    static constexpr int kVals = 4;
+    __device__ __forceinline__ void load_async(int j, double* slot) const {
         const uint64_t pf = pass::pol_first();
-        Vals v{};
-        v.v[0] = pass::ld_first(x_in + j, pf);
-        v.v[1] = pass::ld_first(z_in + j, pf);
-        v.v[2] = pass::ld_first(d_in + j, pf);
-        v.v[3] = pass::ld_first(c + j, pf);
-        return v;
+        pass::cp_async8(slot, x_in + j, pf);
+        pass::cp_async8(slot + 32, z_in + j, pf);
+        pass::cp_async8(slot + 64, d_in + j, pf);
+        pass::cp_async8(slot + 96, c + j, pf);
     }
 };
 
@@ -271,7 +265,8 @@ struct ColIter : ColVecs {
 // finiteness of x, z, delta (the implicit y and gamma are checked per row by
 // k_row_report). Per-thread partials are reduced once per CTA (finish).
 struct ColReport : ColVecs {
-    static constexpr int kUnroll = 12;   // 8 report accumulators per thread: a little less in flight
+    static constexpr int kUnroll = 8;      // 8 report accumulators per thread
+    static constexpr int kMinBlocks = 2;   // (more registers; runs once per check_every iterations)
     double* part;          // [kReportFieldsCol][kGroups][gridDim.x]
     double d2, dmx, s2, smx, amx, cx, cg, nf;
     __device__ __forceinline__ void segment(Smem&, int, int, int, int, double atl, const Vals& vv) {
@@ -537,8 +532,8 @@ pass::Tiles row_panel_tiles(const cf_plan* p, int panel) {
     return pass::Tiles{p->row_tb.p + t0, (int32_t)(t1 - t0)};
 }
 pass::Tiles col_tiles(const cf_plan* p) { return pass::Tiles{p->col_tb.p, (int32_t)p->col_tiles}; }
-pass::Jds row_jds(const cf_plan* p) { return pass::Jds{p->rj_idx.p, p->rj_val.p, p->rj_perm.p, p->rj_joff.p}; }
-pass::Jds col_jds(const cf_plan* p) { return pass::Jds{p->cj_idx.p, p->cj_val.p, p->cj_perm.p, p->cj_joff.p}; }
+pass::Jds row_jds(const cf_plan* p) { return pass::Jds{p->rj_idx.p, p->rj_val.p, p->rj_pl.p}; }
+pass::Jds col_jds(const cf_plan* p) { return pass::Jds{p->cj_idx.p, p->cj_val.p, p->cj_pl.p}; }
 
 template <class P>
 int persistent_grid(int n_tiles) {
@@ -546,9 +541,9 @@ int persistent_grid(int n_tiles) {
     static int sms = 0;
     if (per_sm < 0) {
         CF_CUDA(cudaFuncSetAttribute(pass::k_pass<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)pass::kSmemBytes));
+                                     (int)pass::smem_bytes<P>()));
         CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pass::k_pass<P>, pass::kPThreads,
-                                                              pass::kSmemBytes));
+                                                              pass::smem_bytes<P>()));
         int dev = 0;
         CF_CUDA(cudaGetDevice(&dev));
         CF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -564,7 +559,7 @@ int launch_pass(const P& pol, const pass::Jds& L, const pass::Tiles& T, const in
     if (T.n_tiles == 0) return CF_OK;
     const int grid = persistent_grid<P>(T.n_tiles);
     if (grid_out) *grid_out = grid;
-    pass::k_pass<P><<<grid, pass::kPThreads, pass::kSmemBytes, st>>>(pol, L, T, done);
+    pass::k_pass<P><<<grid, pass::kPThreads, pass::smem_bytes<P>(), st>>>(pol, L, T, done);
     CF_LAUNCHED();
     return CF_OK;
 }

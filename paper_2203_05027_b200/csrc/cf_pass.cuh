@@ -1,33 +1,31 @@
-// Persistent, TMA-pipelined, warp-local jagged-diagonal tile engine for the sparse passes (sm_100a).
+// Persistent warp-local jagged-diagonal tile engine for the sparse passes (sm_100a).
 //
 // A pass walks one compressed layout (CSR panels for the row pass, CSC for the
 // column pass) tile by tile. A tile is a run of <= kPSeg segments (rows or
 // columns) with <= kPCap nonzeros, cut on the host (cf_setup.cu), or one
-// segment longer than kMaxDiag ("long tile", streamed in chunks).
+// segment longer than kMaxDiag ("long tile").
 //
 // Inside a normal tile every WARP BLOCK of 32 consecutive segments is stored
 // in jagged-diagonal order (k_build_jds): the block's segments are ranked by
 // length (descending, stable), rank r holds local segment perm[r], and the
-// k-th nonzero of rank r sits at joff_w[k] + r. So
-//   * lane r owns one segment: it gathers g[idx] for its nonzeros (kUnroll
-//     independent loads in flight) and sums the products SEQUENTIALLY in
+// k-th nonzero of rank r sits at k0 + start_w + sum_{j<k} width_j + r
+// (width_j = ranks longer than j). pl[rank] = perm | len << 5 | start_w << 14,
+// so each lane knows its own length and the offsets come from warp ballots.
+//   * lane r owns one segment: it loads idx/val of its nonzeros straight from
+//     global memory (a diagonal is contiguous, so the warp's loads coalesce;
+//     L1 no-allocate, L2 evict-first), gathers g[idx] (kUnroll independent
+//     loads in flight, L2 evict-last) and sums the products SEQUENTIALLY in
 //     canonical order — np.bincount's order (uv.py:10-12), bit-identical;
-//   * a warp reads idx/val of 32 segments at consecutive shared-memory
-//     addresses (conflict-free); lanes drop out in length order;
 //   * the rank -> natural-order transpose of the sums stays inside the warp, so
 //     the epilogue runs in natural segment order with no CTA barrier: its
 //     vectors are loaded straight from global memory (coalesced, issued at
-//     tile start so they arrive during the gathers) and its stores coalesce.
-// The L1TEX pipe's ~1 random sector per SM-cycle (the gathers) is then the
-// dominant consumer of the only hot on-chip resource.
-//
-// Warp roles: per compute group (kPSeg threads) one producer warp issues
-// cp.async.bulk (TMA 1D) copies of a future tile's idx/val/perm/joff into the
-// group's slots of a kStages ring (full[s] mbarrier, L2 evict-first hint on
-// every streamed byte); the group's warps consume (empty[s] when done).
-// Groups alternate tiles; a group needs a barrier only for cone epilogues and
-// long tiles. The ring is kept small on purpose: shared memory beyond ~150 KB
-// per SM starves the L1 that the outstanding gathers need (profiles/r01_probes.md).
+//     block start so they arrive during the gathers) and its stores coalesce.
+// Nothing is staged in shared memory. Measured (profiles/r01_probes.md): a
+// random fp64 gather costs one L1TEX->L2 request, ~1 per SM-cycle, and that
+// request port is the bound; TMA bulk staging of idx/val added ~40 % to a
+// pass and shared memory above ~128 KB per SM starves the L1 the gathers need.
+// So each CTA is one group of kPSeg threads (one warp per warp block), several
+// CTAs per SM, a few KB of shared memory for the transposes and cone epilogues.
 #pragma once
 
 #include <cmath>
@@ -38,14 +36,23 @@
 namespace cf {
 namespace pass {
 
-#ifndef CF_STAGES
-#define CF_STAGES 4
-#endif
-#ifndef CF_GROUPS
-#define CF_GROUPS 2
+#ifndef CF_TMA
+#define CF_TMA 0                   // 1: producer-warp TMA ring; 0: direct coalesced loads (measured faster)
 #endif
 #ifndef CF_UNROLL
-#define CF_UNROLL 20
+#define CF_UNROLL 3
+#endif
+#ifndef CF_MINB
+#define CF_MINB 6                  // (direct engine) resident CTAs per SM the registers are sized for
+#endif
+#ifndef CF_STAGES
+#define CF_STAGES 4                // (TMA engine) ring depth, all groups
+#endif
+#ifndef CF_GROUPS
+#define CF_GROUPS 2                // (TMA engine) compute groups per CTA
+#endif
+#ifndef CF_PIPE
+#define CF_PIPE 0                  // (direct engine) software-pipelined idx/val loads across diagonals and blocks
 #endif
 #ifndef CF_GATHER_NOALLOC
 #define CF_GATHER_NOALLOC 1        // gathers bypass L1 allocation (measured: +3%)
@@ -56,41 +63,58 @@ namespace pass {
 #ifndef CF_PSEG
 #define CF_PSEG 256
 #endif
-constexpr int kPCap = CF_PCAP;     // nonzeros per staged tile
+constexpr int kPCap = CF_PCAP;     // nonzeros per tile
 constexpr int kPSeg = CF_PSEG;     // segments per tile (== threads of a compute group)
 constexpr int kMaxDiag = 256;      // longest segment inside a normal tile (longer ones get their own tile)
-constexpr int kStages = CF_STAGES; // ring depth (all groups)
-constexpr int kGroups = CF_GROUPS; // compute groups; group g consumes the CTA's tiles i = g, g+kGroups, ...
 constexpr int kUnroll = CF_UNROLL; // independent gathers in flight per thread
 constexpr int kComputeWarps = kPSeg / 32;      // per group
 constexpr int kComputeThreads = kPSeg;         // per group
+#if CF_TMA
+constexpr int kGroups = CF_GROUPS; // group g consumes the CTA's tiles i = g, g+kGroups, ...
+constexpr int kStages = CF_STAGES;
 constexpr int kPThreads = kGroups * (kComputeThreads + 32);   // + one producer warp per group
-constexpr int kJoffHdr = 2 * kComputeWarps;    // per-warp {start, maxlen} header of a tile's joff
-constexpr int kJoffMax = kJoffHdr + kComputeWarps * (kMaxDiag + 1);
-constexpr int kFvTab = 256;
+constexpr int kMinBlocks = 1;
 static_assert(kStages % kGroups == 0, "a ring slot must be reused by the same compute group (mbarrier parity)");
+#else
+constexpr int kGroups = 1;
+constexpr int kPThreads = kComputeThreads;
+constexpr int kMinBlocks = CF_MINB;
+#endif
+constexpr int kLongChunk = kComputeWarps * 128;   // long tiles: products buffered per chunk (in the vals buffer)
+constexpr int kFvTab = 256;
+constexpr int kPlPermBits = 5, kPlLenBits = 9;
+static_assert(kMaxDiag < (1 << kPlLenBits), "segment length must fit pl");
 
+#if CF_TMA
 struct alignas(16) Stage {
     int32_t meta[4];                    // s0, nseg, k0, len (written by the producer)
-    int32_t meta2[4];                   // joff length (0 = long tile), first joff entry
+    int32_t meta2[4];                   // normal (1) / long (0) tile
     int32_t idx[kPCap + 8];
     double val[kPCap + 4];
-    uint8_t perm[kPSeg + 16];
-    uint16_t joff[kJoffMax + 16];
+    uint32_t pl[kPSeg + 4];
 };
+#endif
 
 struct Smem {
+#if CF_TMA
     Stage st[kStages];
     alignas(8) uint64_t full[kStages];
     alignas(8) uint64_t empty[kStages];
+#endif
     double fvtab[kFvTab];               // 1/(1+cnt) for small column counts (uv.py:82)
     double wacc[kGroups][kPSeg];        // rank -> natural transpose of the sums (warp-private slices)
     int32_t wcnt[kGroups][kPSeg];
-    double cscr[kGroups][4][kPSeg];     // cone epilogue: x+, w, delta, delta+
     double red[kGroups][32];
+    double vals[kGroups * kComputeWarps][4][32];  // epilogue vectors of a warp block (cp.async); long tiles: products
+    double cscr[kGroups][4][kPSeg];     // cone epilogue only: x+, w, delta, delta+ (last member)
 };
+static_assert(sizeof(((Smem*)0)->vals) / kGroups >= kLongChunk * sizeof(double), "long-tile buffer");
 
 constexpr size_t kSmemBytes = sizeof(Smem);
+// policies without a cone epilogue do not allocate the cone scratch
+constexpr size_t kSmemBytesNoCones = offsetof(Smem, cscr);
+template <class P>
+constexpr size_t smem_bytes() { return P::kGroupEpilogue ? kSmemBytes : kSmemBytesNoCones; }
 
 // x / mu; exact multiply when mu is a power of two (then x * (1/mu) == x / mu bit for bit)
 struct MuDiv {
@@ -105,7 +129,8 @@ __host__ inline MuDiv make_mudiv(double mu) {
     return d;
 }
 
-// Epilogue vectors of one segment, loaded by the policy (natural order, coalesced).
+// Epilogue vectors of one segment (natural order), copied global -> shared by
+// cp.async at block start (no registers held while the gathers are in flight).
 struct Vals {
     double v[5];
 };
@@ -124,44 +149,19 @@ __device__ __forceinline__ uint64_t pol_last() {
     asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred P1;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-        "@!P1 bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_addr(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
-        "%4;" ::"r"(smem_addr(dst)),
-        "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
-        : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
-
 // compute group of the calling thread and its thread index inside the group
+#if CF_TMA
 __device__ __forceinline__ int group_id() { return (int)threadIdx.x / kComputeThreads; }
 __device__ __forceinline__ int group_tid() { return (int)threadIdx.x % kComputeThreads; }
 // named barrier of the caller's compute group (ids 1..kGroups; 0 is __syncthreads)
 __device__ __forceinline__ void group_sync() {
     asm volatile("bar.sync %0, %1;" ::"r"(1 + group_id()), "n"(kComputeThreads) : "memory");
 }
+#else
+__device__ __forceinline__ int group_id() { return 0; }
+__device__ __forceinline__ int group_tid() { return (int)threadIdx.x; }
+__device__ __forceinline__ void group_sync() { __syncthreads(); }
+#endif
 
 // deterministic reduction over the caller's compute group; result valid in its thread 0
 template <class Op>
@@ -204,6 +204,153 @@ __device__ __forceinline__ void st_hint(double* p, double v, uint64_t pol) {
     asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
 }
 
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, uint64_t pol) {
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(smem_addr(dst)), "l"(src),
+                 "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// Tile table: tb[t] = {first segment, first nonzero, normal (1) / long (0), 0};
+// tile t spans [tb[t].x, tb[t+1].x) segments and [tb[t].y, tb[t+1].y) nonzeros.
+struct Tiles {
+    const int4* tb;
+    int32_t n_tiles;
+};
+
+// The JDS layout of a pass: idx/val in warp-local jagged-diagonal order inside
+// every normal tile (canonical order inside long tiles); pl per segment
+// position = local segment of rank r in the warp block | its length << 5 |
+// the block's first nonzero (tile-relative) << 14.
+struct Jds {
+    const int32_t* idx;
+    const double* val;
+    const uint32_t* pl;
+};
+
+// L2 prefetch (TMA unit, no data returned to the SM) of [first, first+count)
+template <class T>
+__device__ __forceinline__ void prefetch_l2(const T* first, int64_t count) {
+    if (count <= 0) return;
+    const uintptr_t a = (uintptr_t)first & ~(uintptr_t)15u;
+    const uintptr_t e = ((uintptr_t)(first + count) + 15u) & ~(uintptr_t)15u;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)(e - a)) : "memory");
+}
+__device__ __forceinline__ void prefetch_tile(const Jds& L, const Tiles& T, int tile) {
+    if (tile >= T.n_tiles) return;
+    const int4 lo = __ldg(T.tb + tile), hi = __ldg(T.tb + tile + 1);
+    prefetch_l2(L.idx + lo.y, hi.y - lo.y);
+    prefetch_l2(L.val + lo.y, hi.y - lo.y);
+    if (lo.z) prefetch_l2(L.pl + lo.x, hi.x - lo.x);
+}
+
+// ---------------------------------------------------------------- the engine
+// P (the pass policy) provides (device):
+//   const double* gvec() const                 gathered operand
+//   static constexpr int kVals                 epilogue vectors per segment (<= 4)
+//   void load_async(int s, double* slot) const cp.async vector f of segment s (global index) to slot[32 f]
+//   bool carry_in() const; double carry(int s) const   starting value of a segment's sum
+//   static constexpr int kUnroll               gathers in flight per thread
+//   static constexpr int kMinBlocks            resident CTAs per SM the registers are sized for
+//   static constexpr bool kGroupEpilogue       epilogue needs all segments of the tile at once (cones)
+//   void check(double a, int j, double g)      per-nonzero hook (report finiteness)
+//   void segment(Smem&, int tile, int s0, int q, int cnt, double acc, const Vals&)
+//                                              epilogue of local segment q (natural order)
+//   void group(Smem&, int tile, int s0, int nseg)   (kGroupEpilogue) after a group barrier
+//   void finish(Smem&)                         compute threads, after the last tile
+// rank r's pl entry -> its length, and the block's first nonzero (from rank 0)
+__device__ __forceinline__ int pl_len(uint32_t pr) { return (int)((pr >> kPlPermBits) & ((1u << kPlLenBits) - 1u)); }
+__device__ __forceinline__ int pl_start(uint32_t pr) { return (int)(pr >> (kPlPermBits + kPlLenBits)); }
+
+// idx/val of diagonals [k, k+U) of the caller's warp block; pos advances past them
+template <int U>
+__device__ __forceinline__ void load_batch(const Jds& L, int (&nj)[U], double (&nv)[U], int& pos, int mylen, int k,
+                                           uint64_t pf) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const bool ok = mylen > k + u;
+        nj[u] = ok ? ld_first(L.idx + pos, pf) : 0;
+        nv[u] = ok ? ld_first(L.val + pos, pf) : 0.0;
+        pos += __popc(__ballot_sync(0xffffffffu, ok));   // width of diagonal k+u
+    }
+}
+
+// long tile: one segment [k0, k0+len) in canonical order; the products of a
+// chunk are buffered and summed in order by thread 0
+template <class P>
+__device__ __forceinline__ void long_tile(P& p, Smem& sm, const Jds& L, int tile, int s0, int k0, int len) {
+    const int gt = group_tid(), grp = group_id();
+    const uint64_t pf = pol_first(), pl_ = pol_last();
+    const double* __restrict__ g = p.gvec();
+    double* lacc = sm.wacc[grp];
+    double* lbuf = &sm.vals[grp * kComputeWarps][0][0];
+    Vals vv{};
+    group_sync();   // the previous tile's epilogue vectors (same buffer) are consumed
+    if (gt == 0) {
+        if (P::kVals > 0) {
+            p.load_async(s0, &lacc[1]);
+            cp_async_commit();
+            cp_async_wait_all();
+            for (int f = 0; f < P::kVals; ++f) vv.v[f] = lacc[1 + 32 * f];
+        }
+        lacc[0] = p.carry_in() ? p.carry(s0) : 0.0;
+    }
+    group_sync();
+    for (int c0 = 0; c0 < len; c0 += kLongChunk) {
+        const int cl = min(kLongChunk, len - c0);
+        for (int e = gt; e < cl; e += kComputeThreads) {
+            const int jj = ld_first(L.idx + k0 + c0 + e, pf);
+            const double a = ld_first(L.val + k0 + c0 + e, pf);
+            const double gj = ld_gather(g + jj, pl_);
+            p.check(a, jj, gj);
+            lbuf[e] = __dmul_rn(a, gj);
+        }
+        group_sync();
+        if (gt == 0) {
+            double acc = lacc[0];
+            for (int e = 0; e < cl; ++e) acc = __dadd_rn(acc, lbuf[e]);
+            lacc[0] = acc;
+        }
+        group_sync();
+    }
+    if (gt == 0) p.segment(sm, tile, s0, 0, len, lacc[0], vv);
+    group_sync();
+}
+
+#if CF_TMA
+// PTX: mbarriers and TMA bulk copies (producer-warp ring)
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
+        "%4;" ::"r"(smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+
 // Aligned superset copy of `count` elements starting at `first`: the copy
 // starts at the 16-byte boundary below `first`; element 0 lands at lead_of(first).
 template <class T>
@@ -223,58 +370,29 @@ __device__ __forceinline__ void copy_span(void* dst, const T* first, int64_t cou
     if (bytes) bulk_g2s(dst, (const void*)((uintptr_t)first & ~(uintptr_t)15u), bytes, bar, pol);
 }
 
-// Tile table: tb[t] = {first segment, first nonzero, first joff entry, joff length (0 = long tile)};
-// tile t spans [tb[t].x, tb[t+1].x) segments and [tb[t].y, tb[t+1].y) nonzeros.
-struct Tiles {
-    const int4* tb;
-    int32_t n_tiles;
-};
-
-// The JDS layout of a pass: idx/val in warp-local jagged-diagonal order inside
-// every normal tile (canonical order inside long tiles); perm (rank -> local
-// segment of the warp block, one byte per segment position); joff per tile =
-// {start, maxlen} per warp block, then every block's diagonal starts
-// (tile-relative nonzero offsets).
-struct Jds {
-    const int32_t* idx;
-    const double* val;
-    const uint8_t* perm;
-    const uint16_t* joff;
-};
-
-// ---------------------------------------------------------------- the engine
-// P (the pass policy) provides (device):
-//   const double* gvec() const                 gathered operand
-//   Vals load(int s) const                     epilogue vectors of segment s (global index, natural order)
-//   bool carry_in() const; double carry(const Vals&) const   starting value of a segment's sum
-//   static constexpr int kUnroll               gathers in flight per thread
-//   static constexpr bool kGroupEpilogue       epilogue needs all segments of the tile at once (cones)
-//   void check(double a, int j, double g)      per-nonzero hook (report finiteness)
-//   void segment(Smem&, int tile, int s0, int q, int cnt, double acc, const Vals&)
-//                                              epilogue of local segment q (natural order)
-//   void group(Smem&, int tile, int s0, int nseg)   (kGroupEpilogue) after a group barrier
-//   void finish(Smem&)                         compute threads, after the last tile
 __device__ __forceinline__ void issue_tile(const Jds& L, int4 lo, int4 hi, Stage& st, uint64_t* bar, uint64_t pol) {
-    const int s0 = lo.x, nseg = hi.x - lo.x, k0 = lo.y, len = hi.y - lo.y, j0 = lo.z, jn = lo.w;
+    const int s0 = lo.x, nseg = hi.x - lo.x, k0 = lo.y, len = hi.y - lo.y, normal = lo.z;
     st.meta[0] = s0;
     st.meta[1] = nseg;
     st.meta[2] = k0;
     st.meta[3] = len;
-    st.meta2[0] = jn;
-    st.meta2[1] = j0;
-    if (jn == 0) {  // long tile: nothing staged (streamed by the consumers)
+    st.meta2[0] = normal;
+    if (!normal) {  // long tile: nothing staged (streamed by the consumers)
         mbar_expect_tx(bar, 0);
         return;
     }
-    const uint32_t total = span_bytes(L.idx + k0, len) + span_bytes(L.val + k0, len) +
-                           span_bytes(L.perm + s0, nseg) + span_bytes(L.joff + j0, jn);
+    const uint32_t total =
+        span_bytes(L.idx + k0, len) + span_bytes(L.val + k0, len) + span_bytes(L.pl + s0, nseg);
     mbar_expect_tx(bar, total);
     copy_span(st.idx, L.idx + k0, len, bar, pol);
     copy_span(st.val, L.val + k0, len, bar, pol);
-    copy_span(st.perm, L.perm + s0, nseg, bar, pol);
-    copy_span(st.joff, L.joff + j0, jn, bar, pol);
+    copy_span(st.pl, L.pl + s0, nseg, bar, pol);
 }
 
+// Per compute group (kPSeg threads) one producer warp copies a future tile's
+// idx/val/pl into the group's slots of a kStages ring with cp.async.bulk (TMA
+// 1D; full[s] mbarrier, L2 evict-first); the group's warps consume (empty[s]).
+// Groups alternate tiles. Inside a tile, warp w takes warp block w.
 template <class P>
 __global__ void __launch_bounds__(kPThreads, 1) k_pass(const P p0, const Jds L, const Tiles T, const int32_t* done) {
     if (done && *done) return;
@@ -299,7 +417,6 @@ __global__ void __launch_bounds__(kPThreads, 1) k_pass(const P p0, const Jds L, 
         const int pg = warp - kGroups * kComputeWarps;
         if (lane == 0) {
             const uint64_t pf = pol_first();
-            // the next tile's table entries are loaded before waiting for its slot
             int4 lo = make_int4(0, 0, 0, 0), hi = lo;
             if (pg < my) {
                 lo = T.tb[blockIdx.x + pg * G];
@@ -325,110 +442,82 @@ __global__ void __launch_bounds__(kPThreads, 1) k_pass(const P p0, const Jds L, 
     }
 
     // ---------------------------------------------------- compute warps
-    const uint64_t pl = pol_last(), pf = pol_first();
     const double* __restrict__ g = p.gvec();
     const int grp = group_id();
     const int gt = group_tid();
     const int gw = gt >> 5;      // warp within the group = warp block of the tile
     double* wacc = sm.wacc[grp] + gw * 32;
     int32_t* wcnt = sm.wcnt[grp] + gw * 32;
+    double* slot = &sm.vals[grp * kComputeWarps + gw][0][lane];
+    constexpr int U = P::kUnroll;
     for (int i = grp; i < my; i += kGroups) {
         const int s = i % kStages;
         Stage& st = sm.st[s];
         mbar_wait(&sm.full[s], (uint32_t)((i / kStages) & 1));
         const int s0 = st.meta[0], nseg = st.meta[1], k0 = st.meta[2], len = st.meta[3];
-        const int jn = st.meta2[0];
         const int tile = (int)blockIdx.x + i * G;
-        if (jn > 0) {
+        if (st.meta2[0]) {
             const int nb = min(32, nseg - gw * 32);   // segments of this warp block
             if (nb > 0) {
+                const bool nat = lane < nb;             // natural segment gw*32 + lane exists
+                const int seg = s0 + gw * 32 + lane;
+                if (P::kVals > 0) {
+                    if (nat) p.load_async(seg, slot);
+                    cp_async_commit();
+                }
                 const int32_t* ib = st.idx + lead_of(L.idx + k0);
                 const double* vb = st.val + lead_of(L.val + k0);
-                const uint8_t* pb = st.perm + lead_of(L.perm + s0) + gw * 32;
-                const uint16_t* jh = st.joff + lead_of(L.joff + st.meta2[1]);
-                const uint16_t* jb = jh + jh[2 * gw];   // this block's diagonal starts
-                const int mlen = jh[2 * gw + 1];
-                const bool nat = lane < nb;             // natural segment gw*32 + lane exists
-                const Vals vv = nat ? p.load(s0 + gw * 32 + lane) : Vals{};
-                const int r = lane;                     // rank within the block
-                const int q = nat ? (int)pb[r] : 0;     // local segment (within the block) of rank r
-                const double c0 = p.carry_in() ? p.carry(vv) : 0.0;
-                double acc = __shfl_sync(0xffffffffu, c0, q);
-                int cnt = 0;
-                constexpr int U = P::kUnroll;
+                const uint32_t pr = nat ? st.pl[lead_of(L.pl + s0) + gw * 32 + lane] : 0u;
+                const int q = (int)(pr & 31u);          // local segment (within the block) of rank r
+                const int mylen = pl_len(pr);
+                const int mlen = __shfl_sync(0xffffffffu, mylen, 0);   // rank 0 is the longest
+                int pos = __shfl_sync(0xffffffffu, pl_start(pr), 0) + lane;
+                // rank r's own carry (no shuffle: the load's latency hides behind the gathers)
+                double acc = (p.carry_in() && nat) ? p.carry(s0 + gw * 32 + q) : 0.0;
                 for (int k = 0; k < mlen; k += U) {
-                    int e[U];
-                    bool ok[U];
-                    bool any = false;
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const int kk = k + u;
-                        const int a = kk < mlen ? (int)jb[kk] : 0;
-                        const int b = kk < mlen ? (int)jb[kk + 1] : 0;
-                        ok[u] = nat && (b - a) > r;
-                        e[u] = a + r;
-                        any |= ok[u];
-                    }
-                    if (!__any_sync(0xffffffffu, any)) break;
+                    // indices first; the values are read from shared memory only
+                    // when the gathers land (keeps U fewer doubles live)
+                    const int p0 = pos;
                     int jj[U];
-                    double av[U], gv[U];
+                    double gv[U];
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
-                        jj[u] = ok[u] ? ib[e[u]] : 0;
-                        av[u] = ok[u] ? vb[e[u]] : 0.0;
+                        const bool ok = mylen > k + u;
+                        jj[u] = ok ? ib[pos] : 0;
+                        pos += __popc(__ballot_sync(0xffffffffu, ok));   // width of diagonal k+u
                     }
-#pragma unroll
-#ifdef CF_EXP_LOCALGATHER
-                    for (int u = 0; u < U; ++u) gv[u] = ok[u] ? ld_gather(g + (jj[u] & 4095), pl) : 0.0;
-#else
-                    for (int u = 0; u < U; ++u) gv[u] = ok[u] ? ld_gather(g + jj[u], pl) : 0.0;
-#endif
 #pragma unroll
                     for (int u = 0; u < U; ++u)
-                        if (ok[u]) {
-                            p.check(av[u], jj[u], gv[u]);
-                            acc = __dadd_rn(acc, __dmul_rn(av[u], gv[u]));
-                            ++cnt;
+                        gv[u] = (mylen > k + u) ? ld_gather(g + jj[u], pol_last()) : 0.0;
+                    int p1 = p0;
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const bool ok = mylen > k + u;
+                        if (ok) {
+                            const double a = vb[p1];
+                            p.check(a, jj[u], gv[u]);
+                            acc = __dadd_rn(acc, __dmul_rn(a, gv[u]));
                         }
+                        p1 += __popc(__ballot_sync(0xffffffffu, ok));
+                    }
                 }
-                // rank -> natural order inside the warp
+                // rank -> natural order inside the warp (a segment's count is its length)
                 if (nat) {
                     wacc[q] = acc;
-                    wcnt[q] = cnt;
+                    wcnt[q] = mylen;
+                }
+                Vals vv{};
+                if (P::kVals > 0) {
+                    cp_async_wait_all();
+#pragma unroll
+                    for (int f = 0; f < P::kVals; ++f) vv.v[f] = slot[32 * f];
                 }
                 __syncwarp();
                 if (nat) p.segment(sm, tile, s0, gw * 32 + lane, wcnt[lane], wacc[lane], vv);
                 __syncwarp();
             }
         } else {
-            // long tile: one segment [k0, k0+len), canonical order, chunked through the stage
-            double* buf = st.val;
-            double* lacc = sm.wacc[grp];
-            Vals vv{};
-            if (gt == 0) {
-                vv = p.load(s0);
-                lacc[0] = p.carry_in() ? p.carry(vv) : 0.0;
-            }
-            group_sync();
-            for (int c0 = 0; c0 < len; c0 += kPCap) {
-                const int cl = min(kPCap, len - c0);
-                for (int e = gt; e < cl; e += kComputeThreads) {
-                    const int jj = ld_first(L.idx + k0 + c0 + e, pf);
-                    const double a = ld_first(L.val + k0 + c0 + e, pf);
-                    const double gj = ld_gather(g + jj, pl);
-                    p.check(a, jj, gj);
-                    buf[e] = __dmul_rn(a, gj);
-                }
-                group_sync();
-                if (gt == 0) {
-                    double acc = lacc[0];
-                    for (int e = 0; e < cl; ++e) acc = __dadd_rn(acc, buf[e]);
-                    lacc[0] = acc;
-                }
-                group_sync();
-            }
-            if (gt == 0) p.segment(sm, tile, s0, 0, len, lacc[0], vv);
-            group_sync();
+            long_tile(p, sm, L, tile, s0, k0, len);
         }
         if (P::kGroupEpilogue) {
             group_sync();
@@ -440,6 +529,216 @@ __global__ void __launch_bounds__(kPThreads, 1) k_pass(const P p0, const Jds L, 
     }
     p.finish(sm);
 }
+
+#elif CF_PIPE
+// Each warp streams its warp blocks (block gw of tiles blockIdx.x, +G, ...) as
+// one software pipeline: idx/val of the next U diagonals — or of the first U
+// diagonals of its next block — are loaded while the current gathers are in
+// flight, so a block's dependent chain (pl -> idx -> gather) is hidden.
+template <class P>
+__global__ void __launch_bounds__(kPThreads, P::kMinBlocks) k_pass(const P p0, const Jds L, const Tiles T,
+                                                               const int32_t* done) {
+    if (done && *done) return;
+    P p = p0;  // per-thread mutable copy (report accumulators live in registers)
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+    const int G = gridDim.x;
+    const int lane = threadIdx.x & 31;
+    const int gt = threadIdx.x;
+    const int gw = gt >> 5;      // warp = warp block of the tile
+    for (int c = gt; c < kFvTab; c += kPThreads) sm.fvtab[c] = 1.0 / (1.0 + (double)c);
+    __syncthreads();
+    const uint64_t pl_ = pol_last(), pf = pol_first();
+    const double* __restrict__ g = p.gvec();
+    const int32_t* plw = reinterpret_cast<const int32_t*>(L.pl);
+    double* wacc = sm.wacc[0] + gw * 32;
+    int32_t* wcnt = sm.wcnt[0] + gw * 32;
+    constexpr int U = P::kUnroll;
+
+    int tile = blockIdx.x;
+    int4 lo = make_int4(0, 0, 0, 0), hi = lo;
+    int nb = 0;          // segments of this warp's block in the current tile (<= 0: none)
+    uint32_t pr = 0;     // this lane's pl entry
+    int mylen = 0, pos = 0;
+    int nj[U];
+    double nv[U];
+    if (tile < T.n_tiles) {
+        lo = __ldg(T.tb + tile);
+        hi = __ldg(T.tb + tile + 1);
+        nb = lo.z ? min(32, hi.x - lo.x - gw * 32) : 0;
+        pr = (nb > 0 && lane < nb) ? (uint32_t)ld_first(plw + lo.x + gw * 32 + lane, pf) : 0u;
+        mylen = pl_len(pr);
+        pos = lo.y + __shfl_sync(0xffffffffu, pl_start(pr), 0) + lane;
+        if (nb > 0) load_batch<U>(L, nj, nv, pos, mylen, 0, pf);
+    }
+    while (tile < T.n_tiles) {
+        // next tile of this CTA: its table entries and this warp's pl entry are loaded now
+        const int ntile = tile + G;
+        const bool has_next = ntile < T.n_tiles;
+        int4 nlo = lo, nhi = hi;
+        if (has_next) {
+            nlo = __ldg(T.tb + ntile);
+            nhi = __ldg(T.tb + ntile + 1);
+        }
+        const int nnb = (has_next && nlo.z) ? min(32, nhi.x - nlo.x - gw * 32) : 0;
+        const uint32_t npr = (nnb > 0 && lane < nnb) ? (uint32_t)ld_first(plw + nlo.x + gw * 32 + lane, pf) : 0u;
+        bool pre = false;    // next block's first batch already in nj/nv
+        const int nmylen = pl_len(npr);
+        int npos = 0;
+        const int s0 = lo.x, nseg = hi.x - lo.x, k0 = lo.y, len = hi.y - lo.y;
+        if (lo.z) {
+            if (nb > 0) {
+                const bool nat = lane < nb;             // natural segment gw*32 + lane exists
+                double* slot = &sm.vals[gw][0][lane];
+                if (P::kVals > 0) {
+                    if (nat) p.load_async(s0 + gw * 32 + lane, slot);
+                    cp_async_commit();
+                }
+                const int q = (int)(pr & 31u);          // local segment (within the block) of rank r
+                const int mlen = __shfl_sync(0xffffffffu, mylen, 0);   // rank 0 is the longest
+                // rank r's own carry (no shuffle: the load's latency hides behind the gathers)
+                double acc = (p.carry_in() && nat) ? p.carry(s0 + gw * 32 + q) : 0.0;
+                for (int k = 0; k < mlen; k += U) {
+                    double av[U], gv[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        gv[u] = (mylen > k + u) ? ld_gather(g + nj[u], pl_) : 0.0;
+                        av[u] = nv[u];
+                    }
+                    if (k + U < mlen) {
+                        load_batch<U>(L, nj, nv, pos, mylen, k + U, pf);
+                    } else if (nnb > 0) {
+                        npos = nlo.y + __shfl_sync(0xffffffffu, pl_start(npr), 0) + lane;
+                        load_batch<U>(L, nj, nv, npos, nmylen, 0, pf);
+                        pre = true;
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        if (mylen > k + u) {
+                            p.check(av[u], 0, gv[u]);
+                            acc = __dadd_rn(acc, __dmul_rn(av[u], gv[u]));
+                        }
+                }
+                // rank -> natural order inside the warp (a segment's count is its length)
+                if (nat) {
+                    wacc[q] = acc;
+                    wcnt[q] = mylen;
+                }
+                Vals vv{};
+                if (P::kVals > 0) {
+                    cp_async_wait_all();
+#pragma unroll
+                    for (int f = 0; f < P::kVals; ++f) vv.v[f] = slot[32 * f];
+                }
+                __syncwarp();
+                if (nat) p.segment(sm, tile, s0, gw * 32 + lane, wcnt[lane], wacc[lane], vv);
+                __syncwarp();
+            }
+        } else {
+            long_tile(p, sm, L, tile, s0, k0, len);
+        }
+        if (P::kGroupEpilogue) {
+            __syncthreads();
+            p.group(sm, tile, s0, nseg);
+            __syncthreads();   // cone scratch is rewritten by the next tile
+        }
+        if (!pre && nnb > 0) {
+            npos = nlo.y + __shfl_sync(0xffffffffu, pl_start(npr), 0) + lane;
+            load_batch<U>(L, nj, nv, npos, nmylen, 0, pf);
+        }
+        tile = ntile;
+        lo = nlo;
+        hi = nhi;
+        nb = nnb;
+        pr = npr;
+        mylen = nmylen;
+        pos = npos;
+    }
+    p.finish(sm);
+}
+
+#else
+// Each warp walks its warp blocks (block gw of tiles blockIdx.x, +G, ...):
+// pl -> idx/val of U diagonals -> U gathers -> sequential sums, then the
+// natural-order epilogue. Many resident warps hide the dependent chain.
+template <class P>
+__global__ void __launch_bounds__(kPThreads, P::kMinBlocks) k_pass(const P p0, const Jds L, const Tiles T,
+                                                               const int32_t* done) {
+    if (done && *done) return;
+    P p = p0;  // per-thread mutable copy (report accumulators live in registers)
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+    const int G = gridDim.x;
+    const int lane = threadIdx.x & 31;
+    const int gt = threadIdx.x;
+    const int gw = gt >> 5;      // warp = warp block of the tile
+    for (int c = gt; c < kFvTab; c += kPThreads) sm.fvtab[c] = 1.0 / (1.0 + (double)c);
+    __syncthreads();
+    constexpr int U = P::kUnroll;
+    for (int tile = blockIdx.x; tile < T.n_tiles; tile += G) {
+        const int4 lo = __ldg(T.tb + tile), hi = __ldg(T.tb + tile + 1);
+        const int s0 = lo.x, nseg = hi.x - lo.x, k0 = lo.y, len = hi.y - lo.y;
+        if (lo.z) {
+            const int nb = min(32, nseg - gw * 32);   // segments of this warp block
+            if (nb > 0) {
+                const bool nat = lane < nb;             // natural segment gw*32 + lane exists
+                const int seg = s0 + gw * 32 + lane;
+                const uint32_t pr =
+                    nat ? (uint32_t)ld_first(reinterpret_cast<const int32_t*>(L.pl) + seg, pol_first()) : 0u;
+                double* slot = &sm.vals[gw][0][lane];
+                if (P::kVals > 0) {
+                    if (nat) p.load_async(seg, slot);
+                    cp_async_commit();
+                }
+                const int q = (int)(pr & 31u);          // local segment (within the block) of rank r
+                const int mylen = pl_len(pr);
+                const int mlen = __shfl_sync(0xffffffffu, mylen, 0);   // rank 0 is the longest
+                int pos = k0 + __shfl_sync(0xffffffffu, pl_start(pr), 0) + lane;
+                // rank r's own carry (no shuffle: the load's latency hides behind the gathers)
+                double acc = (p.carry_in() && nat) ? p.carry(s0 + gw * 32 + q) : 0.0;
+                for (int k = 0; k < mlen; k += U) {
+                    int nj[U];
+                    double nv[U], gv[U];
+                    load_batch<U>(L, nj, nv, pos, mylen, k, pol_first());
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        gv[u] = (mylen > k + u) ? ld_gather(p.gvec() + nj[u], pol_last()) : 0.0;
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        if (mylen > k + u) {
+                            p.check(nv[u], nj[u], gv[u]);
+                            acc = __dadd_rn(acc, __dmul_rn(nv[u], gv[u]));
+                        }
+                }
+                // rank -> natural order inside the warp (a segment's count is its length)
+                double* wacc = sm.wacc[0] + gw * 32;
+                int32_t* wcnt = sm.wcnt[0] + gw * 32;
+                if (nat) {
+                    wacc[q] = acc;
+                    wcnt[q] = mylen;
+                }
+                Vals vv{};
+                if (P::kVals > 0) {
+                    cp_async_wait_all();
+#pragma unroll
+                    for (int f = 0; f < P::kVals; ++f) vv.v[f] = slot[32 * f];
+                }
+                __syncwarp();
+                if (nat) p.segment(sm, tile, s0, gw * 32 + lane, wcnt[lane], wacc[lane], vv);
+                __syncwarp();
+            }
+        } else {
+            long_tile(p, sm, L, tile, s0, k0, len);
+        }
+        if (P::kGroupEpilogue) {
+            __syncthreads();
+            p.group(sm, tile, s0, nseg);
+            __syncthreads();   // cone scratch is rewritten by the next tile
+        }
+    }
+    p.finish(sm);
+}
+#endif
 
 }  // namespace pass
 }  // namespace cf

@@ -128,29 +128,29 @@ inline int bits_for(uint64_t maxval) {
 
 // Warp-local jagged-diagonal layout of one tile (see cf_pass.cuh). Warp w
 // handles the block of segments [32w, 32w+32): ranks them by length
-// (descending, stable), writes perm[rank] = local segment (one byte per
-// segment position), the block's diagonal starts jo_w[k] (tile-relative) after
-// a per-warp {start, maxlen} header, and scatters the k-th nonzero of rank r to
-// k0 + jo_w[k] + r. A long tile (joff length 0) is copied as is.
-constexpr int kJoffHdr = 2 * (kTileSeg / 32);
-
+// (descending, stable), writes pl[rank] = local segment | length << 5 |
+// start_w << 14 (one u32 per segment position) and scatters the k-th nonzero of rank r to
+// k0 + start_w + sum_{j<k} width_j + r, where width_j = number of the block's
+// segments longer than j and start_w = nonzeros of the blocks before w. The
+// pass recomputes those offsets from the lengths with warp ballots. A long
+// tile (normal flag 0) is copied as is.
 __global__ void __launch_bounds__(kTileSeg) k_build_jds(const int32_t* ptr, const int32_t* isrc,
                                                         const double* vsrc, const int4* tb, int32_t* idst,
-                                                        double* vdst, uint8_t* perm, uint16_t* joff) {
+                                                        double* vdst, uint32_t* pl) {
     constexpr int kW = kTileSeg / 32;
     __shared__ int lens[kTileSeg];
     __shared__ int bsum[kW], bmax[kW];
-    __shared__ int boff[kW + 1], bstart[kW + 1];
+    __shared__ int boff[kW + 1];
     __shared__ int jo[kW][kTileDiag + 2];
     const int t = blockIdx.x;
     const int4 lo = tb[t], hi = tb[t + 1];
-    const int s0 = lo.x, nseg = hi.x - lo.x, k0 = lo.y, k1 = hi.y, j0 = lo.z, jn = lo.w;
-    if (jn == 0) {
+    const int s0 = lo.x, nseg = hi.x - lo.x, k0 = lo.y, k1 = hi.y, normal = lo.z;
+    if (!normal) {
         for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
             idst[k] = isrc[k];
             vdst[k] = vsrc[k];
         }
-        if (threadIdx.x == 0) perm[s0] = 0;
+        if (threadIdx.x == 0) pl[s0] = 0;
         return;
     }
     const int w = threadIdx.x >> 5, r = threadIdx.x & 31;
@@ -164,9 +164,6 @@ __global__ void __launch_bounds__(kTileSeg) k_build_jds(const int32_t* ptr, cons
         const int l2 = __shfl_sync(0xffffffffu, len, r2);
         rank += (l2 > len) || (l2 == len && r2 < r);
     }
-    if (valid) perm[s0 + q] = 0;  // (overwritten below; keeps the byte defined)
-    __syncwarp();
-    if (valid) perm[s0 + w * 32 + rank] = (uint8_t)r;
     int sum = valid ? len : 0, mx = valid ? len : 0;
     for (int off = 16; off > 0; off >>= 1) {
         sum += __shfl_xor_sync(0xffffffffu, sum, off);
@@ -179,16 +176,10 @@ __global__ void __launch_bounds__(kTileSeg) k_build_jds(const int32_t* ptr, cons
     __syncthreads();
     if (threadIdx.x == 0) {
         boff[0] = 0;
-        bstart[0] = kJoffHdr;
-        for (int b = 0; b < kW; ++b) {
-            const bool nonempty = b * 32 < nseg;
-            boff[b + 1] = boff[b] + (nonempty ? bsum[b] : 0);
-            bstart[b + 1] = bstart[b] + (nonempty ? bmax[b] + 1 : 0);
-            joff[j0 + 2 * b] = (uint16_t)(nonempty ? bstart[b] : 0);
-            joff[j0 + 2 * b + 1] = (uint16_t)(nonempty ? bmax[b] : 0);
-        }
+        for (int b = 0; b < kW; ++b) boff[b + 1] = boff[b] + (b * 32 < nseg ? bsum[b] : 0);
     }
     __syncthreads();
+    if (valid) pl[s0 + w * 32 + rank] = (uint32_t)r | ((uint32_t)len << 5) | ((uint32_t)boff[w] << 14);
     if (w * 32 < nseg) {
         const int mlen = bmax[w];
         // width of diagonal k = number of segments of the block longer than k
@@ -203,7 +194,6 @@ __global__ void __launch_bounds__(kTileSeg) k_build_jds(const int32_t* ptr, cons
             for (int k = 0; k < mlen; ++k) jo[w][k + 1] += jo[w][k];
         }
         __syncwarp();
-        for (int k = r; k <= mlen; k += 32) joff[j0 + bstart[w] + k] = (uint16_t)jo[w][k];
         if (valid) {
             const int src0 = ptr[s0 + q];
             for (int kk = 0; kk < len; ++kk) {
@@ -232,42 +222,30 @@ void tile_starts(const std::vector<int32_t>& ptr, int64_t s_begin, int64_t s_end
     }
 }
 
-// tile table {s0, k0, joff start, joff length (0 = long tile)} from tile starts (+ the end segment)
+// tile table {s0, k0, normal (1) / long (0), 0} from tile starts (+ the end segment)
 void tile_table(const std::vector<int32_t>& ptr, const std::vector<int64_t>& starts, int64_t s_end,
-                std::vector<int4>& tb, int64_t& joff_total) {
+                std::vector<int4>& tb) {
     tb.clear();
-    joff_total = 0;
     for (size_t t = 0; t < starts.size(); ++t) {
         const int64_t s0 = starts[t], s1 = (t + 1 < starts.size()) ? starts[t + 1] : s_end;
         const int64_t nnz = ptr[s1] - ptr[s0];
-        int64_t jn = 0;
-        if (!(s1 - s0 == 1 && nnz > kTileDiag)) {
-            jn = kJoffHdr;
-            for (int64_t b0 = s0; b0 < s1; b0 += 32) {
-                int64_t mx = 0;
-                for (int64_t q = b0; q < std::min(s1, b0 + 32); ++q) mx = std::max<int64_t>(mx, ptr[q + 1] - ptr[q]);
-                jn += mx + 1;
-            }
-        }
-        tb.push_back(make_int4((int)s0, ptr[s0], (int)joff_total, (int)jn));
-        joff_total += jn;
+        const int normal = !(s1 - s0 == 1 && nnz > kTileDiag);
+        tb.push_back(make_int4((int)s0, ptr[s0], normal, 0));
     }
-    tb.push_back(make_int4((int)s_end, ptr[s_end], (int)joff_total, 0));
+    tb.push_back(make_int4((int)s_end, ptr[s_end], 0, 0));
 }
 
 int build_jds(cf_plan* p, const int32_t* ptr, const int32_t* isrc, const double* vsrc, const std::vector<int4>& tb,
-              int64_t nseg_total, int64_t joff_total, DevBuf<int4>& dtb, DevBuf<int32_t>& idst,
-              DevBuf<double>& vdst, DevBuf<uint8_t>& perm, DevBuf<uint16_t>& joff) {
+              int64_t nseg_total, DevBuf<int4>& dtb, DevBuf<int32_t>& idst, DevBuf<double>& vdst,
+              DevBuf<uint32_t>& pl) {
     CF_TRY(dtb.alloc(tb.size()));
     CF_CUDA(cudaMemcpyAsync(dtb.p, tb.data(), tb.size() * sizeof(int4), cudaMemcpyHostToDevice, p->stream));
     CF_TRY(idst.alloc(p->o));
     CF_TRY(vdst.alloc(p->o));
-    CF_TRY(perm.alloc(nseg_total));
-    CF_TRY(joff.alloc(joff_total));
+    CF_TRY(pl.alloc(nseg_total));
     const int64_t ntiles = (int64_t)tb.size() - 1;
     if (ntiles > 0) {
-        k_build_jds<<<(unsigned)ntiles, kTileSeg, 0, p->stream>>>(ptr, isrc, vsrc, dtb.p, idst.p, vdst.p, perm.p,
-                                                                   joff.p);
+        k_build_jds<<<(unsigned)ntiles, kTileSeg, 0, p->stream>>>(ptr, isrc, vsrc, dtb.p, idst.p, vdst.p, pl.p);
         CF_LAUNCHED();
     }
     return CF_OK;
@@ -289,8 +267,7 @@ int build_tiles(cf_plan* p, const int64_t* sizes, int64_t nb) {
     }
     p->row_panel_tile[p->n_panels] = (int64_t)rstarts.size();
     std::vector<int4> rtb;
-    int64_t rjoff = 0;
-    tile_table(rp, rstarts, nsr, rtb, rjoff);
+    tile_table(rp, rstarts, nsr, rtb);
     p->row_tiles = (int64_t)rtb.size() - 1;
     // columns (cone-aligned when the cone is not the orthant)
     std::vector<int64_t> cstarts;
@@ -347,14 +324,11 @@ int build_tiles(cf_plan* p, const int64_t* sizes, int64_t nb) {
         tcone.push_back((int32_t)nb);
     }
     std::vector<int4> ctb;
-    int64_t cjoff = 0;
-    tile_table(cp, cstarts, n, ctb, cjoff);
+    tile_table(cp, cstarts, n, ctb);
     p->col_tiles = (int64_t)ctb.size() - 1;
     p->n_big = (int64_t)big.size();
-    CF_TRY(build_jds(p, p->rowptr.p, p->colidx.p, p->valr.p, rtb, nsr, rjoff, p->row_tb, p->rj_idx, p->rj_val,
-                     p->rj_perm, p->rj_joff));
-    CF_TRY(build_jds(p, p->colptr.p, p->rowidx.p, p->valc.p, ctb, n, cjoff, p->col_tb, p->cj_idx, p->cj_val,
-                     p->cj_perm, p->cj_joff));
+    CF_TRY(build_jds(p, p->rowptr.p, p->colidx.p, p->valr.p, rtb, nsr, p->row_tb, p->rj_idx, p->rj_val, p->rj_pl));
+    CF_TRY(build_jds(p, p->colptr.p, p->rowidx.p, p->valc.p, ctb, n, p->col_tb, p->cj_idx, p->cj_val, p->cj_pl));
     if (p->all_unit) {
         CF_TRY(p->tile_big.alloc(1));
         CF_TRY(p->tile_cone.alloc(1));
