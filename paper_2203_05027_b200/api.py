@@ -21,6 +21,7 @@ own ``ProblemInstance`` / ``SolverConfig`` / ``SolverState`` objects work too.
 from __future__ import annotations
 
 import math
+import threading
 from dataclasses import dataclass, replace
 from typing import NamedTuple
 
@@ -220,11 +221,25 @@ def run_plan(plan: DevicePlan, p, cfg, b_norms=None, c_norms=None) -> SolveResul
 def solve(p, cfg: SolverConfig | None = None, init: SolverState | None = None) -> SolveResult:
     """Run the ADMM loop on the GPU until a terminal status (solver.py:275-334)."""
     cfg = cfg or SolverConfig()
-    plan = build_plan(p)
+    # the host norms (numpy, GIL released) overlap the device setup (ctypes, GIL released)
+    box = {}
+
+    def _norms():
+        try:
+            box["b"], box["c"] = norms(p.b), norms(p.c)
+        except Exception:   # re-raised by run_plan computing them again
+            pass
+
+    th = threading.Thread(target=_norms, daemon=True)
+    th.start()
+    try:
+        plan = build_plan(p)
+    finally:
+        th.join()
     try:
         if init is not None:
             plan.set_state(cfg.mu, init, export=False)
-        return run_plan(plan, p, cfg)
+        return run_plan(plan, p, cfg, box.get("b"), box.get("c"))
     finally:
         plan.close()
 

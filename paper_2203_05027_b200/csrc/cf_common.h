@@ -50,6 +50,22 @@ int cuda_fail(cudaError_t e, const char* what, const char* file, int line);
 // cudaMalloc/cudaFree (and their implicit synchronisation) again. Allocation and release are
 // ordered on the legacy stream and synchronised, so a buffer is usable on any stream at return.
 cudaError_t pool_alloc(void** p, size_t bytes);
+// host -> device upload of pageable arrays through cached pinned staging buffers (cf_h2d.cu)
+struct H2DJob {
+    void* dst;
+    const void* src;
+    size_t bytes;
+};
+int h2d_staged(const std::vector<H2DJob>& jobs, cudaStream_t stream);
+// process-wide cached pinned host buffer, held (locked) for the lifetime of the object
+class PinnedScratch {
+  public:
+    PinnedScratch();
+    ~PinnedScratch();
+    void* get(size_t bytes);   // nullptr on failure; valid until the object dies
+    PinnedScratch(const PinnedScratch&) = delete;
+    PinnedScratch& operator=(const PinnedScratch&) = delete;
+};
 void pool_free(void* p);
 template <class T>
 struct DevBuf {

@@ -207,24 +207,66 @@ __global__ void __launch_bounds__(kTileSeg) k_build_jds(const int32_t* ptr, cons
 
 // Greedy tile starts over segments [s_begin, s_end) of a compressed layout:
 // a tile takes consecutive segments while it stays within kTileSeg segments
-// and kTileNnz nonzeros; a segment that alone exceeds the nonzero budget gets
-// a (long) tile of its own.
-void tile_starts(const std::vector<int32_t>& ptr, int64_t s_begin, int64_t s_end, std::vector<int64_t>& starts) {
+// and kTileNnz nonzeros and holds no segment longer than kTileDiag; such a long
+// segment gets a (long) tile of its own. `longs` lists the long segments in
+// increasing order; the nonzero budget is found by binary search on ptr.
+void tile_starts(const int32_t* ptr, int64_t s_begin, int64_t s_end, const std::vector<int64_t>& longs,
+                 std::vector<int64_t>& starts) {
+    size_t li = std::lower_bound(longs.begin(), longs.end(), s_begin) - longs.begin();
     int64_t s = s_begin;
     while (s < s_end) {
-        int64_t e = s + 1;
-        const bool long_seg = ptr[s + 1] - ptr[s] > kTileDiag;
-        while (!long_seg && e < s_end && e - s < kTileSeg && ptr[e + 1] - ptr[s] <= kTileNnz &&
-               ptr[e + 1] - ptr[e] <= kTileDiag)
-            ++e;
+        while (li < longs.size() && longs[li] < s) ++li;
         starts.push_back(s);
-        s = e;
+        if (li < longs.size() && longs[li] == s) {   // long segment: a tile of its own
+            ++s;
+            continue;
+        }
+        int64_t e = std::min<int64_t>(s_end, s + kTileSeg);
+        if (li < longs.size()) e = std::min<int64_t>(e, longs[li]);
+        // last e with ptr[e] - ptr[s] <= kTileNnz (at least s + 1: a short segment fits alone)
+        const int32_t* hi = std::upper_bound(ptr + s + 1, ptr + e + 1, ptr[s] + kTileNnz);
+        s = std::max<int64_t>(s + 1, (int64_t)(hi - ptr) - 1);
     }
 }
 
+__global__ void k_long_segments(const int32_t* ptr, int64_t nseg, int32_t* out, int32_t cap, int32_t* count) {
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg; s += (int64_t)gridDim.x * blockDim.x)
+        if (ptr[s + 1] - ptr[s] > kTileDiag) {
+            const int32_t k = atomicAdd(count, 1);
+            if (k < cap) out[k] = (int32_t)s;
+        }
+}
+
+// sorted indices of the segments longer than kTileDiag
+int long_segments(cf_plan* p, const int32_t* ptr_dev, int64_t nseg, std::vector<int64_t>& out) {
+    out.clear();
+    if (nseg == 0) return CF_OK;
+    DevBuf<int32_t> cnt;
+    CF_TRY(cnt.alloc(1));
+    int32_t cap = 1 << 16, h = 0;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        DevBuf<int32_t> list;
+        CF_TRY(list.alloc(cap));
+        CF_CUDA(cudaMemsetAsync(cnt.p, 0, 4, p->stream));
+        k_long_segments<<<grid1d(nseg), 256, 0, p->stream>>>(ptr_dev, nseg, list.p, cap, cnt.p);
+        CF_LAUNCHED();
+        CF_CUDA(cudaMemcpyAsync(&h, cnt.p, 4, cudaMemcpyDeviceToHost, p->stream));
+        CF_CUDA(cudaStreamSynchronize(p->stream));
+        if (h <= cap) {
+            std::vector<int32_t> v(h);
+            if (h) CF_CUDA(cudaMemcpy(v.data(), list.p, (size_t)h * 4, cudaMemcpyDeviceToHost));
+            out.assign(v.begin(), v.end());
+            std::sort(out.begin(), out.end());
+            return CF_OK;
+        }
+        cap = h;
+    }
+    set_error("long_segments: count changed between attempts");
+    return CF_ECUDA;
+}
+
 // tile table {s0, k0, normal (1) / long (0), 0} from tile starts (+ the end segment)
-void tile_table(const std::vector<int32_t>& ptr, const std::vector<int64_t>& starts, int64_t s_end,
-                std::vector<int4>& tb) {
+void tile_table(const int32_t* ptr, const std::vector<int64_t>& starts, int64_t s_end, std::vector<int4>& tb) {
     tb.clear();
     for (size_t t = 0; t < starts.size(); ++t) {
         const int64_t s0 = starts[t], s1 = (t + 1 < starts.size()) ? starts[t + 1] : s_end;
@@ -253,27 +295,48 @@ int build_jds(cf_plan* p, const int32_t* ptr, const int32_t* isrc, const double*
 
 int build_tiles(cf_plan* p, const int64_t* sizes, int64_t nb) {
     const int64_t m = p->m, n = p->n;
-    std::vector<int32_t> rp((int64_t)p->n_panels * m + 1), cp(n + 1);
-    CF_CUDA(cudaMemcpyAsync(rp.data(), p->rowptr.p, rp.size() * 4, cudaMemcpyDeviceToHost, p->stream));
-    CF_CUDA(cudaMemcpyAsync(cp.data(), p->colptr.p, (n + 1) * 4, cudaMemcpyDeviceToHost, p->stream));
-    CF_CUDA(cudaStreamSynchronize(p->stream));
-    // rows, panel by panel (segment = panel*m + row)
+    const bool verbose = getenv("CF_VERBOSE") != nullptr;
+    auto t_last = std::chrono::steady_clock::now();
+    auto tick = [&](const char* what) {
+        if (!verbose) return;
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "[cf tiles]   %-28s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(now - t_last).count());
+        t_last = now;
+    };
     const int64_t nsr = (int64_t)p->n_panels * m;
+    std::vector<int64_t> rlong, clong;
+    CF_TRY(long_segments(p, p->rowptr.p, nsr, rlong));
+    CF_TRY(long_segments(p, p->colptr.p, n, clong));
+    // both pointer arrays in (cached) pinned memory
+    PinnedScratch scratch;
+    int32_t* rp = static_cast<int32_t*>(scratch.get((size_t)(nsr + 1 + n + 1) * 4));
+    if (!rp) {
+        set_error("build_tiles: pinned host allocation failed");
+        return CF_ENOMEM;
+    }
+    int32_t* cp = rp + nsr + 1;
+    CF_CUDA(cudaMemcpyAsync(rp, p->rowptr.p, (size_t)(nsr + 1) * 4, cudaMemcpyDeviceToHost, p->stream));
+    CF_CUDA(cudaMemcpyAsync(cp, p->colptr.p, (size_t)(n + 1) * 4, cudaMemcpyDeviceToHost, p->stream));
+    CF_CUDA(cudaStreamSynchronize(p->stream));
+    tick("ptr D2H + long segments");
+    // rows, panel by panel (segment = panel*m + row)
     std::vector<int64_t> rstarts;
+    rstarts.reserve(nsr / kTileSeg + 16);
     p->row_panel_tile.assign(p->n_panels + 1, 0);
     for (int pn = 0; pn < p->n_panels; ++pn) {
         p->row_panel_tile[pn] = (int64_t)rstarts.size();
-        tile_starts(rp, (int64_t)pn * m, (int64_t)(pn + 1) * m, rstarts);
+        tile_starts(rp, (int64_t)pn * m, (int64_t)(pn + 1) * m, rlong, rstarts);
     }
     p->row_panel_tile[p->n_panels] = (int64_t)rstarts.size();
     std::vector<int4> rtb;
     tile_table(rp, rstarts, nsr, rtb);
     p->row_tiles = (int64_t)rtb.size() - 1;
+    tick("row tiles (host)");
     // columns (cone-aligned when the cone is not the orthant)
     std::vector<int64_t> cstarts;
     std::vector<int32_t> tcone, tbig, big, cone_ptr;
     if (p->all_unit) {
-        tile_starts(cp, 0, n, cstarts);
+        tile_starts(cp, 0, n, clong, cstarts);
     } else {
         cone_ptr.resize(nb + 1);
         int64_t col = 0;
@@ -287,7 +350,7 @@ int build_tiles(cf_plan* p, const int64_t* sizes, int64_t nb) {
             const int64_t c0 = cone_ptr[q];
             if (sizes[q] > kSmallCone) {
                 const size_t before = cstarts.size();
-                tile_starts(cp, c0, c0 + sizes[q], cstarts);
+                tile_starts(cp, c0, c0 + sizes[q], clong, cstarts);
                 for (size_t t = before; t < cstarts.size(); ++t) {
                     tcone.push_back((int32_t)q);
                     tbig.push_back((int32_t)big.size());
@@ -304,7 +367,7 @@ int build_tiles(cf_plan* p, const int64_t* sizes, int64_t nb) {
             };
             if (!cone_ok(q)) {  // cone with a very long column: treat like a big cone (k_big_cone)
                 const size_t before = cstarts.size();
-                tile_starts(cp, c0, c0 + sizes[q], cstarts);
+                tile_starts(cp, c0, c0 + sizes[q], clong, cstarts);
                 for (size_t t = before; t < cstarts.size(); ++t) {
                     tcone.push_back((int32_t)q);
                     tbig.push_back((int32_t)big.size());
@@ -325,10 +388,13 @@ int build_tiles(cf_plan* p, const int64_t* sizes, int64_t nb) {
     }
     std::vector<int4> ctb;
     tile_table(cp, cstarts, n, ctb);
+    tick("col tiles (host)");
     p->col_tiles = (int64_t)ctb.size() - 1;
     p->n_big = (int64_t)big.size();
     CF_TRY(build_jds(p, p->rowptr.p, p->colidx.p, p->valr.p, rtb, nsr, p->row_tb, p->rj_idx, p->rj_val, p->rj_pl));
     CF_TRY(build_jds(p, p->colptr.p, p->rowidx.p, p->valc.p, ctb, n, p->col_tb, p->cj_idx, p->cj_val, p->cj_pl));
+    if (verbose) CF_CUDA(cudaStreamSynchronize(p->stream));
+    tick("jds build (device)");
     if (p->all_unit) {
         CF_TRY(p->tile_big.alloc(1));
         CF_TRY(p->tile_cone.alloc(1));
@@ -382,19 +448,20 @@ int build(cf_plan* p, const int64_t* rows, const int64_t* cols, const double* va
         CF_TRY(drows.alloc(o));
         CF_TRY(dcols.alloc(o));
         CF_TRY(dvals.alloc(o));
-        if (o) {
-            CF_CUDA(cudaMemcpyAsync(drows.p, rows, o * 8, cudaMemcpyHostToDevice, st));
-            CF_CUDA(cudaMemcpyAsync(dcols.p, cols, o * 8, cudaMemcpyHostToDevice, st));
-            CF_CUDA(cudaMemcpyAsync(dvals.p, vals, o * 8, cudaMemcpyHostToDevice, st));
-        }
-        rows = drows.p;
-        cols = dcols.p;
-        vals = dvals.p;
     }
     CF_TRY(p->b.alloc(m));
     CF_TRY(p->c.alloc(n));
-    if (m) CF_CUDA(cudaMemcpyAsync(p->b.p, bsrc, m * 8, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
-    if (n) CF_CUDA(cudaMemcpyAsync(p->c.p, csrc, n * 8, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    if (!on_device) {
+        CF_TRY(h2d_staged({{drows.p, rows, (size_t)o * 8}, {dcols.p, cols, (size_t)o * 8}, {dvals.p, vals, (size_t)o * 8},
+                           {p->b.p, bsrc, (size_t)m * 8}, {p->c.p, csrc, (size_t)n * 8}},
+                          st));
+        rows = drows.p;
+        cols = dcols.p;
+        vals = dvals.p;
+    } else {
+        if (m) CF_CUDA(cudaMemcpyAsync(p->b.p, bsrc, m * 8, cudaMemcpyDeviceToDevice, st));
+        if (n) CF_CUDA(cudaMemcpyAsync(p->c.p, csrc, n * 8, cudaMemcpyDeviceToDevice, st));
+    }
 
     clk.mark("inputs H2D");
     // ---- validate (model.py:152-201)
