@@ -20,6 +20,8 @@ Also on the line:
   cpu_baseline the oracle port (numpy, literal reference iteration) on a bounded
                1/20-scale sample of the same workload (rank 0, N=1)
   clocks       nvidia-smi sampled during the timed region
+  gather_bound the dominant pass against the measured random-gather ceiling
+               (1.03 fp64 gathers per SM-cycle x 148 SMs x sampled clock)
 
 The C2 instance fits one GPU, so N>1 runs N independent replicas ("replicas
 only", DESIGN.md §6): value = N*K / max-over-ranks time, scaling "weak".
@@ -77,6 +79,24 @@ def hbm_peak():
         return v, "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# Random fp64 gathers from an L2-resident vector retire at ~1.03 per SM-cycle
+# (one L1TEX->L2 request each; profiles/r01_probes.md, scratch/gather_probe2.cu),
+# and a fully coalesced idx/val stream next to them costs ~7 % more
+# (scratch/stream_probe.cu: 100M gathers + stream in 0.394 ms). Every pass does
+# one gather per nonzero, so this — not HBM — is the ceiling of a pass.
+GATHERS_PER_SM_CYCLE = 1.03
+N_SMS = 148
+
+
+def gather_bound(o, pass_ms, clocks):
+    """The dominant pass against the gather-request ceiling at the sampled SM clock."""
+    mhz = (clocks or {}).get("sm_mhz") or 1965.0
+    peak = GATHERS_PER_SM_CYCLE * N_SMS * mhz * 1e6 / 1e9
+    achieved = o / (pass_ms / 1000.0) / 1e9
+    return {"achieved": achieved, "peak": peak, "unit": "Ggathers/s", "frac": achieved / peak,
+            "sm_mhz": mhz, "source": "probe: 1.03 random fp64 gathers per SM-cycle (profiles/r01_probes.md)"}
 
 
 class ClockSampler:
@@ -344,6 +364,7 @@ def run_ours(args, spec, rank, world, local_rank):
                        f"({(row_b + col_b) / 1e9:.2f} GB streamed per iteration vs 126 MB L2)"},
             "gpu_launches": tim["launches"], "roofline": roofline, "iteration_roofline": iteration_roofline,
             "time_to_tol": ttt, "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
+            "gather_bound": gather_bound(o, dms, clocks),
         }
         print(json.dumps(line), flush=True)
     return 0
