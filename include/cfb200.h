@@ -37,6 +37,8 @@ extern "C" {
 #define CF_ENOMEM 3          /* device allocation failed */
 #define CF_EPROBLEM 4        /* validate() found violations: see cf_problem_checks */
 #define CF_ESTATE 5          /* call not valid in the plan's current state */
+#define CF_IO_PARSE 6        /* CONEPROB parse error: line + message as fileio.ParseError */
+#define CF_IO_FALLBACK 7     /* input outside the native parser's subset: use the Python parser */
 
 /* report status, mirrors the strings of solver.py:241,272,323 */
 #define CF_STATUS_RUNNING 0
@@ -232,6 +234,32 @@ int cf_plan_last_timing(const cf_plan* plan, double* loop_ms, int64_t* launches,
 int cf_plan_set_profiling(cf_plan* plan, int enable);
 /* Synchronise the plan's stream. */
 int cf_plan_sync(cf_plan* plan);
+
+/* ---------------------------------------------------------------- CONEPROB text I/O (host)
+ * Replaces parse_problem / write_problem (conefree/fileio.py:56-190) with a
+ * multi-threaded native reader/writer. Errors reproduce
+ * fileio.ParseError: CF_IO_PARSE with *err_line (0 = "file ended ...") and
+ * the reference's message text; CF_IO_FALLBACK when the input is outside the
+ * native subset (non-ASCII bytes, integers beyond int64) so the caller runs the
+ * Python restatement (paper_2203_05027_b200/binio.py). */
+typedef struct cf_text cf_text;
+/* open a file (path) or an in-memory UTF-8 text (path == NULL) */
+int cf_coneprob_open(const char* path, const char* text, int64_t len, cf_text** out);
+void cf_coneprob_close(cf_text* t);
+/* header, dimensions and CONES line (fileio.py:98-138): dims = {m, n, nnz, n_blocks} */
+int cf_coneprob_header(cf_text* t, int64_t dims[4], int64_t* err_line, char* msg, int64_t cap);
+/* the block sizes read by cf_coneprob_header (n_blocks int64) */
+int cf_coneprob_sizes(const cf_text* t, int64_t* sizes);
+/* entries, b, c and trailing content (fileio.py:140-190) into caller arrays;
+ * threads <= 0: all host cores */
+int cf_coneprob_body(cf_text* t, int64_t* rows, int64_t* cols, double* vals, double* b, double* c, int threads,
+                     int64_t* err_line, char* msg, int64_t cap);
+/* Python repr() of a float (fileio.py:52-53) into out (>= 32 bytes); returns the length */
+int cf_format_double(double x, char* out);
+/* write_problem (fileio.py:56-72) to a file; entries must already be in canonical order */
+int cf_coneprob_write(const char* path, int64_t m, int64_t n, int64_t nnz, const int64_t* rows, const int64_t* cols,
+                      const double* vals, const double* b, const double* c, int64_t n_blocks, const int64_t* sizes,
+                      int threads);
 
 #ifdef __cplusplus
 }

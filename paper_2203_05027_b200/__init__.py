@@ -16,6 +16,15 @@ from .api import (
     solve,
     solve_batch,
 )
+from .binio import (
+    ParseError,
+    parse_problem,
+    read_problem,
+    read_problem_binary,
+    write_problem,
+    write_problem_binary,
+    write_problem_file,
+)
 from .engine import DevicePlan
 from .instances import GeneratedInstance, GenSpec, generate, generate_witnessed, shape_for_nnz
 from .problem import ConeSpec, ProblemInstance, TripletMatrix, ValidationReport, validate
@@ -28,6 +37,7 @@ __all__ = [
     "GenSpec",
     "GeneratedInstance",
     "IterationReport",
+    "ParseError",
     "ProblemInstance",
     "SolveResult",
     "SolverConfig",
@@ -35,6 +45,12 @@ __all__ = [
     "TripletMatrix",
     "ValidationReport",
     "check_termination",
+    "parse_problem",
+    "read_problem",
+    "read_problem_binary",
+    "write_problem",
+    "write_problem_binary",
+    "write_problem_file",
     "generate",
     "generate_witnessed",
     "shape_for_nnz",

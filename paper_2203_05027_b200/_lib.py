@@ -113,6 +113,13 @@ SIGNATURES = {
                                c_int64, POINTER(CfChecks), _D]),
     "cf_plan_set_profiling": (c_int, [_P, c_int]),
     "cf_plan_sync": (c_int, [_P]),
+    "cf_coneprob_open": (c_int, [c_char_p, c_char_p, c_int64, POINTER(c_void_p)]),
+    "cf_coneprob_close": (None, [_P]),
+    "cf_coneprob_header": (c_int, [_P, _I64, _I64, c_char_p, c_int64]),
+    "cf_coneprob_sizes": (c_int, [_P, _P]),
+    "cf_coneprob_body": (c_int, [_P, _P, _P, _P, _P, _P, c_int, _I64, c_char_p, c_int64]),
+    "cf_format_double": (c_int, [c_double, c_char_p]),
+    "cf_coneprob_write": (c_int, [c_char_p, c_int64, c_int64, c_int64, _P, _P, _P, _P, _P, c_int64, _P, c_int]),
 }
 
 _lib = None

@@ -26,6 +26,7 @@ if REF_SRC not in sys.path:
     sys.path.insert(0, REF_SRC)
 
 import conefree as cf  # noqa: E402  (the reference package)
+import conefree.bench  # noqa: E402,F401
 from conefree import solver as ref_solver  # noqa: E402
 
 OUT = os.path.dirname(os.path.abspath(__file__))
@@ -285,6 +286,109 @@ def generator():
     print("C1:", r.report.iter, r.report.status, r.report.pobj)
 
 
+BENCH_JOBS = (
+    # (instance_id, m, n, density, cone_kind, seed): C4-shaped jobs (batched on the GPU),
+    # an SOCP one, and one above benchrun.BATCH_MAX_NNZ (solved alone)
+    (0, 100, 200, 0.05, "lp", 0), (1, 100, 200, 0.05, "lp", 1), (2, 100, 200, 0.05, "lp", 2),
+    (3, 100, 200, 0.05, "lp", 3), (4, 100, 200, 0.05, "socp4", 7), (5, 200, 800, 0.15, "lp", 3),
+)
+
+
+def bench_rows():
+    """The reference's own run_bench (bench.py:96-106) over BENCH_JOBS: deterministic columns."""
+    cfg = cf.SolverConfig(term_mode="scs", eps_prim=1e-4, eps_dual=1e-4, eps_gap=1e-4)
+    jobs = [cf.bench.BenchJob(i, cf.GenSpec(m, n, dens, kind, seed), cfg) for i, m, n, dens, kind, seed in BENCH_JOBS]
+    rows = cf.bench.run_bench(jobs, workers=1)
+    num = ("instance_id", "m", "n", "nnz", "density", "mu", "iters", "prim_res_2", "dual_res_2", "gap", "cone_gap")
+    out = {k: np.array([r[k] for r in rows]) for k in num}
+    out["cone_kind"] = np.array([r["cone_kind"] for r in rows])
+    out["term_mode"] = np.array([r["term_mode"] for r in rows])
+    out["status"] = np.array([r["status"] for r in rows])
+    out["jobs"] = np.array([[i, m, n, seed] for i, m, n, dens, kind, seed in BENCH_JOBS], dtype=np.int64)
+    out["densities"] = np.array([dens for _, _, _, dens, _, _ in BENCH_JOBS])
+    out["kinds"] = np.array([kind for _, _, _, _, kind, _ in BENCH_JOBS])
+    np.savez_compressed(os.path.join(OUT, "bench_rows.npz"), **out)
+    print("bench_rows:", [(r["instance_id"], r["iters"], r["status"]) for r in rows])
+
+
+def _coneprob_cases():
+    """Valid and malformed CONEPROB texts (mutations of one small instance)."""
+    from conefree import fileio
+
+    p = cf.generate(cf.GenSpec(4, 8, 0.5, "socp4", seed=5))
+    base = fileio.write_problem(p)
+    L = base.splitlines()
+    nnz = p.A.nnz
+    e0, e_last = 3, 3 + nnz - 1            # 0-based line indices of the first/last entry
+    b0, c0 = 3 + nnz, 3 + nnz + 4
+    cases = [base, base.replace("\n", "\r\n"), base.replace("\n", "\r"), "# comment\n\n" + base,
+             base.replace("\n", "\n  # note\n", 5), base.replace("\n", "\x0b", 3), base.replace("\n", "\x0c", 4),
+             base.replace("\n", "\x1c", 2), base.replace(" ", "\t"), base.replace(" ", " \x1f "), "", "\n\n",
+             "CONEPROB 2\n", "coneprob 1\n", "CONEPROB  1\n", "CONEPROB 1", "CONEPROB 1\n4 8\n",
+             "CONEPROB 1\n4 8 x\n", "CONEPROB 1\n4 1.5 3\n", "CONEPROB 1\n0 8 3\n", "CONEPROB 1\n4 8 -1\n",
+             "CONEPROB 1\n4 8 1_0\nCONE 1 8\n", "CONEPROB 1\n+4 8 0\nCONES\n", "CONEPROB 1\n4 8 0\nCONES x\n",
+             "CONEPROB 1\n4 8 0\nCONES 2 4\n", "CONEPROB 1\n4 8 0\nCONES 2 4 y\n", "CONEPROB 1\n4 8 0\nCONES 2 8 0\n",
+             "CONEPROB 1\n4 8 0\nCONES 2 4 3\n", "CONEPROB 1\n4 8 0\nCONES 2 4 4\n",
+             "CONEPROB 1\n1 1 1\nCONES 1 1\n0 0 1_0.5\n1e1_0\n-2\n",
+             "CONEPROB 1\n1 1 0\nCONES 1 1\n1\n2\n3\n", "CONEPROB 1\n1 1 0\nCONES 1 1\n1 2\n2\n",
+             "CONEPROB 1\n1 1 0\nCONES 1 1\ninf\n2\n", "CONEPROB 1\n1 1 0\nCONES 1 1\n1\n-NaN\n",
+             "CONEPROB 1\n4 8 0\nCONES 2 4 4\n" + "1\n" * 4 + "1\n" * 7,
+             "CONEPROB 1\n1 1 1\nCONES 1 1\n0 0 it's\n", 'CONEPROB 1\n1 1 1\nCONES 1 1\n0 0 "q\n',
+             "CONEPROB 1\n1 1 1\nCONES 1 1\n0 0 a\\b'\"\n", "CONEPROB 1\n1 1 1\nCONES 1 1\n0 0 1e-400\n",
+             "CONEPROB 1\n1 1 1\nCONES 1 1\n0 0 -0.0\n", "CONEPROB 1\n1 1 1\nCONES 1 1\n0 0 1e999\n",
+             "CONEPROB 1\n1 1 1\nCONES 1 1\n0 0 0x10\n", "CONEPROB 1\n1 1 1\nCONES 1 1\n0 0 1__0\n",
+             "CONEPROB 1\n1 1 1\nCONES 1 1\n0 0 .5\n1.\n-.5e+3\n", "CONEPROB 1\n1 1 1\nCONES 1 1\n0 0 1e\n",
+             "CONEPROB 1\n1 1 1\nCONES 1 1\n0 0 +Infinity\n", "CONEPROB 1\n1 1 1\nCONES 1 1\n00 0_0 7\n1\n1\n",
+             "CONEPROB 1\n99999999999999999999 1 0\nCONES 1 1\n", "CONEPROB 1\n1 1 1\nCONES 1 1\n0 0 7 # x\n",
+             "# caf\u00e9\n" + base, base.replace("\n", "\u2028", 1), "CONEPROB 1\n2 1 2\nCONES 1 1\n0 0 1\n0 0 2\n1\n1\n1\n"]
+    muts = {
+        e0 + 1: "1 2", e0 + 2: "x 0 1.0", e0 + 3: "0 y 1.0", e_last: "0 0 z", e0: "9 0 1.0", e0 + 4: "0 -1 1.0",
+        e_last - 1: "0 0 nan", b0: "b?", c0 + 2: "inf", c0 + 7: "1 2",
+    }
+    for li, text in muts.items():
+        lines = list(L)
+        lines[li] = text
+        cases.append("\n".join(lines) + "\n")
+    # duplicates: an entry repeated later; and a zero-valued duplicate (zero wins on that line)
+    for a, bq, txt in ((e0, e0 + 5, None), (e0 + 2, e_last, "zero")):
+        lines = list(L)
+        i, j, _ = lines[a].split()
+        lines[bq] = f"{i} {j} {'0.0' if txt else '2.5'}"
+        cases.append("\n".join(lines) + "\n")
+    lines = list(L)
+    lines[e0 + 6] = lines[e0 + 1]
+    lines[e0 + 3] = "3 x 1"
+    cases.append("\n".join(lines) + "\n")
+    cases += ["\n".join(L[:e0 + 3]) + "\n", "\n".join(L[:b0 + 2]) + "\n", "\n".join(L[:-1]) + "\n",
+              base + "extra\n", base + "# trailing comment\n\n"]
+    return cases
+
+
+def coneprob_cases():
+    """parse_problem on valid and malformed texts: ParseError line/message or a hash of the arrays."""
+    from conefree import fileio
+
+    texts, lines, msgs, hashes = [], [], [], []
+    for t in _coneprob_cases():
+        try:
+            p = fileio.parse_problem(t)
+            lines.append(-1)
+            msgs.append("")
+            hashes.append(sha(p.A.rows, p.A.cols, p.A.vals, p.b, p.c, np.asarray(p.cones.block_sizes)))
+        except fileio.ParseError as e:
+            lines.append(e.line)
+            msgs.append(e.message)
+            hashes.append("")
+        except Exception as e:   # e.g. numpy refusing a huge m: the same exception is expected
+            lines.append(-2)
+            msgs.append(f"{type(e).__name__}: {e}")
+            hashes.append("")
+        texts.append(t)
+    np.savez_compressed(os.path.join(OUT, "coneprob_cases.npz"), texts=np.array(texts), lines=np.array(lines),
+                        messages=np.array(msgs), hashes=np.array(hashes))
+    print("coneprob_cases:", len(texts), "cases,", sum(1 for x in lines if x >= 0), "errors")
+
+
 if __name__ == "__main__":
     np.seterr(all="ignore")
     example1()
@@ -293,6 +397,8 @@ if __name__ == "__main__":
     mixed_cones()
     solves()
     generator()
+    bench_rows()
+    coneprob_cases()
     for fn in sorted(os.listdir(OUT)):
         if fn.endswith(".npz"):
             print(fn, os.path.getsize(os.path.join(OUT, fn)))

@@ -110,3 +110,23 @@ def test_no_gpu_fails_loudly():
 
 def test_decide_max_iters_passthrough():
     assert _decide(_rep(status="max_iters"), SolverConfig(), (0.0, 0.0), (0.0, 0.0)) == "max_iters"
+
+
+def test_benchrun_csv_and_shapes():
+    """benchrun mirrors bench.py's CSV layout and shape_for_nnz (bench.py:48-55, 109-119)."""
+    import math
+
+    from paper_2203_05027_b200.benchrun import BENCH_COLUMNS, bench_csv, shape_for_nnz
+
+    assert BENCH_COLUMNS[0] == "instance_id" and BENCH_COLUMNS[-1] == "status" and len(BENCH_COLUMNS) == 15
+    for nnz, dens, kind in ((20_000, 0.01, "lp"), (1_000, 0.05, "lp"), (40_000_000, 5e-6, "socp4")):
+        cells = nnz / dens
+        m = max(1, round(math.sqrt(cells / 4.0)))
+        n = max(1, round(cells / m))
+        if kind == "socp4":
+            n = max(4, 4 * round(n / 4))
+        assert shape_for_nnz(nnz, dens, kind) == (m, n)
+    row = {c: 0 for c in BENCH_COLUMNS}
+    row.update({"density": 0.1, "time_ms": 1.5, "status": "solved", "cone_kind": "lp", "term_mode": "scs"})
+    text = bench_csv([row])
+    assert text.splitlines()[1].split(",")[4] == "0.1" and text.endswith("\n")
