@@ -255,7 +255,11 @@ def run_ours(args, spec, rank, world, local_rank):
     cs = config_struct(timed_cfg, bn, cn)
     sampler = ClockSampler(local_rank).start() if rank == 0 else None
     time.sleep(0.4 if sampler else 0.0)
-    plan.set_profiling(True)
+    # per-pass CUDA events inside the timed region cost ~10 us per iteration of
+    # launch overlap: negligible at C2 (1.2 ms/iteration), not for small problems,
+    # whose pass split comes from a separate profiled run of the same length
+    profile_in_timed = o >= 1_000_000
+    plan.set_profiling(profile_in_timed)
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     w0 = time.time()
@@ -270,6 +274,13 @@ def run_ours(args, spec, rank, world, local_rank):
     ms = e0.elapsed_time(e1)
     tim = plan.last_timing()
     assert tim["iters"] == args.steps and trace[-1]["status"] == "max_iters", (tim, trace[-1])
+    pass_tim = tim
+    if not profile_in_timed:
+        plan.set_state(1.0, None, export=False)
+        plan.set_profiling(True)
+        plan.run(cs, want_x=False)
+        plan.set_profiling(False)
+        pass_tim = plan.last_timing()
     ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if dist:
         tdist.all_reduce(ms_t, op=tdist.ReduceOp.MAX)
@@ -279,8 +290,8 @@ def run_ours(args, spec, rank, world, local_rank):
     # ---------------- roofline of the dominant pass (per-pass events inside the timed region)
     row_b, col_b = algorithmic_bytes(m, n, o)
     peak, peak_src = hbm_peak()
-    row_ms = tim["row_pass_ms"] / args.steps
-    col_ms = tim["col_pass_ms"] / args.steps
+    row_ms = pass_tim["row_pass_ms"] / args.steps
+    col_ms = pass_tim["col_pass_ms"] / args.steps
     passes = {"row_pass": (row_b, row_ms), "col_pass": (col_b, col_ms)}
     dom = max(passes, key=lambda k: passes[k][1])
     dbytes, dms = passes[dom]
@@ -299,7 +310,8 @@ def run_ours(args, spec, rank, world, local_rank):
                 "peak_source": peak_src}
     iteration_roofline = {"achieved": it_achieved, "frac": it_achieved / peak, "bytes_per_iteration": row_b + col_b,
                           "ms_per_iteration": per_iter_ms, "row_pass_ms": row_ms, "col_pass_ms": col_ms,
-                          "report_and_launch_ms": per_iter_ms - row_ms - col_ms}
+                          "report_and_launch_ms": (per_iter_ms - row_ms - col_ms) if profile_in_timed else None,
+                          "pass_times": "timed region" if profile_in_timed else "separate profiled run"}
 
     # ---------------- time to tolerance (device-resident, cold start)
     ttt = None

@@ -21,6 +21,8 @@
 #include <cmath>
 
 #include "cf_common.h"
+#include <utility>
+
 #include "cf_pass.cuh"
 #include "cf_report.cuh"
 
@@ -310,6 +312,8 @@ struct BigConeArgs {
     const int32_t* done;
 };
 __global__ void __launch_bounds__(1024) k_big_cone(const BigConeArgs a) {
+    pass::pdl_wait();
+    pass::pdl_trigger();
     if (a.done && *a.done) return;
     __shared__ double sh[32];
     __shared__ double s_alpha;
@@ -352,6 +356,8 @@ struct RowReportArgs {
     const int32_t* done;
 };
 __global__ void __launch_bounds__(kThreads) k_row_report(const RowReportArgs a) {
+    pass::pdl_wait();
+    pass::pdl_trigger();
     if (a.done && *a.done) return;
     __shared__ double sh[32];
     double s2 = 0.0, mx = 0.0, axm = 0.0, bl = 0.0, nf = 0.0;
@@ -403,6 +409,8 @@ __device__ double reduce_partials(const double* p, int G, double* sh, Op op) {
 // Final stage of compute_report (solver.py:219-242) + check_termination
 // (solver.py:245-272) + the max_iters rule (:322-323).
 __global__ void __launch_bounds__(1024) k_finalize(const FinalizeArgs a) {
+    pass::pdl_wait();
+    pass::pdl_trigger();
     if (a.done && *a.done) return;
     __shared__ double sh[32];
     double f[kReportFieldsRow + kReportFieldsCol];
@@ -535,6 +543,25 @@ pass::Tiles col_tiles(const cf_plan* p) { return pass::Tiles{p->col_tb.p, (int32
 pass::Jds row_jds(const cf_plan* p) { return pass::Jds{p->rj_idx.p, p->rj_val.p, p->rj_pl.p}; }
 pass::Jds col_jds(const cf_plan* p) { return pass::Jds{p->cj_idx.p, p->cj_val.p, p->cj_pl.p}; }
 
+// Launch with programmatic stream serialization (the kernel calls pdl_wait()
+// before touching its predecessor's results): the launch overlaps the
+// predecessor's tail instead of waiting for it to drain.
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 template <class P>
 int persistent_grid(int n_tiles) {
     static int per_sm = -1;
@@ -559,8 +586,8 @@ int launch_pass(const P& pol, const pass::Jds& L, const pass::Tiles& T, const in
     if (T.n_tiles == 0) return CF_OK;
     const int grid = persistent_grid<P>(T.n_tiles);
     if (grid_out) *grid_out = grid;
-    pass::k_pass<P><<<grid, pass::kPThreads, pass::smem_bytes<P>(), st>>>(pol, L, T, done);
-    CF_LAUNCHED();
+    CF_CUDA(launch_pdl(pass::k_pass<P>, (unsigned)grid, (unsigned)pass::kPThreads, pass::smem_bytes<P>(), st, pol, L,
+                       T, done));
     return CF_OK;
 }
 
@@ -648,8 +675,7 @@ int launch_iteration(cf_plan* p, const IterOpts& opt, const int32_t* done, int64
             g.delta = p->delta.p;
             g.mu = opt.mu;
             g.done = done;
-            k_big_cone<<<(unsigned)p->n_big, 1024, 0, p->stream>>>(g);
-            CF_LAUNCHED();
+            CF_CUDA(launch_pdl(k_big_cone, (unsigned)p->n_big, 1024u, 0, p->stream, g));
             ++nl;
         }
     }
@@ -715,9 +741,8 @@ int launch_report(cf_plan* p, double mu, bool ax_ready, const cf_config* cfg, in
         a.part = p->part_row.p;
         a.m = (int32_t)p->m;
         a.done = done;
-        k_row_report<<<p->row_report_ctas, kThreads, 0, p->stream>>>(a);
+        CF_CUDA(launch_pdl(k_row_report, (unsigned)p->row_report_ctas, (unsigned)kThreads, 0, p->stream, a));
         ++nl;
-        CF_LAUNCHED();
     }
     int g_col = 0;
     if (p->n > 0) {
@@ -744,9 +769,8 @@ int launch_report(cf_plan* p, double mu, bool ax_ready, const cf_config* cfg, in
     if (cfg) f.cfg = *cfg;
     f.slot = p->report_slot.p + slot;
     f.done = const_cast<int32_t*>(done);
-    k_finalize<<<1, 1024, 0, p->stream>>>(f);
+    CF_CUDA(launch_pdl(k_finalize, 1u, 1024u, 0, p->stream, f));
     ++nl;
-    CF_LAUNCHED();
     if (launches) *launches += nl;
     return CF_OK;
 }

@@ -149,6 +149,14 @@ __device__ __forceinline__ uint64_t pol_last() {
     asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+// Programmatic dependent launch (sm_90+): a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start while its
+// predecessor drains; pdl_wait() blocks until the predecessor has completed and
+// its writes are visible (a no-op without the attribute). pdl_trigger() lets
+// the successor launch once every CTA of this grid has triggered or exited.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // compute group of the calling thread and its thread index inside the group
 #if CF_TMA
 __device__ __forceinline__ int group_id() { return (int)threadIdx.x / kComputeThreads; }
@@ -395,7 +403,6 @@ __device__ __forceinline__ void issue_tile(const Jds& L, int4 lo, int4 hi, Stage
 // Groups alternate tiles. Inside a tile, warp w takes warp block w.
 template <class P>
 __global__ void __launch_bounds__(kPThreads, 1) k_pass(const P p0, const Jds L, const Tiles T, const int32_t* done) {
-    if (done && *done) return;
     P p = p0;  // per-thread mutable copy (report accumulators live in registers)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
@@ -411,6 +418,9 @@ __global__ void __launch_bounds__(kPThreads, 1) k_pass(const P p0, const Jds L, 
         fence_mbar_init();
     }
     __syncthreads();
+    pdl_wait();
+    pdl_trigger();
+    if (done && *done) return;
 
     if (warp >= kGroups * kComputeWarps) {
         // ------------------------------------------------ producers: warp kGroups*kComputeWarps + g feeds group g
@@ -538,7 +548,6 @@ __global__ void __launch_bounds__(kPThreads, 1) k_pass(const P p0, const Jds L, 
 template <class P>
 __global__ void __launch_bounds__(kPThreads, P::kMinBlocks) k_pass(const P p0, const Jds L, const Tiles T,
                                                                const int32_t* done) {
-    if (done && *done) return;
     P p = p0;  // per-thread mutable copy (report accumulators live in registers)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
@@ -548,6 +557,9 @@ __global__ void __launch_bounds__(kPThreads, P::kMinBlocks) k_pass(const P p0, c
     const int gw = gt >> 5;      // warp = warp block of the tile
     for (int c = gt; c < kFvTab; c += kPThreads) sm.fvtab[c] = 1.0 / (1.0 + (double)c);
     __syncthreads();
+    pdl_wait();   // everything above is independent of the previous kernel
+    pdl_trigger();
+    if (done && *done) return;
     const uint64_t pl_ = pol_last(), pf = pol_first();
     const double* __restrict__ g = p.gvec();
     const int32_t* plw = reinterpret_cast<const int32_t*>(L.pl);
@@ -664,7 +676,6 @@ __global__ void __launch_bounds__(kPThreads, P::kMinBlocks) k_pass(const P p0, c
 template <class P>
 __global__ void __launch_bounds__(kPThreads, P::kMinBlocks) k_pass(const P p0, const Jds L, const Tiles T,
                                                                const int32_t* done) {
-    if (done && *done) return;
     P p = p0;  // per-thread mutable copy (report accumulators live in registers)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
@@ -674,6 +685,9 @@ __global__ void __launch_bounds__(kPThreads, P::kMinBlocks) k_pass(const P p0, c
     const int gw = gt >> 5;      // warp = warp block of the tile
     for (int c = gt; c < kFvTab; c += kPThreads) sm.fvtab[c] = 1.0 / (1.0 + (double)c);
     __syncthreads();
+    pdl_wait();   // everything above is independent of the previous kernel
+    pdl_trigger();
+    if (done && *done) return;
     constexpr int U = P::kUnroll;
     for (int tile = blockIdx.x; tile < T.n_tiles; tile += G) {
         const int4 lo = __ldg(T.tb + tile), hi = __ldg(T.tb + tile + 1);
@@ -696,19 +710,21 @@ __global__ void __launch_bounds__(kPThreads, P::kMinBlocks) k_pass(const P p0, c
                 int pos = k0 + __shfl_sync(0xffffffffu, pl_start(pr), 0) + lane;
                 // rank r's own carry (no shuffle: the load's latency hides behind the gathers)
                 double acc = (p.carry_in() && nat) ? p.carry(s0 + gw * 32 + q) : 0.0;
+                const double* __restrict__ g = p.gvec();
                 for (int k = 0; k < mlen; k += U) {
                     int nj[U];
                     double nv[U], gv[U];
                     load_batch<U>(L, nj, nv, pos, mylen, k, pol_first());
 #pragma unroll
                     for (int u = 0; u < U; ++u)
-                        gv[u] = (mylen > k + u) ? ld_gather(p.gvec() + nj[u], pol_last()) : 0.0;
+                        gv[u] = (mylen > k + u) ? ld_gather(g + (uint32_t)nj[u], pol_last()) : 0.0;
 #pragma unroll
-                    for (int u = 0; u < U; ++u)
-                        if (mylen > k + u) {
-                            p.check(nv[u], nj[u], gv[u]);
-                            acc = __dadd_rn(acc, __dmul_rn(nv[u], gv[u]));
-                        }
+                    for (int u = 0; u < U; ++u) {
+                        if (mylen > k + u) p.check(nv[u], nj[u], gv[u]);
+                        // no predicate: a lane past its segment adds 0.0*0.0 = +0.0, which leaves acc
+                        // unchanged (a sum that starts at +0.0 is never -0.0 in round-to-nearest)
+                        acc = __dadd_rn(acc, __dmul_rn(nv[u], gv[u]));
+                    }
                 }
                 // rank -> natural order inside the warp (a segment's count is its length)
                 double* wacc = sm.wacc[0] + gw * 32;
