@@ -419,8 +419,9 @@ def run_sharded_bench(args, spec, rank, world, local_rank):
     dist.barrier()
     torch.cuda.synchronize()
     tim = {}
-    run_sharded(be, row_cuts, col_cuts, cfg, bn, cn, timing=tim, gather_result=False)
+    res = run_sharded(be, row_cuts, col_cuts, cfg, bn, cn, timing=tim, gather_result=False)
     torch.cuda.synchronize()
+    assert tim["iters"] == args.steps and res.report.status == "max_iters", (tim, res.report)
     ms = torch.tensor([tim["loop_ms"]], dtype=torch.float64, device="cuda")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms)

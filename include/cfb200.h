@@ -111,7 +111,8 @@ int cf_device_count(int* count);
  *   b (m), c (n): f64.  block_sizes (n_blocks, host): the ConeSpec.
  *   inputs_on_device: 0 = rows/cols/vals/b/c are host pointers (copied with
  *   cudaMemcpyAsync), 1 = device pointers (read, never written or retained).
- *   stream: cudaStream_t the plan issues all work on (NULL = the plan creates one).
+ *   stream: cudaStream_t the plan issues all work on (NULL = the plan creates one;
+ *           (void*)1 = cudaStreamLegacy, the legacy default stream, e.g. torch's default).
  * On CF_EPROBLEM, *checks tells which checks failed and *out is NULL; the
  * caller produces the reference's messages (solver.py:300-302). */
 int cf_plan_create(int64_t m, int64_t n, int64_t o,

@@ -48,6 +48,9 @@ def report_to_dict(r: CfReport) -> dict:
     return d
 
 
+CUDA_STREAM_LEGACY = 1   # cudaStreamLegacy: the legacy default stream (torch's default stream)
+
+
 class DevicePlan:
     """Owner of a cf_plan handle (device copy of A in CSR + CSC, cones, iterates)."""
 
@@ -77,10 +80,14 @@ class DevicePlan:
 
     @classmethod
     def _create(cls, m, n, o, rows, cols, vals, b, c, sizes, on_device, stream):
+        """stream: None = the plan creates its own stream; an int = that cudaStream_t. torch's
+        default stream has handle 0, which the C ABI reads as "create one", so 0 is passed as
+        cudaStreamLegacy (1): the plan's kernels are then ordered with torch's work on it."""
         h = c_void_p()
         chk = CfChecks()
+        handle = None if stream is None else (CUDA_STREAM_LEGACY if int(stream) == 0 else int(stream))
         rc = lib().cf_plan_create(m, n, o, rows, cols, vals, b, c, int(sizes.size), _ptr(sizes), on_device,
-                                  c_void_p(stream or 0), byref(chk), byref(h))
+                                  c_void_p(handle), byref(chk), byref(h))
         if rc == _lib.CF_EPROBLEM:
             raise ProblemRejected(chk, _lib.last_error())
         check(rc, "cf_plan_create")

@@ -50,3 +50,28 @@ def test_sharded_cuda_backend_matches_oracle(nccl_group, kind, mu):
     ref = solve(p, cfg)
     assert res.report.iter == ref.report.iter
     np.testing.assert_allclose(res.report.pobj, ref.report.pobj, rtol=1e-10)
+
+
+def test_sharded_large_instance_matches_single_plan(nccl_group):
+    """20M nonzeros (the size where an unordered plan stream raced torch's copies):
+    the sharded loop on torch's default stream equals the single-plan iteration bit for bit."""
+    import torch
+
+    from paper_2203_05027_b200 import SolverConfig
+    from paper_2203_05027_b200.devgen import generate_device_shard
+    from paper_2203_05027_b200.sharded import CudaRankBackend, run_sharded
+
+    st = torch.cuda.current_stream()
+    plan, rc, cc, cs, bn, cn, cones = generate_device_shard(1_000_000, 2_000_000, 1e-5, "lp", 0, 0, 1,
+                                                            stream=st.cuda_stream)
+    iters = 8
+    plan.set_state(1.0, None, export=False)
+    plan.iterate(1.0, iters)
+    ref = plan.get_state(want_yg=False)
+    plan.set_state(1.0, None, export=False)
+    be = CudaRankBackend.from_plan(plan, cc[0], cc[1], cs, cones)
+    cfg = SolverConfig(max_iters=iters, check_every=5, eps_prim=0.0, eps_dual=0.0, eps_gap=0.0)
+    res = run_sharded(be, rc, cc, cfg, bn, cn)
+    assert np.array_equal(res.x, ref["x"])
+    assert np.array_equal(res.lam, ref["lam"])
+    be.close()
