@@ -166,6 +166,8 @@ int cf_plan_solve(cf_plan* plan, const cf_config* cfg,
  * Sums run sequentially in canonical order, bit-identical to np.bincount. */
 int cf_apply_A(cf_plan* plan, const double* x_dev, double* y_dev);
 int cf_apply_At(cf_plan* plan, const double* y_dev, double* x_dev);
+/* cf_apply_At without the final stream synchronisation (ordered on the plan's stream) */
+int cf_apply_At_async(cf_plan* plan, const double* y_dev, double* x_dev);
 /* project_product (cones.py:103-110) of a device n-vector onto the plan's cone. */
 int cf_project(cf_plan* plan, const double* w_dev, double* out_dev);
 

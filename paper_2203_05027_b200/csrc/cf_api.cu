@@ -376,6 +376,12 @@ int cf_apply_At(cf_plan* p, const double* y_dev, double* x_dev) {
     return CF_OK;
 }
 
+int cf_apply_At_async(cf_plan* p, const double* y_dev, double* x_dev) {
+    CF_TRY(check_plan(p, "cf_apply_At_async"));
+    CF_TRY(launch_spmv_cols(p, y_dev, x_dev));
+    return CF_OK;
+}
+
 int cf_project(cf_plan* p, const double* w_dev, double* out_dev) {
     CF_TRY(check_plan(p, "cf_project"));
     CF_TRY(launch_project(p, w_dev, out_dev));

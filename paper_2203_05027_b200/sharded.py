@@ -147,6 +147,16 @@ class CudaRankBackend:
             self.plan.apply_At(vec.data_ptr(), self.partial.data_ptr())
         return self.partial
 
+    def partial_into(self, which: str, out):
+        """A^T (h or lam) of the local rows straight into `out` (n doubles), no host sync."""
+        vec = self.h if which == "h" else self.lam
+        if self.m == 0:
+            out.zero_()
+        else:
+            from . import _lib
+
+            _lib.check(self.lib.cf_apply_At_async(self.plan.handle, self._p(vec), self._p(out)))
+
     @classmethod
     def from_plan(cls, plan, col_lo: int, col_hi: int, c_slice, cone_ptr_slice=None):
         """A rank backend over a plan already built on the device (devgen.generate_device_shard)."""
@@ -258,6 +268,18 @@ def run_sharded(be, row_cuts, col_cuts, cfg, b_norms, c_norms, group=None, timin
         pad_idx = torch.cat([torch.arange(col_cuts[r], col_cuts[r + 1], dtype=torch.int64) - col_cuts[r] + r * S
                              for r in range(world)]).to(torch_dev)
 
+    # NCCL fast path: A^T h lands directly in the reduce-scatter input and x is
+    # all-gathered straight into the plan's x buffer (no staging copies, no host sync)
+    fast = (nccl and contiguous and hasattr(be, "partial_into") and world * S == n
+            and getattr(be, "xs", None) is not None and be.xs.numel() == S)
+
+    def reduce_scatter_partial(which):
+        if not fast:
+            return reduce_scatter(be.partial_At(which))
+        be.partial_into(which, padded)
+        dist.reduce_scatter_tensor(rs_out, padded, op=dist.ReduceOp.SUM, group=group)
+        return rs_out
+
     def reduce_scatter(vec):
         if contiguous:
             padded[:n].copy_(vec)
@@ -289,16 +311,20 @@ def run_sharded(be, row_cuts, col_cuts, cfg, b_norms, c_norms, group=None, timin
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
     for k in range(1, cfg.max_iters + 1):
-        ath = reduce_scatter(be.partial_At("h"))
+        ath = reduce_scatter_partial("h")
         be.column_update(ath, cfg.mu)
-        x_full = gather_x(be.x_slice())
-        be.set_x(x_full)
+        if fast:
+            dist.all_gather_into_tensor(be.x_full, be.xs, group=group)
+            x_full = be.x_full
+        else:
+            x_full = gather_x(be.x_slice())
+            be.set_x(x_full)
         report = (k % cfg.check_every == 0) or (k == cfg.max_iters)
         be.row_step(cfg.mu, report)
         if not report:
             continue
         rp = torch.as_tensor(be.row_parts(), dtype=torch.float64, device=torch_dev)
-        atl = reduce_scatter(be.partial_At("lam"))
+        atl = reduce_scatter_partial("lam")
         cp = torch.as_tensor(be.col_parts(atl), dtype=torch.float64, device=torch_dev)
         sums = torch.stack([rp[0], rp[3], cp[0], cp[2], cp[5]])
         maxs = torch.stack([rp[1], rp[2], rp[4], cp[1], cp[3], cp[4], cp[6], cp[7]])
