@@ -18,6 +18,7 @@
 // storage order, so A x and A^T lam are bit-identical to the reference's
 // apply_U(apply_Vt(x)) and apply_V(apply_Ut(lam)). Everything is compiled with
 // -fmad=false so every fp64 operation rounds like its numpy counterpart.
+#include <algorithm>
 #include <cmath>
 
 #include "cf_common.h"
@@ -91,6 +92,7 @@ struct Layout {
     static constexpr bool kGroupEpilogue = false;
     static constexpr int kUnroll = pass::kUnroll;   // gathers in flight per thread
     static constexpr int kMinBlocks = pass::kMinBlocks;
+    static constexpr int kWideUnroll = 16;          // ... when the tiles cannot fill the GPU (Wide<P>)
     __device__ __forceinline__ const double* gvec() const { return g_; }
     static constexpr int kVals = 0;
     __device__ __forceinline__ void load_async(int, double*) const {}
@@ -268,6 +270,7 @@ struct ColIter : ColVecs {
 // k_row_report). Per-thread partials are reduced once per CTA (finish).
 struct ColReport : ColVecs {
     static constexpr int kUnroll = 8;      // 8 report accumulators per thread
+    static constexpr int kWideUnroll = 8;
     static constexpr int kMinBlocks = 2;   // (more registers; runs once per check_every iterations)
     double* part;          // [kReportFieldsCol][kGroups][gridDim.x]
     double d2, dmx, s2, smx, amx, cx, cg, nf;
@@ -580,10 +583,27 @@ int persistent_grid(int n_tiles) {
     return n_tiles < g ? (n_tiles > 0 ? n_tiles : 1) : g;
 }
 
+// Small problems: when the tiles cannot fill the GPU, the pass is latency-bound
+// and each lane keeps more gathers in flight (fewer, wider batches) instead.
+template <class P>
+struct Wide : P {
+    static constexpr int kUnroll = P::kWideUnroll;
+    static constexpr int kMinBlocks = 2;
+};
+constexpr int kWideTiles = 148 * 4;   // below this many tiles a pass runs as Wide<P>
+
 template <class P>
 int launch_pass(const P& pol, const pass::Jds& L, const pass::Tiles& T, const int32_t* done, cudaStream_t st,
                 int* grid_out = nullptr) {
     if (T.n_tiles == 0) return CF_OK;
+    if (T.n_tiles < kWideTiles) {
+        const Wide<P> w{pol};
+        const int grid = persistent_grid<Wide<P>>(T.n_tiles);
+        if (grid_out) *grid_out = grid;
+        CF_CUDA(launch_pdl(pass::k_pass<Wide<P>>, (unsigned)grid, (unsigned)pass::kPThreads,
+                           pass::smem_bytes<Wide<P>>(), st, w, L, T, done));
+        return CF_OK;
+    }
     const int grid = persistent_grid<P>(T.n_tiles);
     if (grid_out) *grid_out = grid;
     CF_CUDA(launch_pdl(pass::k_pass<P>, (unsigned)grid, (unsigned)pass::kPThreads, pass::smem_bytes<P>(), st, pol, L,
@@ -828,7 +848,7 @@ int launch_row_diag(cf_plan* p) {
     return CF_OK;
 }
 
-int max_col_report_ctas() { return persistent_grid<ColReport>(1 << 30); }
+int max_col_report_ctas() { return std::max(persistent_grid<ColReport>(1 << 30), kWideTiles); }
 
 // ---------------------------------------------------------------- row-sharded building blocks
 namespace {
