@@ -76,6 +76,37 @@ __device__ double block_reduce_b(double v, double* sh) {
     return v;   // valid in thread 0
 }
 
+// x / mu; an exact multiply when mu is a power of two (x * (1/mu) == x / mu bit for bit)
+struct MuDivB {
+    double mu, inv;
+    bool pow2;
+    __device__ __forceinline__ double operator()(double x) const { return pow2 ? x * inv : x / mu; }
+};
+__device__ __forceinline__ MuDivB make_mudiv_b(double mu) {
+    int e = 0;
+    const double fr = frexp(mu, &e);
+    return MuDivB{mu, 1.0 / mu, fr == 0.5 && e > -1000 && e < 1000};
+}
+
+// sequential sum of val[q] * g[idx[q]] over [p0, p1) in order, four independent
+// shared-memory loads in flight (the adds stay in canonical order)
+__device__ __forceinline__ double seg_dot(const double* __restrict__ val, const int32_t* __restrict__ idx,
+                                          const double* __restrict__ g, int p0, int p1) {
+    double acc = 0.0;
+    int q = p0;
+    for (; q + 4 <= p1; q += 4) {
+        const int i0 = idx[q], i1 = idx[q + 1], i2 = idx[q + 2], i3 = idx[q + 3];
+        const double v0 = val[q], v1 = val[q + 1], v2 = val[q + 2], v3 = val[q + 3];
+        const double g0 = g[i0], g1 = g[i1], g2 = g[i2], g3 = g[i3];
+        acc = __dadd_rn(acc, __dmul_rn(v0, g0));
+        acc = __dadd_rn(acc, __dmul_rn(v1, g1));
+        acc = __dadd_rn(acc, __dmul_rn(v2, g2));
+        acc = __dadd_rn(acc, __dmul_rn(v3, g3));
+    }
+    for (; q < p1; ++q) acc = __dadd_rn(acc, __dmul_rn(val[q], g[idx[q]]));
+    return acc;
+}
+
 __device__ __forceinline__ void project_block_b(const double* w, int q, double* out) {
     const double w0 = w[0];
     double ssq = 0.0;
@@ -92,7 +123,7 @@ __device__ __forceinline__ void project_block_b(const double* w, int q, double* 
     }
 }
 
-__global__ void __launch_bounds__(kBT) k_batch(const BatchArgs a) {
+__global__ void __launch_bounds__(kBT, 3) k_batch(const BatchArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int CM = a.cap_m, CN = a.cap_n, CO = a.cap_o;
     // shared-memory carve-up (doubles first)
@@ -110,7 +141,9 @@ __global__ void __launch_bounds__(kBT) k_batch(const BatchArgs a) {
     double* z = x + CN;
     double* dl = z + CN;
     double* wv = dl + CN;     // cones: x+ - delta/mu, then z+
-    double* red = wv + CN;    // 32
+    double* fvs = wv + CN;    // 1/(1+cnt_j) (uv.py:82), constant per problem
+    double* cmu = fvs + CN;   // c_j / mu, constant per problem
+    double* red = cmu + CN;   // 32
     int32_t* colidx = reinterpret_cast<int32_t*>(red + 32);
     int32_t* rowidx = colidx + CO;
     int32_t* rowptr = rowidx + CO;
@@ -130,6 +163,7 @@ __global__ void __launch_bounds__(kBT) k_batch(const BatchArgs a) {
         const int o = (int)(a.colptr[c0 + n] - kc0);
         const cf_config cfg = a.cfg[pid];
         const double mu = cfg.mu;
+        const MuDivB div = make_mudiv_b(mu);
         // ---- load the problem (canonical CSC, CSR, vectors) and a cold start (solver.py:309)
         for (int i = t; i <= m; i += kBT) rowptr[i] = (int32_t)(a.rowptr[r0 + i] - kr0);
         for (int j = t; j <= n; j += kBT) colptr[j] = (int32_t)(a.colptr[c0 + j] - kc0);
@@ -148,7 +182,10 @@ __global__ void __launch_bounds__(kBT) k_batch(const BatchArgs a) {
             br[i] = 0.0;
         }
         for (int j = t; j < n; j += kBT) {
-            c[j] = a.c[c0 + j];
+            const double cj = a.c[c0 + j];
+            c[j] = cj;
+            cmu[j] = div(cj);
+            fvs[j] = 1.0 / (1.0 + (double)(a.colptr[c0 + j + 1] - a.colptr[c0 + j]));
             x[j] = 0.0;
             z[j] = 0.0;
             dl[j] = 0.0;
@@ -168,14 +205,13 @@ __global__ void __launch_bounds__(kBT) k_batch(const BatchArgs a) {
             // ---- column pass: x_update, z_update, delta update (solver.py:168-176,186-188,196)
             for (int j = t; j < n; j += kBT) {
                 const int p0 = colptr[j], p1 = colptr[j + 1];
-                double ath = 0.0;
-                for (int q = p0; q < p1; ++q) ath = __dadd_rn(ath, __dmul_rn(valc[q], h[rowidx[q]]));
+                const double ath = seg_dot(valc, rowidx, h, p0, p1);
                 const int cnt = p1 - p0;
-                const double fv = 1.0 / (1.0 + (double)cnt);
-                const double xj = x[j], zj = z[j], dj = dl[j], cj = c[j];
-                const double dm = dj / mu;
+                const double fv = fvs[j];
+                const double xj = x[j], zj = z[j], dj = dl[j];
+                const double dm = div(dj);
                 const double v = __dadd_rn(__dmul_rn((double)cnt, xj), ath);
-                const double xp = fv * (((v + zj) + dm) - cj / mu);
+                const double xp = fv * (((v + zj) + dm) - cmu[j]);
                 const double w = xp - dm;
                 x[j] = xp;
                 if (!a.cones) {
@@ -198,14 +234,13 @@ __global__ void __launch_bounds__(kBT) k_batch(const BatchArgs a) {
             // ---- row pass: y_update + lam/gamma of dual_update (solver.py:179-183,194-195)
             for (int i = t; i < m; i += kBT) {
                 const int p0 = rowptr[i], p1 = rowptr[i + 1];
-                double axi = 0.0;
-                for (int q = p0; q < p1; ++q) axi = __dadd_rn(axi, __dmul_rn(valr[q], x[colidx[q]]));
+                const double axi = seg_dot(valr, colidx, x, p0, p1);
                 const double bi = b[i];
                 const double r = fu[i] * (db[i] + axi);
                 const double ln = lam[i] + mu * (r - bi);
                 const double bmr = bi - r;
                 lam[i] = ln;
-                h[i] = bmr - ln / mu;
+                h[i] = bmr - div(ln);
                 if (report) {
                     br[i] = bmr;
                     ax[i] = axi;
@@ -280,7 +315,7 @@ __global__ void __launch_bounds__(kBT) k_batch(const BatchArgs a) {
 }
 
 size_t batch_smem(int cm, int cn, int co, int ck) {
-    return sizeof(double) * (size_t)(2 * co + 7 * cm + 5 * cn + 32) +
+    return sizeof(double) * (size_t)(2 * co + 7 * cm + 7 * cn + 32) +
            sizeof(int32_t) * (size_t)(2 * co + cm + 1 + cn + 1 + ck + 1) + 16;
 }
 
