@@ -51,9 +51,6 @@ namespace pass {
 #ifndef CF_GROUPS
 #define CF_GROUPS 2                // (TMA engine) compute groups per CTA
 #endif
-#ifndef CF_PIPE
-#define CF_PIPE 0                  // (direct engine) software-pipelined idx/val loads across diagonals and blocks
-#endif
 #ifndef CF_GATHER_NOALLOC
 #define CF_GATHER_NOALLOC 1        // gathers bypass L1 allocation (measured: +3%)
 #endif
@@ -237,22 +234,6 @@ struct Jds {
     const uint32_t* pl;
 };
 
-// L2 prefetch (TMA unit, no data returned to the SM) of [first, first+count)
-template <class T>
-__device__ __forceinline__ void prefetch_l2(const T* first, int64_t count) {
-    if (count <= 0) return;
-    const uintptr_t a = (uintptr_t)first & ~(uintptr_t)15u;
-    const uintptr_t e = ((uintptr_t)(first + count) + 15u) & ~(uintptr_t)15u;
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)(e - a)) : "memory");
-}
-__device__ __forceinline__ void prefetch_tile(const Jds& L, const Tiles& T, int tile) {
-    if (tile >= T.n_tiles) return;
-    const int4 lo = __ldg(T.tb + tile), hi = __ldg(T.tb + tile + 1);
-    prefetch_l2(L.idx + lo.y, hi.y - lo.y);
-    prefetch_l2(L.val + lo.y, hi.y - lo.y);
-    if (lo.z) prefetch_l2(L.pl + lo.x, hi.x - lo.x);
-}
-
 // ---------------------------------------------------------------- the engine
 // P (the pass policy) provides (device):
 //   const double* gvec() const                 gathered operand
@@ -267,6 +248,7 @@ __device__ __forceinline__ void prefetch_tile(const Jds& L, const Tiles& T, int 
 //                                              epilogue of local segment q (natural order)
 //   void group(Smem&, int tile, int s0, int nseg)   (kGroupEpilogue) after a group barrier
 //   void finish(Smem&)                         compute threads, after the last tile
+
 // rank r's pl entry -> its length, and the block's first nonzero (from rank 0)
 __device__ __forceinline__ int pl_len(uint32_t pr) { return (int)((pr >> kPlPermBits) & ((1u << kPlLenBits) - 1u)); }
 __device__ __forceinline__ int pl_start(uint32_t pr) { return (int)(pr >> (kPlPermBits + kPlLenBits)); }
@@ -536,135 +518,6 @@ __global__ void __launch_bounds__(kPThreads, 1) k_pass(const P p0, const Jds L, 
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[s]);
-    }
-    p.finish(sm);
-}
-
-#elif CF_PIPE
-// Each warp streams its warp blocks (block gw of tiles blockIdx.x, +G, ...) as
-// one software pipeline: idx/val of the next U diagonals — or of the first U
-// diagonals of its next block — are loaded while the current gathers are in
-// flight, so a block's dependent chain (pl -> idx -> gather) is hidden.
-template <class P>
-__global__ void __launch_bounds__(kPThreads, P::kMinBlocks) k_pass(const P p0, const Jds L, const Tiles T,
-                                                               const int32_t* done) {
-    P p = p0;  // per-thread mutable copy (report accumulators live in registers)
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-    const int G = gridDim.x;
-    const int lane = threadIdx.x & 31;
-    const int gt = threadIdx.x;
-    const int gw = gt >> 5;      // warp = warp block of the tile
-    for (int c = gt; c < kFvTab; c += kPThreads) sm.fvtab[c] = 1.0 / (1.0 + (double)c);
-    __syncthreads();
-    pdl_wait();   // everything above is independent of the previous kernel
-    pdl_trigger();
-    if (done && *done) return;
-    const uint64_t pl_ = pol_last(), pf = pol_first();
-    const double* __restrict__ g = p.gvec();
-    const int32_t* plw = reinterpret_cast<const int32_t*>(L.pl);
-    double* wacc = sm.wacc[0] + gw * 32;
-    int32_t* wcnt = sm.wcnt[0] + gw * 32;
-    constexpr int U = P::kUnroll;
-
-    int tile = blockIdx.x;
-    int4 lo = make_int4(0, 0, 0, 0), hi = lo;
-    int nb = 0;          // segments of this warp's block in the current tile (<= 0: none)
-    uint32_t pr = 0;     // this lane's pl entry
-    int mylen = 0, pos = 0;
-    int nj[U];
-    double nv[U];
-    if (tile < T.n_tiles) {
-        lo = __ldg(T.tb + tile);
-        hi = __ldg(T.tb + tile + 1);
-        nb = lo.z ? min(32, hi.x - lo.x - gw * 32) : 0;
-        pr = (nb > 0 && lane < nb) ? (uint32_t)ld_first(plw + lo.x + gw * 32 + lane, pf) : 0u;
-        mylen = pl_len(pr);
-        pos = lo.y + __shfl_sync(0xffffffffu, pl_start(pr), 0) + lane;
-        if (nb > 0) load_batch<U>(L, nj, nv, pos, mylen, 0, pf);
-    }
-    while (tile < T.n_tiles) {
-        // next tile of this CTA: its table entries and this warp's pl entry are loaded now
-        const int ntile = tile + G;
-        const bool has_next = ntile < T.n_tiles;
-        int4 nlo = lo, nhi = hi;
-        if (has_next) {
-            nlo = __ldg(T.tb + ntile);
-            nhi = __ldg(T.tb + ntile + 1);
-        }
-        const int nnb = (has_next && nlo.z) ? min(32, nhi.x - nlo.x - gw * 32) : 0;
-        const uint32_t npr = (nnb > 0 && lane < nnb) ? (uint32_t)ld_first(plw + nlo.x + gw * 32 + lane, pf) : 0u;
-        bool pre = false;    // next block's first batch already in nj/nv
-        const int nmylen = pl_len(npr);
-        int npos = 0;
-        const int s0 = lo.x, nseg = hi.x - lo.x, k0 = lo.y, len = hi.y - lo.y;
-        if (lo.z) {
-            if (nb > 0) {
-                const bool nat = lane < nb;             // natural segment gw*32 + lane exists
-                double* slot = &sm.vals[gw][0][lane];
-                if (P::kVals > 0) {
-                    if (nat) p.load_async(s0 + gw * 32 + lane, slot);
-                    cp_async_commit();
-                }
-                const int q = (int)(pr & 31u);          // local segment (within the block) of rank r
-                const int mlen = __shfl_sync(0xffffffffu, mylen, 0);   // rank 0 is the longest
-                // rank r's own carry (no shuffle: the load's latency hides behind the gathers)
-                double acc = (p.carry_in() && nat) ? p.carry(s0 + gw * 32 + q) : 0.0;
-                for (int k = 0; k < mlen; k += U) {
-                    double av[U], gv[U];
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        gv[u] = (mylen > k + u) ? ld_gather(g + nj[u], pl_) : 0.0;
-                        av[u] = nv[u];
-                    }
-                    if (k + U < mlen) {
-                        load_batch<U>(L, nj, nv, pos, mylen, k + U, pf);
-                    } else if (nnb > 0) {
-                        npos = nlo.y + __shfl_sync(0xffffffffu, pl_start(npr), 0) + lane;
-                        load_batch<U>(L, nj, nv, npos, nmylen, 0, pf);
-                        pre = true;
-                    }
-#pragma unroll
-                    for (int u = 0; u < U; ++u)
-                        if (mylen > k + u) {
-                            p.check(av[u], 0, gv[u]);
-                            acc = __dadd_rn(acc, __dmul_rn(av[u], gv[u]));
-                        }
-                }
-                // rank -> natural order inside the warp (a segment's count is its length)
-                if (nat) {
-                    wacc[q] = acc;
-                    wcnt[q] = mylen;
-                }
-                Vals vv{};
-                if (P::kVals > 0) {
-                    cp_async_wait_all();
-#pragma unroll
-                    for (int f = 0; f < P::kVals; ++f) vv.v[f] = slot[32 * f];
-                }
-                __syncwarp();
-                if (nat) p.segment(sm, tile, s0, gw * 32 + lane, wcnt[lane], wacc[lane], vv);
-                __syncwarp();
-            }
-        } else {
-            long_tile(p, sm, L, tile, s0, k0, len);
-        }
-        if (P::kGroupEpilogue) {
-            __syncthreads();
-            p.group(sm, tile, s0, nseg);
-            __syncthreads();   // cone scratch is rewritten by the next tile
-        }
-        if (!pre && nnb > 0) {
-            npos = nlo.y + __shfl_sync(0xffffffffu, pl_start(npr), 0) + lane;
-            load_batch<U>(L, nj, nv, npos, nmylen, 0, pf);
-        }
-        tile = ntile;
-        lo = nlo;
-        hi = nhi;
-        nb = nnb;
-        pr = npr;
-        mylen = nmylen;
-        pos = npos;
     }
     p.finish(sm);
 }
