@@ -130,6 +130,7 @@ struct cf_plan {
     cf::DevBuf<int32_t> tile_big;      // big-cone id of a tile, -1 otherwise
     cf::DevBuf<int32_t> big_cone;      // cone index of each big cone
     int64_t n_big = 0;
+    int32_t warp_cone = 0;             // uniform cone size in {2,4,...,32} with no big cones (warp epilogue), else 0
     cf::DevBuf<int4> row_tb, col_tb;   // tile table {first segment, first nonzero, normal (1) / long (0), 0}
     // jagged-diagonal copies of the CSR panels (rj_*) and of the CSC (cj_*) read by the passes
     cf::DevBuf<int32_t> rj_idx, cj_idx;

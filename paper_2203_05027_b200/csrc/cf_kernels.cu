@@ -197,9 +197,17 @@ struct ColVecs : Layout {
 // V(y + gamma/mu) = cnt*x + A^T h, then z = Proj_K(x+ - delta/mu), delta update.
 // CONES=false: all blocks of size 1 (cones.py:108-109 shortcut), fused per column.
 // CONES=true : x+, w, delta per column to shared memory, then (group epilogue) one thread per cone.
-template <bool CONES>
+// MODE kLP: all blocks of size 1 (cones.py:108-109 shortcut), fused per column.
+// MODE kGroupCones: x+, w, delta to shared memory, group barrier, one thread per cone.
+// MODE kWarpCones: every cone has the same size cs in {2,4,...,32} and starts at a
+//   multiple of cs, so a cone is cs adjacent lanes of one warp (natural order):
+//   the tail norm is summed in order through shuffles, no barrier.
+constexpr int kLP = 0, kGroupCones = 1, kWarpCones = 2;
+
+template <int MODE>
 struct ColIter : ColVecs {
-    static constexpr bool kGroupEpilogue = CONES;
+    static constexpr bool CONES = MODE != kLP;
+    static constexpr bool kGroupEpilogue = MODE == kGroupCones;
     double* x;
     double* z;
     double* delta;
@@ -211,6 +219,7 @@ struct ColIter : ColVecs {
     double* wbuf;
     double mu;
     pass::MuDiv div;
+    int32_t cs;            // kWarpCones: the uniform cone size
     __device__ __forceinline__ void segment(Smem& sm, int, int s0, int q, int cnt, double ath, const Vals& vv) {
         const int j = s0 + q;
         const double fv = cnt < pass::kFvTab ? sm.fvtab[cnt] : 1.0 / (1.0 + (double)cnt);   // uv.py:82
@@ -220,10 +229,38 @@ struct ColIter : ColVecs {
         if (ccorr) v = v - ccorr[j];
         const double xp = fv * (((v + zj) + dm) - div(cj));   // solver.py:171-176 operand order
         const double w = xp - dm;                            // solver.py:188
-        if (!CONES) {
+        if (MODE == kLP) {
             const double zp = w > 0.0 ? w : 0.0;             // NaN -> 0, -0 -> +0
             const double dp = dj + mu * (zp - xp);           // solver.py:196
             pass::st_hint(x + j, xp, pass::pol_last());      // gathered by the next row pass
+            pass::st_hint(z + j, zp, pass::pol_first());
+            pass::st_hint(delta + j, dp, pass::pol_first());
+        } else if (MODE == kWarpCones) {
+            // project_block (cones.py:76-92) on cs adjacent lanes; the callers of segment()
+            // are the tile's lanes < nb, converged, and nb is a multiple of cs
+            const unsigned mask = __activemask();
+            const int lane = threadIdx.x & 31;
+            const int head = lane & ~(cs - 1);
+            double ssq = 0.0;
+            for (int t = 1; t < cs; ++t) {
+                const double wt = __shfl_sync(mask, w, head + t);
+                ssq = __dadd_rn(ssq, __dmul_rn(wt, wt));
+            }
+            const double w0 = __shfl_sync(mask, w, head);
+            const double alpha = sqrt(ssq);
+            double zp;
+            if (alpha <= -w0) {
+                zp = 0.0;
+            } else if (alpha <= w0) {
+                zp = w;
+            } else if (lane == head) {
+                zp = __dadd_rn(__dmul_rn(0.5, w0), __dmul_rn(0.5, alpha));
+            } else {
+                const double factor = w0 / (2.0 * alpha);
+                zp = __dadd_rn(__dmul_rn(0.5, w), __dmul_rn(factor, w));
+            }
+            const double dp = dj + mu * (zp - xp);
+            pass::st_hint(x + j, xp, pass::pol_last());
             pass::st_hint(z + j, zp, pass::pol_first());
             pass::st_hint(delta + j, dp, pass::pol_first());
         } else {
@@ -611,9 +648,9 @@ int launch_pass(const P& pol, const pass::Jds& L, const pass::Tiles& T, const in
     return CF_OK;
 }
 
-template <bool CONES>
-ColIter<CONES> col_iter(cf_plan* p, const IterOpts& opt) {
-    ColIter<CONES> c{};
+template <int MODE>
+ColIter<MODE> col_iter(cf_plan* p, const IterOpts& opt) {
+    ColIter<MODE> c{};
     c.g_ = p->h.p;
     c.x_in = p->x.p;
     c.z_in = p->z.p;
@@ -630,6 +667,7 @@ ColIter<CONES> col_iter(cf_plan* p, const IterOpts& opt) {
     c.ccorr = opt.ccorr;
     c.mu = opt.mu;
     c.div = pass::make_mudiv(opt.mu);
+    c.cs = p->warp_cone;
     return c;
 }
 
@@ -680,9 +718,11 @@ int launch_iteration(cf_plan* p, const IterOpts& opt, const int32_t* done, int64
     }
     if (p->n > 0) {
         if (p->all_unit) {
-            CF_TRY(launch_pass(col_iter<false>(p, opt), col_jds(p), col_tiles(p), done, p->stream));
+            CF_TRY(launch_pass(col_iter<kLP>(p, opt), col_jds(p), col_tiles(p), done, p->stream));
+        } else if (p->warp_cone) {
+            CF_TRY(launch_pass(col_iter<kWarpCones>(p, opt), col_jds(p), col_tiles(p), done, p->stream));
         } else {
-            CF_TRY(launch_pass(col_iter<true>(p, opt), col_jds(p), col_tiles(p), done, p->stream));
+            CF_TRY(launch_pass(col_iter<kGroupCones>(p, opt), col_jds(p), col_tiles(p), done, p->stream));
         }
         ++nl;
         if (!p->all_unit && p->n_big > 0) {

@@ -391,6 +391,13 @@ int build_tiles(cf_plan* p, const int64_t* sizes, int64_t nb) {
     tick("col tiles (host)");
     p->col_tiles = (int64_t)ctb.size() - 1;
     p->n_big = (int64_t)big.size();
+    p->warp_cone = 0;
+    if (!p->all_unit && p->n_big == 0 && nb > 0 && !getenv("CF_GROUP_CONES")) {   // (env: force the group path)
+        const int64_t s = sizes[0];
+        bool uniform = s >= 2 && s <= 32 && (s & (s - 1)) == 0;
+        for (int64_t q = 1; q < nb && uniform; ++q) uniform = sizes[q] == s;
+        if (uniform) p->warp_cone = (int32_t)s;
+    }
     CF_TRY(build_jds(p, p->rowptr.p, p->colidx.p, p->valr.p, rtb, nsr, p->row_tb, p->rj_idx, p->rj_val, p->rj_pl));
     CF_TRY(build_jds(p, p->colptr.p, p->rowidx.p, p->valc.p, ctb, n, p->col_tb, p->cj_idx, p->cj_val, p->cj_pl));
     if (verbose) CF_CUDA(cudaStreamSynchronize(p->stream));

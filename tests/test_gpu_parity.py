@@ -366,3 +366,17 @@ def test_solve_batch_matches_solve():
     ox, olam, otrace, _ = oracle.solve(q, cfg2)
     assert rb.report.status == otrace[-1]["status"] and rb.report.iter == otrace[-1]["iter"]
     assert rel_err(rb.x, ox) <= 1e-8 and rel_err(rb.lam, olam) <= 1e-8
+
+
+def test_warp_cone_epilogue_equals_group_epilogue(monkeypatch):
+    """Uniform K4 cones take the warp-shuffle epilogue; it is bit-identical to the
+    shared-memory group epilogue (forced with CF_GROUP_CONES) and to the oracle's projection."""
+    from paper_2203_05027_b200 import GenSpec, SolverConfig, generate, solve
+
+    p = generate(GenSpec(300, 1200, 0.02, "socp4", seed=4))
+    cfg = SolverConfig(max_iters=300, check_every=25, eps_prim=1e-6, eps_dual=1e-6, eps_gap=1e-6)
+    warp = solve(p, cfg)
+    monkeypatch.setenv("CF_GROUP_CONES", "1")
+    group = solve(p, cfg)
+    assert np.array_equal(warp.x, group.x) and np.array_equal(warp.lam, group.lam)
+    assert [r.iter for r in warp.trace] == [r.iter for r in group.trace]
