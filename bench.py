@@ -349,10 +349,14 @@ def run_ours(args, spec, rank, world, local_rank):
         res = solve(p, tol)
         t1 = time.perf_counter()
         secs = t1 - t0
-        e2e = {"value": res.report.iter / secs, "unit": UNIT,
+        if dist:   # replicas: the job's solves over the slowest rank's wall time
+            s_t = torch.tensor([secs], dtype=torch.float64, device="cuda")
+            tdist.all_reduce(s_t, op=tdist.ReduceOp.MAX)
+            secs = float(s_t.item())
+        e2e = {"value": world * res.report.iter / secs, "unit": UNIT,
                "h2d_bytes_per_step": 24 * o + 8 * m + 8 * n, "d2h_bytes_per_step": 8 * (m + n),
                "seconds": secs, "iters": res.report.iter, "status": res.report.status,
-               "step": "one solve(p, SolverConfig(eps=%g)) from host numpy buffers" % args.eps}
+               "step": "one solve(p, SolverConfig(eps=%g)) from host numpy buffers per rank" % args.eps}
         if ttt is not None and res.report.iter != ttt["iters"]:
             e2e["note"] = "iteration count differs from the device-resident run"
     else:
