@@ -45,5 +45,18 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     return target
 
 
+# Compile-time engine variants kept measured and tested beside the product library
+# (DESIGN.md §4.1): the producer-warp TMA ring engine.
+VARIANTS = {"tma": ["CF_TMA=1"]}
+
+
+def variant_path(name: str) -> str:
+    return os.path.join(HERE, f"libcfb200_{name}.so")
+
+
+def build_variants(verbose: bool = False) -> list:
+    return [build(force=True, verbose=verbose, out=variant_path(k), defines=v) for k, v in VARIANTS.items()]
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))

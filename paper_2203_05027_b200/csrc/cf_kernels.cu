@@ -206,7 +206,6 @@ constexpr int kLP = 0, kGroupCones = 1, kWarpCones = 2;
 
 template <int MODE>
 struct ColIter : ColVecs {
-    static constexpr bool CONES = MODE != kLP;
     static constexpr bool kGroupEpilogue = MODE == kGroupCones;
     double* x;
     double* z;
