@@ -168,6 +168,11 @@ int cf_apply_A(cf_plan* plan, const double* x_dev, double* y_dev);
 int cf_apply_At(cf_plan* plan, const double* y_dev, double* x_dev);
 /* cf_apply_At without the final stream synchronisation (ordered on the plan's stream) */
 int cf_apply_At_async(cf_plan* plan, const double* y_dev, double* x_dev);
+/* the part of cf_apply_At_async on the column tiles that START in [col_lo, col_hi): calling it
+ * for consecutive ranges covers every column once, and after the call for [lo_r, lo_{r+1})
+ * every column < lo_{r+1} is written (the sharded driver overlaps each range's reduction with
+ * the next range's compute) */
+int cf_apply_At_cols(cf_plan* plan, const double* y_dev, double* x_dev, int64_t col_lo, int64_t col_hi);
 /* project_product (cones.py:103-110) of a device n-vector onto the plan's cone. */
 int cf_project(cf_plan* plan, const double* w_dev, double* out_dev);
 

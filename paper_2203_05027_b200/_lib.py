@@ -102,6 +102,7 @@ SIGNATURES = {
     "cf_apply_A": (c_int, [_P, _P, _P]),
     "cf_apply_At": (c_int, [_P, _P, _P]),
     "cf_apply_At_async": (c_int, [_P, _P, _P]),
+    "cf_apply_At_cols": (c_int, [_P, _P, _P, c_int64, c_int64]),
     "cf_project": (c_int, [_P, _P, _P]),
     "cf_plan_last_timing": (c_int, [_P, _D, _I64, _D, _D, _I64]),
     "cf_plan_vector": (c_int, [_P, c_int, POINTER(c_void_p), _I64]),

@@ -60,3 +60,5 @@ def build_variants(verbose: bool = False) -> list:
 
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))
+    if "--all" in sys.argv:
+        print(build_variants(verbose=True))

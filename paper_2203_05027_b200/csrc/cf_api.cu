@@ -382,6 +382,12 @@ int cf_apply_At_async(cf_plan* p, const double* y_dev, double* x_dev) {
     return CF_OK;
 }
 
+int cf_apply_At_cols(cf_plan* p, const double* y_dev, double* x_dev, int64_t col_lo, int64_t col_hi) {
+    CF_TRY(check_plan(p, "cf_apply_At_cols"));
+    CF_TRY(launch_spmv_cols_range(p, y_dev, x_dev, col_lo, col_hi));
+    return CF_OK;
+}
+
 int cf_project(cf_plan* p, const double* w_dev, double* out_dev) {
     CF_TRY(check_plan(p, "cf_project"));
     CF_TRY(launch_project(p, w_dev, out_dev));

@@ -142,6 +142,7 @@ struct cf_plan {
     int32_t n_panels = 1;
     int64_t panel_cols = 0;
     std::vector<int64_t> row_panel_tile;   // first row tile of each panel (n_panels+1)
+    std::vector<int32_t> col_tile_start;   // first column of each column tile (host copy, col_tiles+1)
     cf::DevBuf<double> wbuf;           // w = x+ - delta/mu for big-cone columns
 
     // iterate state: x, z, delta (n); lam, h (m); br = b - r (m) when kept
@@ -197,6 +198,8 @@ int launch_iteration(cf_plan* p, const IterOpts& opt, const int32_t* done, int64
 // y = A x (rows), x = A^T y (cols)
 int launch_spmv_rows(cf_plan* p, const double* x, double* y);
 int launch_spmv_cols(cf_plan* p, const double* y, double* x);
+// x = A^T y on the column tiles that start in [col_lo, col_hi) (async, plan stream)
+int launch_spmv_cols_range(cf_plan* p, const double* y, double* x, int64_t col_lo, int64_t col_hi);
 // report of the current state into p->report_slot[slot]; termination per cfg (nullable)
 int launch_report(cf_plan* p, double mu, bool ax_ready, const cf_config* cfg, int64_t k,
                   int64_t slot, const int32_t* done, int64_t* launches);

@@ -782,6 +782,18 @@ int launch_spmv_cols(cf_plan* p, const double* y, double* x) {
     return launch_pass(c, col_jds(p), col_tiles(p), nullptr, p->stream);
 }
 
+int launch_spmv_cols_range(cf_plan* p, const double* y, double* x, int64_t col_lo, int64_t col_hi) {
+    if (p->n == 0 || p->col_tile_start.size() < 2 || col_hi <= col_lo) return CF_OK;
+    const auto& ts = p->col_tile_start;   // col_tiles + 1 entries, the last = n
+    const int64_t t0 = std::lower_bound(ts.begin(), ts.end() - 1, (int32_t)col_lo) - ts.begin();
+    const int64_t t1 = std::lower_bound(ts.begin(), ts.end() - 1, (int32_t)std::min<int64_t>(col_hi, p->n)) - ts.begin();
+    if (t1 <= t0) return CF_OK;
+    ColSpmv c{};
+    c.g_ = y;
+    c.y = x;
+    return launch_pass(c, col_jds(p), pass::Tiles{p->col_tb.p + t0, (int32_t)(t1 - t0)}, nullptr, p->stream);
+}
+
 int launch_report(cf_plan* p, double mu, bool ax_ready, const cf_config* cfg, int64_t k, int64_t slot,
                   const int32_t* done, int64_t* launches) {
     (void)mu;

@@ -388,6 +388,8 @@ int build_tiles(cf_plan* p, const int64_t* sizes, int64_t nb) {
     }
     std::vector<int4> ctb;
     tile_table(cp, cstarts, n, ctb);
+    p->col_tile_start.resize(ctb.size());
+    for (size_t t = 0; t < ctb.size(); ++t) p->col_tile_start[t] = ctb[t].x;
     tick("col tiles (host)");
     p->col_tiles = (int64_t)ctb.size() - 1;
     p->n_big = (int64_t)big.size();

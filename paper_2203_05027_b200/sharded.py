@@ -147,6 +147,17 @@ class CudaRankBackend:
             self.plan.apply_At(vec.data_ptr(), self.partial.data_ptr())
         return self.partial
 
+    def partial_range_into(self, which: str, out, col_lo: int, col_hi: int):
+        """The column tiles of A^T (h or lam) that start in [col_lo, col_hi), into out (no host sync)."""
+        vec = self.h if which == "h" else self.lam
+        if self.m == 0:
+            out[col_lo:col_hi].zero_()
+        else:
+            from . import _lib
+
+            _lib.check(self.lib.cf_apply_At_cols(self.plan.handle, self._p(vec), self._p(out), int(col_lo),
+                                                 int(col_hi)))
+
     def partial_into(self, which: str, out):
         """A^T (h or lam) of the local rows straight into `out` (n doubles), no host sync."""
         vec = self.h if which == "h" else self.lam
@@ -242,10 +253,12 @@ def solve_sharded(p, cfg: SolverConfig | None = None, group=None, backend_factor
 
 
 def run_sharded(be, row_cuts, col_cuts, cfg, b_norms, c_norms, group=None, timing=None,
-                gather_result: bool = True) -> SolveResult:
+                gather_result: bool = True, overlap_reduce: bool = True) -> SolveResult:
     """The sharded loop on an existing rank backend (row/column cuts shared by all ranks).
 
-    ``timing``: if a dict, receives the CUDA-event time of the loop on this rank (ms)."""
+    ``timing``: if a dict, receives the CUDA-event time of the loop on this rank (ms).
+    ``overlap_reduce``: NCCL + CUDA backend: reduce A^T h slice by slice, overlapped with the
+    next slice's column pass (else one reduce-scatter after the whole pass)."""
     import torch
     import torch.distributed as dist
 
@@ -273,9 +286,23 @@ def run_sharded(be, row_cuts, col_cuts, cfg, b_norms, c_norms, group=None, timin
     fast = (nccl and contiguous and hasattr(be, "partial_into") and world * S == n
             and getattr(be, "xs", None) is not None and be.xs.numel() == S)
 
+    # overlap: the column pass runs slice by slice (tiles starting in slice r); slice r's
+    # sums go to their owner with an async NCCL reduce while slice r+1 computes
+    overlap = fast and overlap_reduce and hasattr(be, "partial_range_into")
+
     def reduce_scatter_partial(which):
         if not fast:
             return reduce_scatter(be.partial_At(which))
+        if overlap:
+            works = []
+            for r in range(world):
+                be.partial_range_into(which, padded, col_cuts[r], col_cuts[r + 1])
+                dst = r if group is None else dist.get_global_rank(group, r)
+                works.append(dist.reduce(padded[col_cuts[r]:col_cuts[r + 1]], dst=dst, op=dist.ReduceOp.SUM,
+                                         group=group, async_op=True))
+            for w in works:
+                w.wait()
+            return padded[lo:hi]
         be.partial_into(which, padded)
         dist.reduce_scatter_tensor(rs_out, padded, op=dist.ReduceOp.SUM, group=group)
         return rs_out
