@@ -453,6 +453,13 @@ def run_sharded_bench(args, spec, rank, world, local_rank):
     return 0
 
 
+def _oracle_iters(p, cfg, budget_s):
+    import oracle
+
+    _, _, tr, _ = oracle.solve(p, cfg, max_wall_s=budget_s)
+    return tr[-1]["iter"]
+
+
 def run_batch(args, spec, rank, world):
     """C4: solve_batch over 4096 generated problems; value = problem-iterations/s of the batch kernel."""
     import numpy as np
@@ -475,20 +482,27 @@ def run_batch(args, spec, rank, world):
         statuses[r.report.status] = statuses.get(r.report.status, 0) + 1
     cpu = None
     if not args.skip_cpu:
-        import oracle
+        # the reference batches with a process pool over solve() (bench.py:96-106): the oracle
+        # port on every host core, problems dealt in order, for a bounded wall time
+        from concurrent.futures import ProcessPoolExecutor
 
-        ts, its = 0.0, 0
+        workers = os.cpu_count() or 1
         t_start = time.perf_counter()
-        for s in range(P):
-            tt = time.perf_counter()
-            _, _, tr, _ = oracle.solve(probs[s], cfg, max_wall_s=args.cpu_budget)
-            ts += time.perf_counter() - tt
-            its += tr[-1]["iter"]
-            if time.perf_counter() - t_start > args.cpu_budget:
-                break
-        cpu = {"value": its / ts, "unit": "problem-iterations/s", "cores": 1, "kind": "port",
-               "sample": f"oracle port solving problems 0..{s} of the batch to eps={args.eps} (or the budget) "
-                         f"one after another: {its} iterations in {ts:.1f} s"}
+        its, done = 0, 0
+        with ProcessPoolExecutor(max_workers=workers) as pool:
+            futs = [pool.submit(_oracle_iters, probs[s], cfg, args.cpu_budget) for s in range(min(P, 64 * workers))]
+            for fu in futs:
+                if time.perf_counter() - t_start > args.cpu_budget:
+                    break
+                its += fu.result()
+                done += 1
+            wall = time.perf_counter() - t_start
+            for fu in futs:
+                fu.cancel()
+        cpu = {"value": its / wall, "unit": "problem-iterations/s", "cores": workers, "kind": "port",
+               "sample": f"oracle port solving the first {done} problems of the batch to eps={args.eps} in a "
+                         f"{workers}-process pool (the reference's run_bench scheme): {its} iterations in "
+                         f"{wall:.1f} s wall"}
     line = {
         "metric": METRIC, "value": value, "unit": "problem-iterations/s", "n_gpus": world, "steps": 1,
         "warmup": args.warmup, "ms_per_step": tim["kernel_ms"], "higher_is_better": True, "scaling": "weak",

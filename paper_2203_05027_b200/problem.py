@@ -100,6 +100,9 @@ class ConeSpec:
             object.__setattr__(self, "_tuple", tuple(int(s) for s in block_sizes))
             object.__setattr__(self, "_array", None)
 
+    def __reduce__(self):   # picklable despite the immutable __setattr__ (process pools)
+        return (ConeSpec, (self._array if self._array is not None else self._tuple,))
+
     @property
     def block_sizes(self) -> tuple:
         if self._tuple is None:

@@ -98,3 +98,16 @@ def test_conespec_compact_orthant_matches_tuple():
     assert big == ConeSpec((1,) * 1000)
     assert big.block_sizes == (1,) * 1000 and big.dim == 1000
     assert ConeSpec((4, 4)).sizes_array().tolist() == [4, 4]
+
+
+def test_problem_types_pickle():
+    """Problems travel to process pools (the reference's run_bench scheme)."""
+    import pickle
+
+    from paper_2203_05027_b200 import ConeSpec, GenSpec, generate
+
+    p = generate(GenSpec(20, 40, 0.1, "socp4", seed=1))
+    q = pickle.loads(pickle.dumps(p))
+    assert q.cones.block_sizes == p.cones.block_sizes and q.A.nnz == p.A.nnz
+    assert (q.A.vals == p.A.vals).all() and (q.b == p.b).all()
+    assert pickle.loads(pickle.dumps(ConeSpec((1, 2, 3)))).block_sizes == (1, 2, 3)
