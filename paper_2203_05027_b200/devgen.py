@@ -153,7 +153,12 @@ def generate_device_shard(m: int, n: int, density: float, cone_kind: str, seed: 
     rows, cols = pos // n, pos % n
     del pos
     vals = torch.randn(o, generator=g_local, device=dev, dtype=torch.float64)
-    vals[vals == 0.0] = 1.0
+    while True:   # zeros are redrawn (generate.py:121-124)
+        zero = vals == 0.0
+        nz = int(zero.sum())
+        if nz == 0:
+            break
+        vals[zero] = torch.randn(nz, generator=g_local, device=dev, dtype=torch.float64)
     if cone_kind == "lp":
         sizes = np.ones(n, dtype=np.int64)
         unit = 1
