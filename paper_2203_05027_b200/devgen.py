@@ -153,7 +153,7 @@ def generate_device_shard(m: int, n: int, density: float, cone_kind: str, seed: 
     rows, cols = pos // n, pos % n
     del pos
     vals = torch.randn(o, generator=g_local, device=dev, dtype=torch.float64)
-    while True:   # zeros are redrawn (generate.py:121-124)
+    while True:   # zeros are redrawn (generate.py:112-117)
         zero = vals == 0.0
         nz = int(zero.sum())
         if nz == 0:
