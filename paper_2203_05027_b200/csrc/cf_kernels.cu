@@ -93,6 +93,7 @@ struct Layout {
     static constexpr int kUnroll = pass::kUnroll;   // gathers in flight per thread
     static constexpr int kMinBlocks = pass::kMinBlocks;
     static constexpr int kWideUnroll = 16;          // ... when the tiles cannot fill the GPU (Wide<P>)
+    static constexpr int kMediumUnroll = 6;         // ... when they fill it in one wave of 4 CTAs/SM
     __device__ __forceinline__ const double* gvec() const { return g_; }
     static constexpr int kVals = 0;
     __device__ __forceinline__ void load_async(int, double*) const {}
@@ -307,6 +308,7 @@ struct ColIter : ColVecs {
 struct ColReport : ColVecs {
     static constexpr int kUnroll = 8;      // 8 report accumulators per thread
     static constexpr int kWideUnroll = 8;
+    static constexpr int kMediumUnroll = 4;
     static constexpr int kMinBlocks = 2;   // (more registers; runs once per check_every iterations)
     double* part;          // [kReportFieldsCol][kGroups][gridDim.x]
     double d2, dmx, s2, smx, amx, cx, cg, nf;
@@ -619,32 +621,41 @@ int persistent_grid(int n_tiles) {
     return n_tiles < g ? (n_tiles > 0 ? n_tiles : 1) : g;
 }
 
-// Small problems: when the tiles cannot fill the GPU, the pass is latency-bound
-// and each lane keeps more gathers in flight (fewer, wider batches) instead.
+// Small and mid-size problems are latency-bound: every tile should get its own
+// CTA in ONE wave, and each lane then keeps more gathers in flight instead.
+//   n_tiles <= 2 x 148: Wide   (16 in flight, 2 CTAs / SM)
+//   n_tiles <= 4 x 148: Medium ( 6 in flight, 4 CTAs / SM)
+//   otherwise         : the persistent default (3 in flight, 6 CTAs / SM)
 template <class P>
 struct Wide : P {
     static constexpr int kUnroll = P::kWideUnroll;
     static constexpr int kMinBlocks = 2;
 };
-constexpr int kWideTiles = 148 * 4;   // below this many tiles a pass runs as Wide<P>
+template <class P>
+struct Medium : P {
+    static constexpr int kUnroll = P::kMediumUnroll;
+    static constexpr int kMinBlocks = 4;
+};
+constexpr int kWideTiles = 148 * 2;
+constexpr int kMediumTiles = 148 * 4;
+
+template <class Q>
+int launch_variant(const Q& pol, const pass::Jds& L, const pass::Tiles& T, const int32_t* done, cudaStream_t st,
+                   int* grid_out) {
+    const int grid = persistent_grid<Q>(T.n_tiles);
+    if (grid_out) *grid_out = grid;
+    CF_CUDA(launch_pdl(pass::k_pass<Q>, (unsigned)grid, (unsigned)pass::kPThreads, pass::smem_bytes<Q>(), st, pol, L,
+                       T, done));
+    return CF_OK;
+}
 
 template <class P>
 int launch_pass(const P& pol, const pass::Jds& L, const pass::Tiles& T, const int32_t* done, cudaStream_t st,
                 int* grid_out = nullptr) {
     if (T.n_tiles == 0) return CF_OK;
-    if (T.n_tiles < kWideTiles) {
-        const Wide<P> w{pol};
-        const int grid = persistent_grid<Wide<P>>(T.n_tiles);
-        if (grid_out) *grid_out = grid;
-        CF_CUDA(launch_pdl(pass::k_pass<Wide<P>>, (unsigned)grid, (unsigned)pass::kPThreads,
-                           pass::smem_bytes<Wide<P>>(), st, w, L, T, done));
-        return CF_OK;
-    }
-    const int grid = persistent_grid<P>(T.n_tiles);
-    if (grid_out) *grid_out = grid;
-    CF_CUDA(launch_pdl(pass::k_pass<P>, (unsigned)grid, (unsigned)pass::kPThreads, pass::smem_bytes<P>(), st, pol, L,
-                       T, done));
-    return CF_OK;
+    if (T.n_tiles <= kWideTiles) return launch_variant(Wide<P>{pol}, L, T, done, st, grid_out);
+    if (T.n_tiles <= kMediumTiles) return launch_variant(Medium<P>{pol}, L, T, done, st, grid_out);
+    return launch_variant(pol, L, T, done, st, grid_out);
 }
 
 template <int MODE>
@@ -899,7 +910,7 @@ int launch_row_diag(cf_plan* p) {
     return CF_OK;
 }
 
-int max_col_report_ctas() { return std::max(persistent_grid<ColReport>(1 << 30), kWideTiles); }
+int max_col_report_ctas() { return std::max(persistent_grid<ColReport>(1 << 30), kMediumTiles); }
 
 // ---------------------------------------------------------------- row-sharded building blocks
 namespace {
