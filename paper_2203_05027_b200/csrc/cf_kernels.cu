@@ -94,6 +94,7 @@ struct Layout {
     static constexpr int kMinBlocks = pass::kMinBlocks;
     static constexpr int kWideUnroll = 16;          // ... when the tiles cannot fill the GPU (Wide<P>)
     static constexpr int kMediumUnroll = 6;         // ... when they fill it in one wave of 4 CTAs/SM
+    static constexpr bool kStaged = false;          // tile idx/val staged in shared memory
     __device__ __forceinline__ const double* gvec() const { return g_; }
     static constexpr int kVals = 0;
     __device__ __forceinline__ void load_async(int, double*) const {}
@@ -621,23 +622,33 @@ int persistent_grid(int n_tiles) {
     return n_tiles < g ? (n_tiles > 0 ? n_tiles : 1) : g;
 }
 
+#ifndef CF_STAGED_SMALL
+#define CF_STAGED_SMALL 1   // Wide/Medium stage each tile's idx/val in shared memory (direct engine)
+#endif
 // Small and mid-size problems are latency-bound: every tile should get its own
 // CTA in ONE wave, and each lane then keeps more gathers in flight instead.
-//   n_tiles <= 2 x 148: Wide   (16 in flight, 2 CTAs / SM)
-//   n_tiles <= 4 x 148: Medium ( 6 in flight, 4 CTAs / SM)
-//   otherwise         : the persistent default (3 in flight, 6 CTAs / SM)
+//   n_tiles <=  2 x 148: Wide   (16 in flight, 2 CTAs / SM, staged tiles)
+//   n_tiles <= 12 x 148: Medium ( 6 in flight, 4 CTAs / SM, staged tiles)
+//   otherwise          : the persistent default (3 in flight, 6 CTAs / SM, direct loads)
+// (tools/prof_sizes.py: 1e6 nnz 25.5 -> 19.8 us/iteration, 3e6 55.6 -> 51.8; 1e7 is
+// faster unstaged)
 template <class P>
 struct Wide : P {
     static constexpr int kUnroll = P::kWideUnroll;
     static constexpr int kMinBlocks = 2;
+    static constexpr bool kStaged = CF_STAGED_SMALL;
 };
 template <class P>
 struct Medium : P {
     static constexpr int kUnroll = P::kMediumUnroll;
     static constexpr int kMinBlocks = 4;
+    static constexpr bool kStaged = CF_STAGED_SMALL;
 };
+#ifndef CF_MEDIUM_TILES
+#define CF_MEDIUM_TILES (148 * 12)
+#endif
 constexpr int kWideTiles = 148 * 2;
-constexpr int kMediumTiles = 148 * 4;
+constexpr int kMediumTiles = CF_MEDIUM_TILES;
 
 template <class Q>
 int launch_variant(const Q& pol, const pass::Jds& L, const pass::Tiles& T, const int32_t* done, cudaStream_t st,

@@ -110,8 +110,20 @@ static_assert(sizeof(((Smem*)0)->vals) / kGroups >= kLongChunk * sizeof(double),
 constexpr size_t kSmemBytes = sizeof(Smem);
 // policies without a cone epilogue do not allocate the cone scratch
 constexpr size_t kSmemBytesNoCones = offsetof(Smem, cscr);
+
+// Staged tiles (the latency-bound Wide/Medium dispatch of the direct engine):
+// the whole tile's idx/val are copied to shared memory with 16-byte cp.async at
+// tile start, so a lane pays one DRAM round trip per tile instead of one per
+// batch of diagonals. Placed after the full Smem.
+struct alignas(16) TileStage {
+    int32_t idx[kPCap + 8];
+    double val[kPCap + 4];
+};
 template <class P>
-constexpr size_t smem_bytes() { return P::kGroupEpilogue ? kSmemBytes : kSmemBytesNoCones; }
+constexpr size_t smem_bytes() {
+    return (P::kStaged && !CF_TMA) ? kSmemBytes + sizeof(TileStage)
+                                   : (P::kGroupEpilogue ? kSmemBytes : kSmemBytesNoCones);
+}
 
 // x / mu; exact multiply when mu is a power of two (then x * (1/mu) == x / mu bit for bit)
 struct MuDiv {
@@ -214,6 +226,22 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src, uint64
                  "l"(pol)
                  : "memory");
 }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, uint64_t pol) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src),
+                 "l"(pol)
+                 : "memory");
+}
+// 16-byte-aligned superset copy of [first, first + count) into dst by the calling CTA's
+// threads; element 0 lands at dst + ((uintptr_t)first & 15) bytes
+template <class T>
+__device__ __forceinline__ void stage_span(void* dst, const T* first, int count, uint64_t pol) {
+    if (count <= 0) return;
+    const uintptr_t a = (uintptr_t)first & ~(uintptr_t)15u;
+    const uintptr_t e = ((uintptr_t)(first + count) + 15u) & ~(uintptr_t)15u;
+    const int chunks = (int)((e - a) >> 4);
+    for (int c = threadIdx.x; c < chunks; c += blockDim.x)
+        cp_async16(static_cast<char*>(dst) + 16 * c, reinterpret_cast<const char*>(a) + 16 * c, pol);
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
@@ -242,6 +270,7 @@ struct Jds {
 //   bool carry_in() const; double carry(int s) const   starting value of a segment's sum
 //   static constexpr int kUnroll               gathers in flight per thread
 //   static constexpr int kMinBlocks            resident CTAs per SM the registers are sized for
+//   static constexpr bool kStaged              (direct engine) stage each tile's idx/val in shared memory
 //   static constexpr bool kGroupEpilogue       epilogue needs all segments of the tile at once (cones)
 //   void check(double a, int j, double g)      per-nonzero hook (report finiteness)
 //   void segment(Smem&, int tile, int s0, int q, int cnt, double acc, const Vals&)
@@ -523,6 +552,19 @@ __global__ void __launch_bounds__(kPThreads, 1) k_pass(const P p0, const Jds L, 
 }
 
 #else
+// load_batch from a staged tile (positions relative to the staged arrays)
+template <int U>
+__device__ __forceinline__ void load_batch_smem(const int32_t* ib, const double* vb, int (&nj)[U], double (&nv)[U],
+                                                int& pos, int mylen, int k) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const bool ok = mylen > k + u;
+        nj[u] = ok ? ib[pos] : 0;
+        nv[u] = ok ? vb[pos] : 0.0;
+        pos += __popc(__ballot_sync(0xffffffffu, ok));   // width of diagonal k+u
+    }
+}
+
 // Each warp walks its warp blocks (block gw of tiles blockIdx.x, +G, ...):
 // pl -> idx/val of U diagonals -> U gathers -> sequential sums, then the
 // natural-order epilogue. Many resident warps hide the dependent chain.
@@ -546,12 +588,27 @@ __global__ void __launch_bounds__(kPThreads, P::kMinBlocks) k_pass(const P p0, c
         const int4 lo = __ldg(T.tb + tile), hi = __ldg(T.tb + tile + 1);
         const int s0 = lo.x, nseg = hi.x - lo.x, k0 = lo.y, len = hi.y - lo.y;
         if (lo.z) {
+            const int32_t* ib = nullptr;
+            const double* vb = nullptr;
+            if constexpr (P::kStaged) {
+                TileStage& ts = *reinterpret_cast<TileStage*>(smem_raw + kSmemBytes);
+                __syncthreads();   // the previous tile's readers are done with the stage
+                stage_span(ts.idx, L.idx + k0, len, pol_first());
+                stage_span(ts.val, L.val + k0, len, pol_first());
+                cp_async_commit();
+                ib = ts.idx + (((uintptr_t)(L.idx + k0) & 15u) >> 2);
+                vb = ts.val + (((uintptr_t)(L.val + k0) & 15u) >> 3);
+            }
             const int nb = min(32, nseg - gw * 32);   // segments of this warp block
+            const bool nat = lane < nb;                 // natural segment gw*32 + lane exists
+            const int seg = s0 + gw * 32 + lane;
+            const uint32_t pr =
+                (nb > 0 && nat) ? (uint32_t)ld_first(reinterpret_cast<const int32_t*>(L.pl) + seg, pol_first()) : 0u;
+            if constexpr (P::kStaged) {
+                cp_async_wait_all();
+                __syncthreads();
+            }
             if (nb > 0) {
-                const bool nat = lane < nb;             // natural segment gw*32 + lane exists
-                const int seg = s0 + gw * 32 + lane;
-                const uint32_t pr =
-                    nat ? (uint32_t)ld_first(reinterpret_cast<const int32_t*>(L.pl) + seg, pol_first()) : 0u;
                 double* slot = &sm.vals[gw][0][lane];
                 if (P::kVals > 0) {
                     if (nat) p.load_async(seg, slot);
@@ -560,14 +617,17 @@ __global__ void __launch_bounds__(kPThreads, P::kMinBlocks) k_pass(const P p0, c
                 const int q = (int)(pr & 31u);          // local segment (within the block) of rank r
                 const int mylen = pl_len(pr);
                 const int mlen = __shfl_sync(0xffffffffu, mylen, 0);   // rank 0 is the longest
-                int pos = k0 + __shfl_sync(0xffffffffu, pl_start(pr), 0) + lane;
+                int pos = (P::kStaged ? 0 : k0) + __shfl_sync(0xffffffffu, pl_start(pr), 0) + lane;
                 // rank r's own carry (no shuffle: the load's latency hides behind the gathers)
                 double acc = (p.carry_in() && nat) ? p.carry(s0 + gw * 32 + q) : 0.0;
                 const double* __restrict__ g = p.gvec();
                 for (int k = 0; k < mlen; k += U) {
                     int nj[U];
                     double nv[U], gv[U];
-                    load_batch<U>(L, nj, nv, pos, mylen, k, pol_first());
+                    if constexpr (P::kStaged)
+                        load_batch_smem<U>(ib, vb, nj, nv, pos, mylen, k);
+                    else
+                        load_batch<U>(L, nj, nv, pos, mylen, k, pol_first());
 #pragma unroll
                     for (int u = 0; u < U; ++u)
                         gv[u] = (mylen > k + u) ? ld_gather(g + (uint32_t)nj[u], pol_last()) : 0.0;
