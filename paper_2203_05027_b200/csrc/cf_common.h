@@ -142,7 +142,17 @@ struct cf_plan {
     int32_t n_panels = 1;
     int64_t panel_cols = 0;
     std::vector<int64_t> row_panel_tile;   // first row tile of each panel (n_panels+1)
-    std::vector<int32_t> col_tile_start;   // first column of each column tile (host copy, col_tiles+1)
+    std::vector<int32_t> col_tile_start;   // first segment of each column tile (host copy, col_tiles+1)
+    // column-pass row bands: with h larger than ~48 MB the column pass runs band by band
+    // (segment = band*n + col, each band's slice of h L2-resident), carrying the partial
+    // column sums in atcarry; only the last band runs the epilogue
+    int32_t n_bands = 1;
+    int64_t band_rows = 0;
+    std::vector<int64_t> col_band_tile;    // first column tile of each band (n_bands+1)
+    cf::DevBuf<double> atcarry;            // partial A^T h / A^T lam between bands (n)
+    // banded CSC, only while the column JDS is built (released afterwards)
+    cf::DevBuf<int32_t> bcolptr, browidx;
+    cf::DevBuf<double> bvalc;
     cf::DevBuf<double> wbuf;           // w = x+ - delta/mu for big-cone columns
 
     // iterate state: x, z, delta (n); lam, h (m); br = b - r (m) when kept

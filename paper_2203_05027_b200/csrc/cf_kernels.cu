@@ -171,27 +171,49 @@ struct RowSpmv : Layout {
     }
 };
 
-// x = A^T y (apply_V . apply_Ut)
+// x = A^T y (apply_V . apply_Ut), band by band with y as the carry.
 struct ColSpmv : Layout {
+    int64_t seg_off;       // band * n
+    bool last;             // (unused: every band writes y)
+    bool has_carry;        // band > 0: the sum continues from y[j]
     double* y;
+    __device__ __forceinline__ bool carry_in() const { return has_carry; }
+    __device__ __forceinline__ double carry(int s) const { return y[s - seg_off]; }
     __device__ __forceinline__ void segment(Smem&, int, int s0, int q, int, double acc, const Vals&) {
-        y[s0 + q] = acc;
+        y[s0 + q - seg_off] = acc;
     }
 };
 
-// Column-pass epilogue vectors: x, z, delta, c of column j.
+// Column-pass state shared by the column policies: the band (segment = band*n + col),
+// the carry of the partial column sums between bands, and the epilogue vectors
+// x, z, delta, c of column j (read by the last band only).
 struct ColVecs : Layout {
     const double* x_in;
     const double* z_in;
     const double* d_in;
     const double* c;
+    int64_t seg_off;       // band * n
+    bool last;             // last band: run the epilogue
+    bool has_carry;        // band > 0: the sum continues from carry_buf[j]
+    double* carry_buf;     // partial sums between bands (the plan's atcarry)
+    const int32_t* colptr; // bands > 1: canonical column pointers (the full column count)
     static constexpr int kVals = 4;
-    __device__ __forceinline__ void load_async(int j, double* slot) const {
+    __device__ __forceinline__ bool carry_in() const { return has_carry; }
+    __device__ __forceinline__ double carry(int s) const { return carry_buf[s - seg_off]; }
+    __device__ __forceinline__ void load_async(int s, double* slot) const {
+        if (!last) return;
         const uint64_t pf = pass::pol_first();
+        const int64_t j = s - seg_off;
         pass::cp_async8(slot, x_in + j, pf);
         pass::cp_async8(slot + 32, z_in + j, pf);
         pass::cp_async8(slot + 64, d_in + j, pf);
         pass::cp_async8(slot + 96, c + j, pf);
+    }
+    // a band before the last only hands its partial sum on
+    __device__ __forceinline__ bool carry_out(int64_t j, double acc) const {
+        if (last) return false;
+        pass::st_hint(carry_buf + j, acc, pass::pol_last());
+        return true;
     }
 };
 
@@ -222,7 +244,9 @@ struct ColIter : ColVecs {
     pass::MuDiv div;
     int32_t cs;            // kWarpCones: the uniform cone size
     __device__ __forceinline__ void segment(Smem& sm, int, int s0, int q, int cnt, double ath, const Vals& vv) {
-        const int j = s0 + q;
+        const int j = (int)(s0 + q - seg_off);
+        if (carry_out(j, ath)) return;
+        if (colptr) cnt = colptr[j + 1] - colptr[j];   // banded: the band holds part of the column
         const double fv = cnt < pass::kFvTab ? sm.fvtab[cnt] : 1.0 / (1.0 + (double)cnt);   // uv.py:82
         const double xj = vv.v[0], zj = vv.v[1], dj = vv.v[2], cj = vv.v[3];
         const double dm = div(dj);
@@ -271,7 +295,9 @@ struct ColIter : ColVecs {
             sm.cscr[gi][2][q] = dj;
         }
     }
-    __device__ __forceinline__ void group(Smem& sm, int tile, int s0, int nseg) {
+    __device__ __forceinline__ void group(Smem& sm, int tile, int sseg0, int nseg) {
+        if (!last) return;
+        const int s0 = (int)(sseg0 - seg_off);   // first column of the tile
         const int gi = pass::group_id();
         const double* sxp = sm.cscr[gi][0];
         const double* sw = sm.cscr[gi][1];
@@ -313,7 +339,8 @@ struct ColReport : ColVecs {
     static constexpr int kMinBlocks = 2;   // (more registers; runs once per check_every iterations)
     double* part;          // [kReportFieldsCol][kGroups][gridDim.x]
     double d2, dmx, s2, smx, amx, cx, cg, nf;
-    __device__ __forceinline__ void segment(Smem&, int, int, int, int, double atl, const Vals& vv) {
+    __device__ __forceinline__ void segment(Smem&, int, int s0, int q, int, double atl, const Vals& vv) {
+        if (carry_out(s0 + q - seg_off, atl)) return;
         const double xj = vv.v[0], zj = vv.v[1], dj = vv.v[2], cj = vv.v[3];
         const double dual = atl + cj;
         const double stat = dual - dj;
@@ -327,6 +354,7 @@ struct ColReport : ColVecs {
         if (!isfinite(xj) || !isfinite(zj) || !isfinite(dj)) nf = 1.0;
     }
     __device__ __forceinline__ void finish(Smem& sm) {
+        if (!last) return;   // (uniform over the grid)
         const int G = gridDim.x;
         const double vals[8] = {d2, dmx, s2, smx, amx, cx, cg, nf};
         const bool is_sum[8] = {true, false, true, false, false, true, false, false};
@@ -581,7 +609,10 @@ pass::Tiles row_panel_tiles(const cf_plan* p, int panel) {
     const int64_t t0 = p->row_panel_tile[panel], t1 = p->row_panel_tile[panel + 1];
     return pass::Tiles{p->row_tb.p + t0, (int32_t)(t1 - t0)};
 }
-pass::Tiles col_tiles(const cf_plan* p) { return pass::Tiles{p->col_tb.p, (int32_t)p->col_tiles}; }
+pass::Tiles col_band_tiles(const cf_plan* p, int band) {
+    const int64_t t0 = p->col_band_tile[band], t1 = p->col_band_tile[band + 1];
+    return pass::Tiles{p->col_tb.p + t0, (int32_t)(t1 - t0)};
+}
 pass::Jds row_jds(const cf_plan* p) { return pass::Jds{p->rj_idx.p, p->rj_val.p, p->rj_pl.p}; }
 pass::Jds col_jds(const cf_plan* p) { return pass::Jds{p->cj_idx.p, p->cj_val.p, p->cj_pl.p}; }
 
@@ -669,6 +700,28 @@ int launch_pass(const P& pol, const pass::Jds& L, const pass::Tiles& T, const in
     return launch_variant(pol, L, T, done, st, grid_out);
 }
 
+// the band fields of a column policy (seg_off/last/has_carry are set per launch)
+template <class P>
+void col_vecs_bands(const cf_plan* p, P& c) {
+    c.carry_buf = p->atcarry.p;
+    c.colptr = p->n_bands > 1 ? p->colptr.p : nullptr;
+}
+
+// run a column policy band by band (segment = band*n + col); the last band runs the
+// epilogue, earlier bands carry their partial sums (grid_out: the last band's grid)
+template <class P>
+int launch_col_bands(cf_plan* p, P pol, const int32_t* done, int64_t* nl, int* grid_out = nullptr) {
+    const int B = p->n_bands;
+    for (int b = 0; b < B; ++b) {
+        pol.seg_off = (int64_t)b * p->n;
+        pol.last = (b == B - 1);
+        pol.has_carry = b > 0;
+        CF_TRY(launch_pass(pol, col_jds(p), col_band_tiles(p, b), done, p->stream, pol.last ? grid_out : nullptr));
+        if (nl) ++*nl;
+    }
+    return CF_OK;
+}
+
 template <int MODE>
 ColIter<MODE> col_iter(cf_plan* p, const IterOpts& opt) {
     ColIter<MODE> c{};
@@ -689,6 +742,7 @@ ColIter<MODE> col_iter(cf_plan* p, const IterOpts& opt) {
     c.mu = opt.mu;
     c.div = pass::make_mudiv(opt.mu);
     c.cs = p->warp_cone;
+    col_vecs_bands(p, c);
     return c;
 }
 
@@ -739,13 +793,12 @@ int launch_iteration(cf_plan* p, const IterOpts& opt, const int32_t* done, int64
     }
     if (p->n > 0) {
         if (p->all_unit) {
-            CF_TRY(launch_pass(col_iter<kLP>(p, opt), col_jds(p), col_tiles(p), done, p->stream));
+            CF_TRY(launch_col_bands(p, col_iter<kLP>(p, opt), done, &nl));
         } else if (p->warp_cone) {
-            CF_TRY(launch_pass(col_iter<kWarpCones>(p, opt), col_jds(p), col_tiles(p), done, p->stream));
+            CF_TRY(launch_col_bands(p, col_iter<kWarpCones>(p, opt), done, &nl));
         } else {
-            CF_TRY(launch_pass(col_iter<kGroupCones>(p, opt), col_jds(p), col_tiles(p), done, p->stream));
+            CF_TRY(launch_col_bands(p, col_iter<kGroupCones>(p, opt), done, &nl));
         }
-        ++nl;
         if (!p->all_unit && p->n_big > 0) {
             BigConeArgs g{};
             g.big_cone = p->big_cone.p;
@@ -801,14 +854,21 @@ int launch_spmv_cols(cf_plan* p, const double* y, double* x) {
     ColSpmv c{};
     c.g_ = y;
     c.y = x;
-    return launch_pass(c, col_jds(p), col_tiles(p), nullptr, p->stream);
+    return launch_col_bands(p, c, nullptr, nullptr);
 }
 
 int launch_spmv_cols_range(cf_plan* p, const double* y, double* x, int64_t col_lo, int64_t col_hi) {
     if (p->n == 0 || p->col_tile_start.size() < 2 || col_hi <= col_lo) return CF_OK;
-    const auto& ts = p->col_tile_start;   // col_tiles + 1 entries, the last = n
+    if (p->n_bands > 1) {
+        // the bands' tile boundaries differ, so a column's bands could not be kept in order
+        // across ranges: the first range runs the whole banded pass, the others are no-ops
+        return col_lo == 0 ? launch_spmv_cols(p, y, x) : CF_OK;
+    }
+    // the tiles that start in [col_lo, col_hi)
+    const auto& ts = p->col_tile_start;   // first column of each tile, + the end (n)
     const int64_t t0 = std::lower_bound(ts.begin(), ts.end() - 1, (int32_t)col_lo) - ts.begin();
-    const int64_t t1 = std::lower_bound(ts.begin(), ts.end() - 1, (int32_t)std::min<int64_t>(col_hi, p->n)) - ts.begin();
+    const int64_t t1 =
+        std::lower_bound(ts.begin(), ts.end() - 1, (int32_t)std::min<int64_t>(col_hi, p->n)) - ts.begin();
     if (t1 <= t0) return CF_OK;
     ColSpmv c{};
     c.g_ = y;
@@ -847,9 +907,9 @@ int launch_report(cf_plan* p, double mu, bool ax_ready, const cf_config* cfg, in
         c.d_in = p->delta.p;
         c.c = p->c.p;
         c.part = p->part_col.p;
-        CF_TRY(launch_pass(c, col_jds(p), col_tiles(p), done, p->stream, &g_col));
+        col_vecs_bands(p, c);
+        CF_TRY(launch_col_bands(p, c, done, &nl, &g_col));
         g_col *= pass::kGroups;  // one partial per (field, group, CTA)
-        ++nl;
     }
     FinalizeArgs f{};
     f.part_row = p->part_row.p;

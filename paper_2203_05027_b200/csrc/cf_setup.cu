@@ -92,6 +92,22 @@ __global__ void k_ptr_from_sorted(const SegT* seg_of, int64_t o, int64_t nseg, i
     }
 }
 
+// column-pass segment of each canonical entry: band(row) * n + col
+__global__ void k_band_keys(const int32_t* rowidx, const int32_t* colof, int64_t o, int64_t n, int64_t band_rows,
+                            uint64_t* keys) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < o; k += (int64_t)gridDim.x * blockDim.x)
+        keys[k] = (uint64_t)(rowidx[k] / band_rows) * (uint64_t)n + (uint64_t)colof[k];
+}
+// gather the canonical CSC entries into banded order
+__global__ void k_fill_banded(const int32_t* perm, const int32_t* rowidx, const double* valc, int64_t o,
+                              int32_t* browidx, double* bvalc) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < o; k += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t s = perm[k];
+        browidx[k] = rowidx[s];
+        bvalc[k] = valc[s];
+    }
+}
+
 // row-pass segment of each canonical entry: panel(col) * m + row
 __global__ void k_row_keys(const int32_t* rowidx, const int32_t* colof, int64_t o, int64_t m, int64_t panel_cols,
                            uint64_t* keys) {
@@ -304,19 +320,22 @@ int build_tiles(cf_plan* p, const int64_t* sizes, int64_t nb) {
         t_last = now;
     };
     const int64_t nsr = (int64_t)p->n_panels * m;
+    const int B = p->n_bands;
+    const int64_t nsc = (int64_t)B * n;   // column-pass segments (band*n + col)
+    const int32_t* cptr_dev = B > 1 ? p->bcolptr.p : p->colptr.p;
     std::vector<int64_t> rlong, clong;
     CF_TRY(long_segments(p, p->rowptr.p, nsr, rlong));
-    CF_TRY(long_segments(p, p->colptr.p, n, clong));
+    CF_TRY(long_segments(p, cptr_dev, nsc, clong));
     // both pointer arrays in (cached) pinned memory
     PinnedScratch scratch;
-    int32_t* rp = static_cast<int32_t*>(scratch.get((size_t)(nsr + 1 + n + 1) * 4));
+    int32_t* rp = static_cast<int32_t*>(scratch.get((size_t)(nsr + 1 + nsc + 1) * 4));
     if (!rp) {
         set_error("build_tiles: pinned host allocation failed");
         return CF_ENOMEM;
     }
-    int32_t* cp = rp + nsr + 1;
+    int32_t* cpall = rp + nsr + 1;
     CF_CUDA(cudaMemcpyAsync(rp, p->rowptr.p, (size_t)(nsr + 1) * 4, cudaMemcpyDeviceToHost, p->stream));
-    CF_CUDA(cudaMemcpyAsync(cp, p->colptr.p, (size_t)(n + 1) * 4, cudaMemcpyDeviceToHost, p->stream));
+    CF_CUDA(cudaMemcpyAsync(cpall, cptr_dev, (size_t)(nsc + 1) * 4, cudaMemcpyDeviceToHost, p->stream));
     CF_CUDA(cudaStreamSynchronize(p->stream));
     tick("ptr D2H + long segments");
     // rows, panel by panel (segment = panel*m + row)
@@ -332,11 +351,26 @@ int build_tiles(cf_plan* p, const int64_t* sizes, int64_t nb) {
     tile_table(rp, rstarts, nsr, rtb);
     p->row_tiles = (int64_t)rtb.size() - 1;
     tick("row tiles (host)");
-    // columns (cone-aligned when the cone is not the orthant)
+    // columns, band by band: the bands before the last only carry partial sums (plain
+    // tiles); the last band runs the epilogue (cone-aligned tiles when not the orthant).
+    // cp below is the LAST band's pointer array in column coordinates.
     std::vector<int64_t> cstarts;
     std::vector<int32_t> tcone, tbig, big, cone_ptr;
+    p->col_band_tile.assign(B + 1, 0);
+    for (int bd = 0; bd + 1 < B; ++bd) {
+        p->col_band_tile[bd] = (int64_t)cstarts.size();
+        tile_starts(cpall, (int64_t)bd * n, (int64_t)(bd + 1) * n, clong, cstarts);
+    }
+    p->col_band_tile[B - 1] = (int64_t)cstarts.size();
+    const int64_t last_off = (int64_t)(B - 1) * n;
+    const int32_t* cp = cpall + last_off;
+    const size_t last_first = cstarts.size();
+    std::vector<int64_t> clong_last;   // the last band's long segments in column coordinates
+    for (int64_t s : clong)
+        if (s >= last_off) clong_last.push_back(s - last_off);
+    std::vector<int64_t> lstarts;
     if (p->all_unit) {
-        tile_starts(cp, 0, n, clong, cstarts);
+        tile_starts(cp, 0, n, clong_last, lstarts);
     } else {
         cone_ptr.resize(nb + 1);
         int64_t col = 0;
@@ -349,9 +383,9 @@ int build_tiles(cf_plan* p, const int64_t* sizes, int64_t nb) {
         while (q < nb) {
             const int64_t c0 = cone_ptr[q];
             if (sizes[q] > kSmallCone) {
-                const size_t before = cstarts.size();
-                tile_starts(cp, c0, c0 + sizes[q], clong, cstarts);
-                for (size_t t = before; t < cstarts.size(); ++t) {
+                const size_t before = lstarts.size();
+                tile_starts(cp, c0, c0 + sizes[q], clong_last, lstarts);
+                for (size_t t = before; t < lstarts.size(); ++t) {
                     tcone.push_back((int32_t)q);
                     tbig.push_back((int32_t)big.size());
                 }
@@ -366,9 +400,9 @@ int build_tiles(cf_plan* p, const int64_t* sizes, int64_t nb) {
                 return true;
             };
             if (!cone_ok(q)) {  // cone with a very long column: treat like a big cone (k_big_cone)
-                const size_t before = cstarts.size();
-                tile_starts(cp, c0, c0 + sizes[q], clong, cstarts);
-                for (size_t t = before; t < cstarts.size(); ++t) {
+                const size_t before = lstarts.size();
+                tile_starts(cp, c0, c0 + sizes[q], clong_last, lstarts);
+                for (size_t t = before; t < lstarts.size(); ++t) {
                     tcone.push_back((int32_t)q);
                     tbig.push_back((int32_t)big.size());
                 }
@@ -379,15 +413,18 @@ int build_tiles(cf_plan* p, const int64_t* sizes, int64_t nb) {
             while (q1 < nb && sizes[q1] <= kSmallCone && cone_ptr[q1] + sizes[q1] - c0 <= kTileSeg &&
                    cp[cone_ptr[q1] + sizes[q1]] - cp[c0] <= kTileNnz && cone_ok(q1))
                 ++q1;
-            cstarts.push_back(c0);
+            lstarts.push_back(c0);
             tcone.push_back((int32_t)q);
             tbig.push_back(-1);
             q = q1;
         }
         tcone.push_back((int32_t)nb);
     }
+    for (int64_t s : lstarts) cstarts.push_back(s + last_off);
+    p->col_band_tile[B] = (int64_t)cstarts.size();
+    (void)last_first;
     std::vector<int4> ctb;
-    tile_table(cp, cstarts, n, ctb);
+    tile_table(cpall, cstarts, nsc, ctb);
     p->col_tile_start.resize(ctb.size());
     for (size_t t = 0; t < ctb.size(); ++t) p->col_tile_start[t] = ctb[t].x;
     tick("col tiles (host)");
@@ -401,7 +438,18 @@ int build_tiles(cf_plan* p, const int64_t* sizes, int64_t nb) {
         if (uniform) p->warp_cone = (int32_t)s;
     }
     CF_TRY(build_jds(p, p->rowptr.p, p->colidx.p, p->valr.p, rtb, nsr, p->row_tb, p->rj_idx, p->rj_val, p->rj_pl));
-    CF_TRY(build_jds(p, p->colptr.p, p->rowidx.p, p->valc.p, ctb, n, p->col_tb, p->cj_idx, p->cj_val, p->cj_pl));
+    if (B > 1) {
+        CF_TRY(build_jds(p, p->bcolptr.p, p->browidx.p, p->bvalc.p, ctb, nsc, p->col_tb, p->cj_idx, p->cj_val,
+                         p->cj_pl));
+        CF_CUDA(cudaStreamSynchronize(p->stream));
+        p->bcolptr.release();
+        p->browidx.release();
+        p->bvalc.release();
+        CF_TRY(p->atcarry.alloc(n));
+    } else {
+        CF_TRY(build_jds(p, p->colptr.p, p->rowidx.p, p->valc.p, ctb, n, p->col_tb, p->cj_idx, p->cj_val,
+                         p->cj_pl));
+    }
     if (verbose) CF_CUDA(cudaStreamSynchronize(p->stream));
     tick("jds build (device)");
     if (p->all_unit) {
@@ -513,6 +561,16 @@ int build(cf_plan* p, const int64_t* rows, const int64_t* cols, const double* va
         if (p->batch_mode) panels = 1;                                // the batched kernel reads plain CSR
         p->n_panels = panels;
         p->panel_cols = std::max<int64_t>(1, (n + panels - 1) / panels);
+        // row bands of the column pass: each band's slice of h must stay L2-resident
+        double band_mb = panel_mb;
+        if (const char* env = getenv("CF_BAND_MB")) band_mb = atof(env);
+        int bands = (int)std::ceil(8.0 * (double)m / (band_mb * 1048576.0));
+        if (bands < 1) bands = 1;
+        if (bands > 64) bands = 64;
+        if ((int64_t)bands * n >= (int64_t)INT32_MAX) bands = 1;
+        if (p->batch_mode || o == 0) bands = 1;
+        p->n_bands = bands;
+        p->band_rows = std::max<int64_t>(1, (m + bands - 1) / bands);
     }
     CF_TRY(p->rowptr.alloc((size_t)p->n_panels * m + 1));
     CF_TRY(p->colidx.alloc(o));
@@ -574,6 +632,29 @@ int build(cf_plan* p, const int64_t* rows, const int64_t* cols, const double* va
         k_fill_csr<<<grid1d(o), 256, 0, st>>>(p->csr2csc.p, colof.p, p->valc.p, o, p->colidx.p, p->valr.p);
         k_ptr_from_sorted<uint64_t><<<grid1d(o), 256, 0, st>>>(rb.Current(), o, nseg_rows, p->rowptr.p);
         CF_LAUNCHED();
+        if (p->n_bands > 1) {
+            // ---- banded CSC for the column pass: stable sort of canonical entries by (row band,
+            //      column); inside a segment the entries keep canonical (row) order
+            const int64_t nseg_cols = (int64_t)p->n_bands * n;
+            CF_TRY(p->bcolptr.alloc(nseg_cols + 1));
+            CF_TRY(p->browidx.alloc(o));
+            CF_TRY(p->bvalc.alloc(o));
+            CF_CUDA(cudaMemsetAsync(p->bcolptr.p, 0, (nseg_cols + 1) * 4, st));
+            k_band_keys<<<grid1d(o), 256, 0, st>>>(p->rowidx.p, colof.p, o, n, p->band_rows, k_a.p);
+            k_iota<<<grid1d(o), 256, 0, st>>>(i_a.p, o);
+            CF_LAUNCHED();
+            cub::DoubleBuffer<uint64_t> bb(k_a.p, k_b.p);
+            cub::DoubleBuffer<int32_t> bp(i_a.p, i_b.p);
+            const int band_bits = bits_for((uint64_t)std::max<int64_t>(nseg_cols - 1, 1));
+            size_t tmp3 = 0;
+            CF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp3, bb, bp, (int64_t)o, 0, band_bits, st));
+            if (tmp3 > std::max(tmp_bytes, tmp2)) CF_TRY(tmp.alloc(tmp3));
+            CF_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp3, bb, bp, (int64_t)o, 0, band_bits, st));
+            k_fill_banded<<<grid1d(o), 256, 0, st>>>(bp.Current(), p->rowidx.p, p->valc.p, o, p->browidx.p,
+                                                     p->bvalc.p);
+            k_ptr_from_sorted<uint64_t><<<grid1d(o), 256, 0, st>>>(bb.Current(), o, nseg_cols, p->bcolptr.p);
+            CF_LAUNCHED();
+        }
         CF_CUDA(cudaStreamSynchronize(st));  // scratch buffers are released at scope exit
     } else {
         if (chk->nonfinite_b || chk->nonfinite_c) {

@@ -380,3 +380,50 @@ def test_warp_cone_epilogue_equals_group_epilogue(monkeypatch):
     group = solve(p, cfg)
     assert np.array_equal(warp.x, group.x) and np.array_equal(warp.lam, group.lam)
     assert [r.iter for r in warp.trace] == [r.iter for r in group.trace]
+
+
+@pytest.mark.parametrize("case", ITERATE_CASES)
+def test_column_bands_match_reference(case, monkeypatch):
+    """Row bands of the column pass (CF_BAND_MB: h split into L2-sized slices, partial
+    column sums carried between bands) keep A^T y bit-identical and the iterates and
+    reports within the parity tolerance, for every cone layout and warm starts."""
+    import torch
+
+    monkeypatch.setenv("CF_BAND_MB", "0.0005")   # 512 bytes of h per band -> several bands
+    d = load_golden(f"iterates_{case}.npz")
+    p = problem_from(d)
+    f = oracle.build_factors(p.A)
+    y = np.random.default_rng(9).standard_normal(f.m)
+    mu = float(d["mu"])
+    with _plan(p) as plan:
+        aty = torch.empty(f.n, dtype=torch.float64, device="cuda")
+        plan.apply_At(_device_vec(y).data_ptr(), aty.data_ptr())
+        np.testing.assert_array_equal(aty.cpu().numpy(), oracle.apply_V(f, oracle.apply_Ut(f, y)))
+        plan.set_state(mu, init_from(d))
+        done = 0
+        for k in d["keep"]:
+            plan.iterate(mu, int(k) - done)
+            done = int(k)
+            st = plan.get_state()
+            for key in STATE_KEYS:
+                assert rel_err(st[key], d[f"k{k}_{key}"]) <= ITER_TOL, (case, int(k), key)
+            rep = plan.report(mu)
+            want = d[f"k{k}_report"]
+            for i, fld in enumerate(REPORT_FIELDS[1:], start=1):
+                assert _scalar_rel(rep[fld], want[i]) <= REPORT_TOL, (case, int(k), fld)
+
+
+def test_column_bands_solve_bit_identical(monkeypatch):
+    """A banded solve returns exactly what the unbanded one does (same sums, same order)."""
+    from paper_2203_05027_b200 import GenSpec, SolverConfig, generate, solve
+
+    for kind in ("lp", "socp4"):
+        q = generate(GenSpec(400, 800, 0.02, kind, seed=12))
+        cfg = SolverConfig(max_iters=500)
+        monkeypatch.setenv("CF_BAND_MB", "0.001")
+        banded = solve(q, cfg)
+        monkeypatch.setenv("CF_BAND_MB", "1000")
+        ref = solve(q, cfg)
+        np.testing.assert_array_equal(banded.x, ref.x)
+        np.testing.assert_array_equal(banded.lam, ref.lam)
+        assert banded.trace == ref.trace
