@@ -427,3 +427,36 @@ def test_column_bands_solve_bit_identical(monkeypatch):
         np.testing.assert_array_equal(banded.x, ref.x)
         np.testing.assert_array_equal(banded.lam, ref.lam)
         assert banded.trace == ref.trace
+
+
+@pytest.mark.parametrize("shape", ["no_nonzeros", "1x1", "one_dense_row", "one_dense_column", "empty_rows_cols"])
+def test_degenerate_shapes_match_oracle(shape):
+    """Shapes at the edges of the tiling: no nonzeros, 1x1, one dense row / column (long
+    tiles), and many empty rows and columns; solve() equals the oracle's loop."""
+    from paper_2203_05027_b200 import ConeSpec, ProblemInstance, SolverConfig, TripletMatrix, solve
+
+    rng = np.random.default_rng(13)
+    if shape == "no_nonzeros":
+        m, n, rows, cols = 3, 5, [], []
+    elif shape == "1x1":
+        m, n, rows, cols = 1, 1, [0], [0]
+    elif shape == "one_dense_row":
+        m, n = 4, 5000
+        rows, cols = [0] * n, list(range(n))
+    elif shape == "one_dense_column":
+        m, n = 5000, 3
+        rows, cols = list(range(m)), [1] * m
+    else:
+        m, n = 400, 900
+        rows = list(rng.choice(np.arange(0, m, 3), 600))
+        cols = list(rng.choice(np.arange(0, n, 4), 600))
+        key = sorted(set(zip(rows, cols)))
+        rows, cols = [r for r, _ in key], [c for _, c in key]
+    vals = rng.standard_normal(len(rows)) + 0.1
+    a = TripletMatrix(m, n, np.array(rows, dtype=np.int64), np.array(cols, dtype=np.int64), vals)
+    p = ProblemInstance(a, rng.standard_normal(m), np.abs(rng.standard_normal(n)), ConeSpec((1,) * n))
+    cfg = SolverConfig(max_iters=400, check_every=25)
+    res = solve(p, cfg)
+    ox, olam, otrace, _ = oracle.solve(p, cfg)
+    assert res.report.iter == otrace[-1]["iter"] and res.report.status == otrace[-1]["status"]
+    assert rel_err(res.x, ox) <= 1e-9 and rel_err(res.lam, olam) <= 1e-9
