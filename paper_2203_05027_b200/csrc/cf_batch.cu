@@ -22,7 +22,13 @@
 namespace cf {
 namespace {
 
-constexpr int kBT = 256;   // threads per problem CTA
+#ifndef CF_BATCH_THREADS
+#define CF_BATCH_THREADS 256
+#endif
+#ifndef CF_BATCH_MINB
+#define CF_BATCH_MINB 4   // 4 problems per SM (C4: 114M -> 120M problem-iterations/s; the spills sit in the report)
+#endif
+constexpr int kBT = CF_BATCH_THREADS;   // threads per problem CTA
 
 struct BatchArgs {
     int32_t P;
@@ -123,7 +129,7 @@ __device__ __forceinline__ void project_block_b(const double* w, int q, double* 
     }
 }
 
-__global__ void __launch_bounds__(kBT, 3) k_batch(const BatchArgs a) {
+__global__ void __launch_bounds__(kBT, CF_BATCH_MINB) k_batch(const BatchArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int CM = a.cap_m, CN = a.cap_n, CO = a.cap_o;
     // shared-memory carve-up (doubles first)
