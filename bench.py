@@ -35,7 +35,6 @@ from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -225,7 +224,7 @@ def run_ours(args, spec, rank, world, local_rank):
     import torch
 
     from paper_2203_05027_b200 import SolverConfig
-    from paper_2203_05027_b200.api import norms, run_plan, solve
+    from paper_2203_05027_b200.api import norms, solve
     from paper_2203_05027_b200.devgen import generate_device, to_host_problem
     from paper_2203_05027_b200.engine import config_struct
 

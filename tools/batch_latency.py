@@ -1,7 +1,6 @@
 """Per-iteration latency of the batched kernel: one problem (one CTA) forced to max_iters."""
 import os
 import sys
-import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 

@@ -7,7 +7,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
 def main():
-    import torch
+    import torch  # noqa: F401  (initialises CUDA before the plan is created)
 
     from bench import CONFIGS
     from paper_2203_05027_b200 import SolverConfig
