@@ -122,3 +122,28 @@ def test_column_range_pass_covers_every_column_once(nccl_group):
     torch.cuda.synchronize()
     assert torch.equal(parts, full)
     plan.close()
+
+
+def test_sharded_with_column_bands_matches_single_plan(nccl_group, monkeypatch):
+    """Banded plans (h split into row bands) through the sharded driver: the range pass
+    falls back to the whole banded pass and the result equals the single-plan iteration."""
+    import torch
+
+    from paper_2203_05027_b200 import SolverConfig
+    from paper_2203_05027_b200.devgen import generate_device_shard
+    from paper_2203_05027_b200.sharded import CudaRankBackend, run_sharded
+
+    monkeypatch.setenv("CF_BAND_MB", "0.05")
+    st = torch.cuda.current_stream()
+    plan, rc, cc, cs, bn, cn, cones = generate_device_shard(30_000, 60_000, 3e-4, "lp", 2, 0, 1,
+                                                            stream=st.cuda_stream)
+    iters = 40
+    plan.set_state(1.0, None, export=False)
+    plan.iterate(1.0, iters)
+    ref = plan.get_state(want_yg=False)
+    plan.set_state(1.0, None, export=False)
+    be = CudaRankBackend.from_plan(plan, cc[0], cc[1], cs, cones)
+    cfg = SolverConfig(max_iters=iters, check_every=25, eps_prim=0.0, eps_dual=0.0, eps_gap=0.0)
+    res = run_sharded(be, rc, cc, cfg, bn, cn)
+    assert np.array_equal(res.x, ref["x"]) and np.array_equal(res.lam, ref["lam"])
+    be.close()
