@@ -37,3 +37,18 @@ def test_run_bench_matches_reference_rows():
     assert len(csv.splitlines()) == len(rows) + 1
     extra = bench_csv(rows, extra=True).splitlines()[0].split(",")
     assert extra[-3:] == ["iters_per_s", "hbm_gbs", "roofline_frac"]
+
+
+def test_concurrent_large_jobs_equal_serial():
+    """Jobs above the batch threshold solved 4 at a time (threads, one plan and stream
+    each) give exactly the serial rows."""
+    from paper_2203_05027_b200 import SolverConfig
+    from paper_2203_05027_b200.benchrun import BenchJob, run_bench
+    from paper_2203_05027_b200.instances import GenSpec
+
+    cfg = SolverConfig(max_iters=2000)
+    jobs = [BenchJob(i, GenSpec(300, 900, 0.1, "lp" if i % 2 else "socp4", seed=i), cfg) for i in range(6)]
+    par = run_bench(jobs, workers=4, batch_max_nnz=1000)
+    ser = run_bench(jobs, workers=1, batch_max_nnz=1000)
+    keys = ("instance_id", "iters", "prim_res_2", "dual_res_2", "gap", "cone_gap", "status")
+    assert [[r[k] for k in keys] for r in par] == [[r[k] for k in keys] for r in ser]
