@@ -244,17 +244,65 @@ def solve(p, cfg: SolverConfig | None = None, init: SolverState | None = None) -
         plan.close()
 
 
-def solve_batch(problems, cfg: SolverConfig | None = None, trace: bool = True, timing: dict | None = None) -> list:
+# shared memory of the batched kernel for a batch whose largest dimensions are m, n, o, k
+# (cf_batch.cu batch_smem) and the per-CTA opt-in limit of sm_100
+_BATCH_SMEM_LIMIT = 227 * 1024
+
+
+def _batch_smem(m: int, n: int, o: int, k: int) -> int:
+    return 8 * (2 * o + 7 * m + 7 * n + 32) + 4 * (2 * o + m + 1 + n + 1 + k + 1) + 16
+
+
+def solve_batch(problems, cfg: SolverConfig | None = None, trace: bool = True, timing: dict | None = None,
+                workers: int = 8) -> list:
     """Solve many independent problems at once: ``[solve(p, cfg) for p in problems]``.
 
-    The reference batches with a process pool over ``solve`` (bench.py:96-106);
-    here every problem is solved by one CTA that keeps it in shared memory
-    (csrc/cf_batch.cu, SURVEY config C4), with per-problem termination. Each
-    result is the SolveResult ``solve(p, cfg)`` returns (same iterates,
-    statuses and iteration counts; ``trace=False`` keeps only the final report).
-    Problems too large for one CTA's shared memory raise ValueError (use solve).
-    ``timing``, if given, receives the device time of the solve kernel.
+    The reference batches with a process pool over ``solve`` (bench.py:96-106).
+    Here the problems that fit one CTA's shared memory run in the batched
+    kernel (csrc/cf_batch.cu, SURVEY config C4): one CTA per problem, every
+    iterate on chip, per-problem termination. The others are solved
+    ``workers`` at a time, each with its own plan and CUDA stream. Each result
+    is the SolveResult ``solve(p, cfg)`` returns (same iterates, statuses and
+    iteration counts; ``trace=False`` keeps only the final report), in input
+    order. ``timing``, if given, receives the device time of the batched kernel.
     """
+    problems = list(problems)
+    # greedy: smallest first while the batch's dimension caps still fit
+    dims = []
+    for i, p in enumerate(problems):
+        k = len(cone_sizes_array(p.cones)) if _host_shapes_ok(p) else 0
+        dims.append((int(p.A.num_rows), int(p.A.num_cols), int(np.asarray(p.A.vals).size), k, i))
+    order = sorted(dims, key=lambda t: _batch_smem(*t[:4]))
+    fit, cm, cn, co, ck = [], 0, 0, 0, 0
+    for m, n, o, k, i in order:
+        nm, nn, no, nk = max(cm, m), max(cn, n), max(co, o), max(ck, k)
+        if _batch_smem(nm, nn, no, nk) > _BATCH_SMEM_LIMIT:
+            break
+        fit.append(i)
+        cm, cn, co, ck = nm, nn, no, nk
+    rest = sorted(set(range(len(problems))) - set(fit))
+    out = [None] * len(problems)
+    if fit:
+        fit.sort()
+        for i, r in zip(fit, _solve_batch_kernel([problems[i] for i in fit], cfg, trace, timing, ids=fit)):
+            out[i] = r
+    if rest:
+        from concurrent.futures import ThreadPoolExecutor
+
+        def one(i):
+            r = solve(problems[i], cfg)
+            return r if trace else r._replace(trace=(r.report,))
+
+        with ThreadPoolExecutor(max_workers=max(1, int(workers))) as pool:
+            for i, r in zip(rest, pool.map(one, rest)):
+                out[i] = r
+    return out
+
+
+def _solve_batch_kernel(problems, cfg: SolverConfig | None = None, trace: bool = True,
+                        timing: dict | None = None, ids=None) -> list:
+    """The batched kernel on problems that fit one CTA each (see solve_batch); ids: the
+    problems' positions in the caller's list (error messages)."""
     import ctypes
 
     from . import _lib
@@ -269,7 +317,7 @@ def solve_batch(problems, cfg: SolverConfig | None = None, trace: bool = True, t
     for i, p in enumerate(problems):
         if not _host_shapes_ok(p):
             rep = validate(p)
-            raise ValueError(f"problem {i}: invalid problem: " + "; ".join(rep.violations[:3]))
+            raise ValueError(f"problem {ids[i] if ids else i}: invalid problem: " + "; ".join(rep.violations[:3]))
     ms = np.array([p.A.num_rows for p in problems], dtype=np.int64)
     ns = np.array([p.A.num_cols for p in problems], dtype=np.int64)
     row_off = np.concatenate(([0], np.cumsum(ms))).astype(np.int64)
@@ -305,7 +353,7 @@ def solve_batch(problems, cfg: SolverConfig | None = None, trace: bool = True, t
         for i, p in enumerate(problems):
             rep = validate(p)
             if not rep.ok:
-                raise ValueError(f"problem {i}: invalid problem: " + "; ".join(rep.violations[:3]))
+                raise ValueError(f"problem {ids[i] if ids else i}: invalid problem: " + "; ".join(rep.violations[:3]))
     check(rc, "cf_batch_solve")
     if timing is not None:
         timing["kernel_ms"] = el.value
@@ -317,7 +365,7 @@ def solve_batch(problems, cfg: SolverConfig | None = None, trace: bool = True, t
             if status == "running" and rep.iter == cfg.max_iters:
                 status = "max_iters"
             if status != d["status"]:
-                raise RuntimeError(f"problem {i}: device termination ({d['status']}) disagrees with "
+                raise RuntimeError(f"problem {ids[i] if ids else i}: device termination ({d['status']}) disagrees with "
                                    f"check_termination ({status}) at iteration {rep.iter}")
             return replace(rep, status=status)
 

@@ -460,3 +460,19 @@ def test_degenerate_shapes_match_oracle(shape):
     ox, olam, otrace, _ = oracle.solve(p, cfg)
     assert res.report.iter == otrace[-1]["iter"] and res.report.status == otrace[-1]["status"]
     assert rel_err(res.x, ox) <= 1e-9 and rel_err(res.lam, olam) <= 1e-9
+
+
+def test_solve_batch_mixes_kernel_and_concurrent_solves():
+    """Problems too large for one CTA are solved alongside the batched kernel (threads with
+    their own plans); every result equals solve() on that problem, in input order."""
+    from paper_2203_05027_b200 import GenSpec, SolverConfig, generate, solve, solve_batch
+
+    probs = [generate(GenSpec(60, 120, 0.05, "lp", seed=1)), generate(GenSpec(900, 2000, 0.01, "lp", seed=2)),
+             generate(GenSpec(60, 120, 0.05, "socp4", seed=3)), generate(GenSpec(1000, 3000, 0.01, "socp4", seed=4))]
+    cfg = SolverConfig(max_iters=3000)
+    got = solve_batch(probs, cfg)
+    for p, r in zip(probs, got):
+        ref = solve(p, cfg)
+        np.testing.assert_array_equal(r.x, ref.x)
+        np.testing.assert_array_equal(r.lam, ref.lam)
+        assert r.trace == ref.trace
