@@ -404,6 +404,8 @@ def run_sharded_bench(args, spec, rank, world, local_rank):
     scale = args.c5_scale
     m, n = int(spec["m"] * scale), int(spec["n"] * scale)
     stream = torch.cuda.current_stream()
+    if args.c5_mode == "cols":
+        return run_col_sharded_bench(args, spec, rank, world, m, n, scale, stream, own_group)
     plan, row_cuts, col_cuts, c_slice, bn, cn, cones = generate_device_shard(
         m, n, spec["density"] / scale, spec["cone_kind"], args.seed, rank, world, stream=stream.cuda_stream)
     be = CudaRankBackend.from_plan(plan, col_cuts[rank], col_cuts[rank + 1], c_slice, cones)
@@ -457,6 +459,61 @@ def _oracle_iters(p, cfg, budget_s):
 
     _, _, tr, _ = oracle.solve(p, cfg, max_wall_s=budget_s)
     return tr[-1]["iter"]
+
+
+def run_col_sharded_bench(args, spec, rank, world, m, n, scale, stream, own_group):
+    """C5 with A's columns split over the ranks: one all-reduce of the m-vector A x per iteration."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2203_05027_b200 import SolverConfig
+    from paper_2203_05027_b200.devgen import generate_device_colshard
+    from paper_2203_05027_b200.sharded import CudaColBackend, run_col_sharded
+
+    def build():
+        plan, col_cuts, bn, cn = generate_device_colshard(m, n, spec["density"] / scale, spec["cone_kind"],
+                                                          args.seed, rank, world, stream=stream.cuda_stream)
+        return CudaColBackend(None, plan=plan), col_cuts, bn, cn
+
+    be, col_cuts, bn, cn = build()
+    o_t = torch.tensor([float(be.plan.o)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(o_t)
+    run_col_sharded(be, col_cuts, SolverConfig(max_iters=max(args.warmup, 1), check_every=25, eps_prim=0.0,
+                                               eps_dual=0.0, eps_gap=0.0), bn, cn, gather_result=False)
+    be.close()
+    be, col_cuts, bn, cn = build()
+    cfg = SolverConfig(max_iters=args.steps, check_every=25, eps_prim=0.0, eps_dual=0.0, eps_gap=0.0)
+    dist.barrier()
+    torch.cuda.synchronize()
+    tim = {}
+    res = run_col_sharded(be, col_cuts, cfg, bn, cn, timing=tim, gather_result=False)
+    torch.cuda.synchronize()
+    assert tim["iters"] == args.steps and res.report.status == "max_iters", (tim, res.report)
+    ms = torch.tensor([tim["loop_ms"]], dtype=torch.float64, device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms)
+    value = args.steps / (ms / 1000.0)
+    o_total = int(o_t.item())
+    row_b, col_b = algorithmic_bytes(m, n, o_total)
+    peak, src = hbm_peak()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (per-rank GPU generator, reference recipe)",
+            "config": {"workload": spec["workload"] if scale == 1.0 else f"C5 structure scaled by {scale}: m={m} n={n}",
+                       "m": m, "n": n, "o": o_total,
+                       "parallelism": f"column-sharded x{world} (NCCL all-reduce of A x)"},
+            "gpu_launches": args.steps * 4 + (args.steps // 25) * 5,
+            "iteration_roofline": {"bytes_per_iteration_total": row_b + col_b,
+                                   "achieved_per_gpu_GBs": (row_b + col_b) / world / (ms / args.steps / 1000) / 1e9,
+                                   "peak": peak, "peak_source": src},
+        }
+        print(json.dumps(line), flush=True)
+    be.close()
+    if own_group:
+        dist.destroy_process_group()
+    return 0
 
 
 def run_batch(args, spec, rank, world):
@@ -536,6 +593,8 @@ def main():
     ap.add_argument("--e2e-max-iters", type=int, default=0)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--c5-scale", type=float, default=1.0, help="shrink C5 (m, n) by this factor (same nnz/row)")
+    ap.add_argument("--c5-mode", choices=("rows", "cols"), default="rows",
+                    help="C5: split A's rows (exchange n-vectors) or columns (all-reduce the m-vector A x)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

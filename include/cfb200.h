@@ -212,6 +212,9 @@ int cf_batch_solve(int64_t n_problems, const int64_t* row_off, const int64_t* co
 #define CF_VEC_AX 5
 #define CF_VEC_B 6
 #define CF_VEC_C 7
+#define CF_VEC_FU 8
+#define CF_VEC_DB 9
+#define CF_VEC_BR 10   /* b - r (report iterations) */
 /* device pointer and length of one of the plan's vectors */
 int cf_plan_vector(cf_plan* plan, int which, double** ptr, int64_t* len);
 /* per-column nonzero counts of the plan (n doubles, device) */
@@ -219,6 +222,24 @@ int cf_plan_column_counts(cf_plan* plan, double* cnt_dev);
 /* the row pass of one iteration (y_update + lam/gamma updates, solver.py:179-183,194-195)
  * with the plan's current x; report=1 also keeps A x for cf_plan_row_parts */
 int cf_plan_row_step(cf_plan* plan, double mu, int report);
+/* Column-sharded building blocks (A's columns split over the ranks, all rows on every
+ * rank; the exchange is one all-reduce of the m-vector A x): */
+/* the plan's row norms d_i = sum a_ik^2 (uv.py:81 before the reciprocal) and max |a_ik|
+ * over its own entries (device arrays of m); with A's columns split over ranks the
+ * driver all-reduces them (sum / max) and sets them back, so fu, d*b and the
+ * finiteness check use the whole rows */
+int cf_plan_row_norms(cf_plan* plan, double* d_dev, double* amax_dev);
+int cf_plan_set_row_norms(cf_plan* plan, const double* d_dev, const double* amax_dev);
+/* the column pass of one iteration on the plan's columns (x_update + z_update + delta
+ * update, solver.py:168-176,186-188,196) from the plan's h */
+int cf_plan_col_step(cf_plan* plan, double mu);
+/* y = A x on the plan (rows; the partial A_r x_r of a column slice), no host sync */
+int cf_apply_A_async(cf_plan* plan, const double* x_dev, double* y_dev);
+/* y_update + lam/gamma updates (solver.py:179-183,194-195) of every row of the plan from the
+ * FULL A x in the plan's ax buffer (CF_VEC_AX, the all-reduced partials):
+ * r = fu (d b + A x), lam += mu (r - b), h = (b - r) - lam / mu; report=1 keeps b - r for
+ * cf_plan_row_parts */
+int cf_plan_row_update(cf_plan* plan, double mu, int report);
 /* row part of compute_report over the plan's rows: out = {sum (Ax-b)^2, max|Ax-b|,
  * max|Ax|, sum b*lam, nonfinite(lam)} (host array of 5) */
 int cf_plan_row_parts(cf_plan* plan, double* out5);

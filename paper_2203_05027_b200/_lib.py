@@ -115,6 +115,11 @@ SIGNATURES = {
                                c_int64, POINTER(CfChecks), _D]),
     "cf_plan_set_profiling": (c_int, [_P, c_int]),
     "cf_plan_sync": (c_int, [_P]),
+    "cf_plan_col_step": (c_int, [_P, c_double]),
+    "cf_plan_row_norms": (c_int, [_P, _P, _P]),
+    "cf_plan_set_row_norms": (c_int, [_P, _P, _P]),
+    "cf_apply_A_async": (c_int, [_P, _P, _P]),
+    "cf_plan_row_update": (c_int, [_P, c_double, c_int]),
     "cf_coneprob_open": (c_int, [c_char_p, c_char_p, c_int64, POINTER(c_void_p)]),
     "cf_coneprob_close": (None, [_P]),
     "cf_coneprob_header": (c_int, [_P, _I64, _I64, c_char_p, c_int64]),

@@ -410,6 +410,9 @@ int cf_plan_vector(cf_plan* p, int which, double** ptr, int64_t* len) {
         case CF_VEC_AX: *ptr = p->ax.p; *len = p->m; break;
         case CF_VEC_B: *ptr = p->b.p; *len = p->m; break;
         case CF_VEC_C: *ptr = p->c.p; *len = p->n; break;
+        case CF_VEC_FU: *ptr = p->fu.p; *len = p->m; break;
+        case CF_VEC_DB: *ptr = p->db.p; *len = p->m; break;
+        case CF_VEC_BR: *ptr = p->br.p; *len = p->m; break;
         default: set_error("cf_plan_vector: unknown vector"); return CF_EINVAL;
     }
     return CF_OK;
@@ -431,6 +434,46 @@ int cf_plan_row_step(cf_plan* p, double mu, int report) {
     opt.report = report != 0;
     CF_TRY(launch_row_only(p, opt));
     p->br_valid = opt.report || p->keep_br;
+    return CF_OK;
+}
+
+int cf_plan_col_step(cf_plan* p, double mu) {
+    CF_TRY(check_plan(p, "cf_plan_col_step"));
+    CF_TRY(check_mu(mu, "cf_plan_col_step"));
+    // the column half of launch_iteration; the row half happens elsewhere (column sharding)
+    IterOpts opt;
+    opt.mu = mu;
+    CF_TRY(launch_col_only(p, opt));
+    return CF_OK;
+}
+
+int cf_apply_A_async(cf_plan* p, const double* x_dev, double* y_dev) {
+    CF_TRY(check_plan(p, "cf_apply_A_async"));
+    CF_TRY(launch_spmv_rows(p, x_dev, y_dev));
+    return CF_OK;
+}
+
+int cf_plan_row_norms(cf_plan* p, double* d_dev, double* amax_dev) {
+    CF_TRY(check_plan(p, "cf_plan_row_norms"));
+    CF_TRY(launch_row_norms(p, d_dev, amax_dev));
+    CF_CUDA(cudaStreamSynchronize(p->stream));
+    return CF_OK;
+}
+
+int cf_plan_set_row_norms(cf_plan* p, const double* d_dev, const double* amax_dev) {
+    CF_TRY(check_plan(p, "cf_plan_set_row_norms"));
+    CF_TRY(launch_set_row_diag(p, d_dev, amax_dev));
+    CF_CUDA(cudaStreamSynchronize(p->stream));
+    return CF_OK;
+}
+
+int cf_plan_row_update(cf_plan* p, double mu, int report) {
+    CF_TRY(check_plan(p, "cf_plan_row_update"));
+    CF_TRY(check_mu(mu, "cf_plan_row_update"));
+    // the plan's ax holds the FULL A x (the all-reduced partials of the column slices)
+    CF_TRY(launch_row_update(p->m, p->ax.p, p->b.p, p->fu.p, p->db.p, p->lam.p, p->h.p,
+                             (report || p->keep_br) ? p->br.p : nullptr, mu, p->stream));
+    p->br_valid = report || p->keep_br;
     return CF_OK;
 }
 

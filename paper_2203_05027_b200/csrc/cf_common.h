@@ -201,6 +201,14 @@ struct IterOpts {
     const double* ccorr = nullptr;
     const double* rcorr = nullptr;
 };
+// the column pass of one iteration (all row bands, cones, big cones)
+int launch_col_only(cf_plan* p, const IterOpts& opt, const int32_t* done = nullptr, int64_t* launches = nullptr);
+// row norms of the plan's entries / fu, d*b, amax from given row norms (column sharding)
+int launch_row_norms(cf_plan* p, double* dout, double* amax);
+int launch_set_row_diag(cf_plan* p, const double* din, const double* amax_in);
+// RowIter's row epilogue from a full A x (column-sharded driver)
+int launch_row_update(int64_t m, const double* ax, const double* b, const double* fu, const double* db, double* lam,
+                      double* h, double* br, double mu, cudaStream_t st);
 // the row pass of one iteration (all column panels)
 int launch_row_only(cf_plan* p, const IterOpts& opt, const int32_t* done = nullptr, int64_t* launches = nullptr);
 // one iteration (col pass + cones + row pass); returns kernel launches issued via *launches

@@ -598,6 +598,33 @@ __global__ void k_row_diag(const int32_t* rowptr, const double* valr, const doub
     }
 }
 
+// the row sums d_i = sum_k a_ik^2 (canonical order) and max |a_ik| of the plan's entries
+__global__ void k_row_norms(const int32_t* rowptr, const double* valr, double* dout, double* amax, int64_t m,
+                            int32_t panels) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        double d = 0.0, am = 0.0;
+        for (int32_t pn = 0; pn < panels; ++pn) {
+            const int64_t seg = pn * m + i;
+            for (int p = rowptr[seg]; p < rowptr[seg + 1]; ++p) {
+                d = d + valr[p] * valr[p];
+                am = fmax(am, fabs(valr[p]));
+            }
+        }
+        dout[i] = d;
+        amax[i] = am;
+    }
+}
+// fu = 1/(1+d) (uv.py:81), d*b and amax from given (e.g. all-reduced) row norms
+__global__ void k_set_row_diag(const double* din, const double* amax_in, const double* b, double* fu, double* db,
+                               double* amax, int64_t m) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        const double d = din[i];
+        fu[i] = 1.0 / (1.0 + d);
+        db[i] = d * b[i];
+        amax[i] = amax_in[i];
+    }
+}
+
 inline int grid_for(int64_t work, int threads) {
     int64_t g = (work + threads - 1) / threads;
     if (g < 1) g = 1;
@@ -791,6 +818,16 @@ int launch_iteration(cf_plan* p, const IterOpts& opt, const int32_t* done, int64
         p->prof_used += 3;
         CF_CUDA(cudaEventRecord(e_a, p->stream));
     }
+    CF_TRY(launch_col_only(p, opt, done, &nl));
+    if (p->profiling) CF_CUDA(cudaEventRecord(e_b, p->stream));
+    CF_TRY(launch_row_only(p, opt, done, &nl));
+    if (p->profiling) CF_CUDA(cudaEventRecord(e_c, p->stream));
+    if (launches) *launches += nl;
+    return CF_OK;
+}
+
+int launch_col_only(cf_plan* p, const IterOpts& opt, const int32_t* done, int64_t* launches) {
+    int64_t nl = 0;
     if (p->n > 0) {
         if (p->all_unit) {
             CF_TRY(launch_col_bands(p, col_iter<kLP>(p, opt), done, &nl));
@@ -813,9 +850,6 @@ int launch_iteration(cf_plan* p, const IterOpts& opt, const int32_t* done, int64
             ++nl;
         }
     }
-    if (p->profiling) CF_CUDA(cudaEventRecord(e_b, p->stream));
-    CF_TRY(launch_row_only(p, opt, done, &nl));
-    if (p->profiling) CF_CUDA(cudaEventRecord(e_c, p->stream));
     if (launches) *launches += nl;
     return CF_OK;
 }
@@ -981,6 +1015,21 @@ int launch_row_diag(cf_plan* p) {
     return CF_OK;
 }
 
+int launch_row_norms(cf_plan* p, double* dout, double* amax) {
+    if (p->m == 0) return CF_OK;
+    k_row_norms<<<grid_for(p->m, 128), 128, 0, p->stream>>>(p->rowptr.p, p->valr.p, dout, amax, p->m, p->n_panels);
+    CF_LAUNCHED();
+    return CF_OK;
+}
+
+int launch_set_row_diag(cf_plan* p, const double* din, const double* amax_in) {
+    if (p->m == 0) return CF_OK;
+    k_set_row_diag<<<grid_for(p->m, 128), 128, 0, p->stream>>>(din, amax_in, p->b.p, p->fu.p, p->db.p, p->amax.p,
+                                                                p->m);
+    CF_LAUNCHED();
+    return CF_OK;
+}
+
 int max_col_report_ctas() { return std::max(persistent_grid<ColReport>(1 << 30), kMediumTiles); }
 
 // ---------------------------------------------------------------- row-sharded building blocks
@@ -1054,11 +1103,33 @@ __global__ void k_row_parts_final(const double* part_row, int G, double* out) {
         out[4] = f4;
     }
 }
+// the row epilogue of RowIter (y_update + lam/gamma, solver.py:179-183,194-195) from a
+// full A x: the column-sharded driver's row step
+__global__ void k_row_update(int64_t m, const double* ax, const double* b, const double* fu, const double* db,
+                             double* lam, double* h, double* br, double mu, pass::MuDiv div) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        const double bi = b[i];
+        const double r = fu[i] * (db[i] + ax[i]);
+        const double ln = lam[i] + mu * (r - bi);
+        const double bmr = bi - r;
+        lam[i] = ln;
+        h[i] = bmr - div(ln);
+        if (br) br[i] = bmr;
+    }
+}
 __global__ void k_counts(const int32_t* colptr, int64_t n, double* cnt) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
         cnt[j] = (double)(colptr[j + 1] - colptr[j]);
 }
 }  // namespace
+
+int launch_row_update(int64_t m, const double* ax, const double* b, const double* fu, const double* db, double* lam,
+                      double* h, double* br, double mu, cudaStream_t st) {
+    if (m == 0) return CF_OK;
+    k_row_update<<<grid_for(m, 256), 256, 0, st>>>(m, ax, b, fu, db, lam, h, br, mu, pass::make_mudiv(mu));
+    CF_LAUNCHED();
+    return CF_OK;
+}
 
 int launch_col_update(int64_t n, const double* ath, const double* cnt, const double* c, double* x, double* z,
                       double* delta, double mu, int64_t n_blocks, const int32_t* cone_ptr, cudaStream_t st) {

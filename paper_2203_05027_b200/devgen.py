@@ -20,7 +20,8 @@ import numpy as np
 
 from .engine import DevicePlan
 
-__all__ = ["DeviceInstance", "generate_device", "generate_device_shard", "c2_spec", "c3_spec", "to_host_problem"]
+__all__ = ["DeviceInstance", "generate_device", "generate_device_shard", "generate_device_colshard", "c2_spec",
+           "c3_spec", "to_host_problem"]
 
 
 @dataclass
@@ -198,6 +199,69 @@ def generate_device_shard(m: int, n: int, density: float, cone_kind: str, seed: 
     c_norms = (float(c.abs().max()), math.sqrt(float((c * c).sum())))
     cone_slice = None if unit == 1 else (np.arange(lo, hi + 1, 4) - lo).astype(np.int32)
     return plan, row_cuts, col_cuts, c[lo:hi].clone(), b_norms, c_norms, cone_slice
+
+
+def generate_device_colshard(m: int, n: int, density: float, cone_kind: str, seed: int, rank: int, world: int,
+                             group=None, stream: int | None = None):
+    """Rank ``rank``'s column slice of a column-sharded instance (all rows), built on its GPU.
+
+    Columns [c0, c1) (cone-aligned) get their share of the nonzeros; the primal witness and
+    the dual draw are shared (same seed on every rank), so b = sum_r A_r Proj_K(x)_r (an
+    all-reduce) and c_r = Proj_K(s)_r - A_r^T lam reproduce the generator recipe of
+    generate.py:103-140 for the whole matrix. Returns (plan, col_cuts, b_norms, c_norms)."""
+    import math
+
+    import torch
+    import torch.distributed as dist
+
+    dev = torch.device("cuda")
+    unit = 1 if cone_kind == "lp" else 4
+    step = -(-n // world)
+    step = -(-step // unit) * unit
+    col_cuts = [min(n, r * step) for r in range(world)] + [n]
+    c0, c1 = col_cuts[rank], col_cuts[rank + 1]
+    nl = c1 - c0
+    o = int(round(m * nl * density))
+    g_local = torch.Generator(device=dev)
+    g_local.manual_seed(int(seed) * 1000003 + rank)
+    g_shared = torch.Generator(device=dev)
+    g_shared.manual_seed(int(seed))
+    pos = _distinct_positions(torch, g_local, m * nl, o, dev)
+    rows, cols = pos // nl, pos % nl
+    del pos
+    vals = torch.randn(o, generator=g_local, device=dev, dtype=torch.float64)
+    while True:   # zeros are redrawn (generate.py:112-117)
+        zero = vals == 0.0
+        nz = int(zero.sum())
+        if nz == 0:
+            break
+        vals[zero] = torch.randn(nz, generator=g_local, device=dev, dtype=torch.float64)
+    sizes = np.full(nl // unit, unit, dtype=np.int64)
+    b = torch.zeros(m, dtype=torch.float64, device=dev)
+    c = torch.zeros(nl, dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
+    plan = DevicePlan.from_device(m, nl, o, rows.data_ptr(), cols.data_ptr(), vals.data_ptr(), b.data_ptr(),
+                                  c.data_ptr(), sizes, stream=stream)
+    del rows, cols, vals
+    xf = _project(torch, torch.randn(n, generator=g_shared, device=dev, dtype=torch.float64), unit)[c0:c1]
+    xf = xf.contiguous()
+    plan.apply_A(xf.data_ptr(), b.data_ptr())
+    dist.all_reduce(b, op=dist.ReduceOp.SUM, group=group)
+    lam = torch.randn(m, generator=g_shared, device=dev, dtype=torch.float64)
+    atl = torch.empty(nl, dtype=torch.float64, device=dev)
+    plan.apply_At(lam.data_ptr(), atl.data_ptr())
+    s = _project(torch, torch.randn(n, generator=g_shared, device=dev, dtype=torch.float64), unit)[c0:c1]
+    c.copy_(s - atl)
+    torch.cuda.synchronize()
+    plan.set_rhs(b.data_ptr(), c.data_ptr(), on_device=True)
+    b_norms = (float(b.abs().max()), math.sqrt(float((b * b).sum())))
+    cc = torch.stack([c.abs().max() if nl else torch.zeros((), device=dev, dtype=torch.float64), (c * c).sum()])
+    mx = cc[:1].clone()
+    sq = cc[1:].clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=group)
+    dist.all_reduce(sq, op=dist.ReduceOp.SUM, group=group)
+    c_norms = (float(mx), math.sqrt(float(sq)))
+    return plan, col_cuts, b_norms, c_norms
 
 
 def _project(torch, w, unit):

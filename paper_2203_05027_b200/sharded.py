@@ -32,7 +32,8 @@ import numpy as np
 from .api import IterationReport, SolveResult, SolverConfig, _decide, norms
 from .problem import ConeSpec, ProblemInstance, TripletMatrix, cone_sizes_array
 
-__all__ = ["solve_sharded", "run_sharded", "partition", "CudaRankBackend", "assemble_report"]
+__all__ = ["solve_sharded", "run_sharded", "partition", "CudaRankBackend", "assemble_report",
+           "solve_col_sharded", "run_col_sharded", "CudaColBackend", "local_columns"]
 
 # report parts: row = {sum prim^2, max|prim|, max|Ax|, sum b.lam, nonfinite};
 # column = {sum dual^2, max|dual|, sum stat^2, max|stat|, max|A^T lam|, sum c.x, cone_gap, nonfinite}
@@ -384,3 +385,210 @@ def run_sharded(be, row_cuts, col_cuts, cfg, b_norms, c_norms, group=None, timin
     lam = torch.cat([parts[r][:row_cuts[r + 1] - row_cuts[r]] for r in range(world)])
     return SolveResult(x=x_full.detach().cpu().numpy().copy(), lam=lam.detach().cpu().numpy().copy(),
                        report=trace[-1], trace=tuple(trace))
+
+
+# ------------------------------------------------------------------ column sharding
+# SURVEY §8e alternative for m < n: every rank holds A's columns [lo, hi) with ALL rows.
+# One iteration is
+#
+#     x_s, z_s, delta_s <- column pass on the slice (h is full and local)
+#     ax   = all-reduce(A_s x_s, sum)            the only exchange: one m-vector
+#     lam, h <- row update of every row from ax   (the same on every rank)
+#
+# so a rank sends ~2m(p-1)/p doubles per iteration instead of the row-sharded 2n(p-1)/p.
+# Reports: the row part is computed locally from the full vectors (identical on every
+# rank); the column part (A_s^T lam over the slice) is all-reduced.
+
+def local_columns(p, c0: int, c1: int):
+    """The rank's columns [c0, c1) renumbered from 0, all rows, with the slice's cones."""
+    cols = np.asarray(p.A.cols, dtype=np.int64)
+    sel = (cols >= c0) & (cols < c1)
+    a = TripletMatrix(p.A.num_rows, c1 - c0, np.asarray(p.A.rows)[sel], cols[sel] - c0, np.asarray(p.A.vals)[sel])
+    sizes = cone_sizes_array(p.cones)
+    starts = np.concatenate(([0], np.cumsum(sizes)))
+    q0, q1 = int(np.searchsorted(starts, c0)), int(np.searchsorted(starts, c1))
+    return ProblemInstance(a, np.asarray(p.b), np.asarray(p.c)[c0:c1], ConeSpec(sizes[q0:q1]))
+
+
+class CudaColBackend:
+    """One rank of the column-sharded solve: a plan over its column slice (all rows)."""
+
+    def __init__(self, lp, plan=None):
+        import ctypes
+
+        import torch
+
+        from . import _lib
+        from .engine import DevicePlan
+
+        self.torch = torch
+        self.lib = _lib.lib()
+        self.stream = torch.cuda.current_stream()
+        self.plan = plan if plan is not None else DevicePlan.from_problem(lp, stream=self.stream.cuda_stream)
+        self.plan.set_state(1.0, None, export=False)
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        self.m, self.n = self.plan.m, self.plan.n
+
+        def view(which):
+            ptr, ln = ctypes.c_void_p(), ctypes.c_int64()
+            _lib.check(self.lib.cf_plan_vector(self.plan.handle, which, ctypes.byref(ptr), ctypes.byref(ln)))
+            return torch.as_tensor(_DevArray(ptr.value or 0, ln.value), device=self.device) if ln.value else \
+                torch.zeros(0, dtype=torch.float64, device=self.device)
+
+        self.x, self.z, self.delta, self.lam, self.ax, self.c = view(0), view(1), view(2), view(3), view(5), view(7)
+        self.atl = torch.zeros(self.n, dtype=torch.float64, device=self.device)
+
+    @staticmethod
+    def _p(t):
+        import ctypes
+
+        return ctypes.c_void_p(t.data_ptr()) if t.numel() else ctypes.c_void_p(0)
+
+    def row_norms(self):
+        """(d, amax) of the slice's entries per row, device tensors of m."""
+        from . import _lib
+
+        d = self.torch.zeros(self.m, dtype=self.torch.float64, device=self.device)
+        am = self.torch.zeros(self.m, dtype=self.torch.float64, device=self.device)
+        _lib.check(self.lib.cf_plan_row_norms(self.plan.handle, self._p(d), self._p(am)))
+        return d, am
+
+    def set_row_norms(self, d, am):
+        from . import _lib
+
+        _lib.check(self.lib.cf_plan_set_row_norms(self.plan.handle, self._p(d), self._p(am)))
+
+    def col_step(self, mu: float):
+        from . import _lib
+
+        _lib.check(self.lib.cf_plan_col_step(self.plan.handle, float(mu)))
+
+    def partial_Ax(self):
+        """A_s x_s into the plan's ax buffer (the driver all-reduces it in place)."""
+        from . import _lib
+
+        if self.n:
+            _lib.check(self.lib.cf_apply_A_async(self.plan.handle, self._p(self.x), self._p(self.ax)))
+        else:
+            self.ax.zero_()
+        return self.ax
+
+    def row_update(self, mu: float, report: bool):
+        from . import _lib
+
+        _lib.check(self.lib.cf_plan_row_update(self.plan.handle, float(mu), 1 if report else 0))
+
+    def row_parts(self):
+        from . import _lib
+
+        out = np.zeros(5)
+        _lib.check(self.lib.cf_plan_row_parts(self.plan.handle, ctypes_ptr(out)))
+        return out
+
+    def col_parts(self):
+        from . import _lib
+
+        out = np.zeros(8)
+        if self.n:
+            _lib.check(self.lib.cf_apply_At_async(self.plan.handle, self._p(self.lam), self._p(self.atl)))
+        _lib.check(self.lib.cf_column_parts(self.n, self._p(self.atl), self._p(self.c), self._p(self.x),
+                                            self._p(self.z), self._p(self.delta), ctypes_ptr(out),
+                                            self.stream.cuda_stream))
+        return out
+
+    def x_slice(self):
+        return self.x
+
+    def lam_full(self):
+        return self.lam
+
+    def close(self):
+        self.plan.close()
+
+
+def ctypes_ptr(a):
+    import ctypes
+
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def run_col_sharded(be, col_cuts, cfg, b_norms, c_norms, group=None, timing=None,
+                    gather_result: bool = True) -> SolveResult:
+    """The column-sharded loop on an existing rank backend (column cuts shared by all ranks)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    # fu = 1/(1 + d) and the implicit-y finiteness check need WHOLE rows: sum the slices' d
+    # (uv.py:81; the association of the sum differs from one GPU's only by rounding)
+    d, am = be.row_norms()
+    dist.all_reduce(d, op=dist.ReduceOp.SUM, group=group)
+    dist.all_reduce(am, op=dist.ReduceOp.MAX, group=group)
+    be.set_row_norms(d, am)
+    trace = []
+    if timing is not None and be.device.type == "cuda":
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+    for k in range(1, cfg.max_iters + 1):
+        be.col_step(cfg.mu)
+        ax = be.partial_Ax()
+        dist.all_reduce(ax, op=dist.ReduceOp.SUM, group=group)
+        report = (k % cfg.check_every == 0) or (k == cfg.max_iters)
+        be.row_update(cfg.mu, report)
+        if not report:
+            continue
+        rp = be.row_parts()          # full rows: the same on every rank
+        cp = torch.as_tensor(be.col_parts(), dtype=torch.float64, device=be.device)
+        sums = torch.stack([cp[0], cp[2], cp[5]])
+        maxs = torch.stack([cp[1], cp[3], cp[4], cp[6], cp[7]])
+        nan = torch.isnan(maxs).to(torch.float64)
+        dist.all_reduce(sums, op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(maxs, op=dist.ReduceOp.MAX, group=group)
+        dist.all_reduce(nan, op=dist.ReduceOp.MAX, group=group)
+        maxs = torch.where(nan > 0, torch.full_like(maxs, float("nan")), maxs)
+        s, mx = sums.tolist(), maxs.tolist()
+        f = [rp[0], rp[1], rp[2], rp[3], rp[4], s[0], mx[0], s[1], mx[1], mx[2], s[2], mx[3], mx[4]]
+        rep = assemble_report(k, f)
+        status = _decide(rep, cfg, b_norms, c_norms)
+        if status == "running" and k == cfg.max_iters:
+            status = "max_iters"
+        trace.append(replace(rep, status=status))
+        if status != "running":
+            break
+    if timing is not None and be.device.type == "cuda":
+        e1.record()
+        e1.synchronize()
+        timing["loop_ms"] = e0.elapsed_time(e1)
+        timing["iters"] = trace[-1].iter
+    if not gather_result:
+        return SolveResult(x=None, lam=None, report=trace[-1], trace=tuple(trace))
+    S = max(col_cuts[r + 1] - col_cuts[r] for r in range(world))
+    xs = torch.zeros(S, dtype=torch.float64, device=be.device)
+    xl = be.x_slice()
+    xs[:xl.numel()] = xl
+    parts = [torch.empty(S, dtype=torch.float64, device=be.device) for _ in range(world)]
+    dist.all_gather(parts, xs, group=group)
+    x = torch.cat([parts[r][:col_cuts[r + 1] - col_cuts[r]] for r in range(world)])
+    del rank
+    return SolveResult(x=x.detach().cpu().numpy().copy(), lam=be.lam_full().detach().cpu().numpy().copy(),
+                       report=trace[-1], trace=tuple(trace))
+
+
+def solve_col_sharded(p, cfg: SolverConfig | None = None, group=None, backend_factory=None) -> SolveResult:
+    """solve() with A's columns split over the ranks of ``group`` (every rank passes the same problem).
+
+    Cold start only. Returns the same SolveResult on every rank."""
+    import torch.distributed as dist
+
+    cfg = cfg or SolverConfig()
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    _, col_cuts = partition(p, world)
+    lp = local_columns(p, col_cuts[rank], col_cuts[rank + 1])
+    be = (backend_factory or CudaColBackend)(lp)
+    try:
+        return run_col_sharded(be, col_cuts, cfg, norms(p.b), norms(p.c), group=group)
+    finally:
+        if hasattr(be, "close"):
+            be.close()

@@ -147,3 +147,19 @@ def test_sharded_with_column_bands_matches_single_plan(nccl_group, monkeypatch):
     res = run_sharded(be, rc, cc, cfg, bn, cn)
     assert np.array_equal(res.x, ref["x"]) and np.array_equal(res.lam, ref["lam"])
     be.close()
+
+
+@pytest.mark.parametrize("kind,mu", [("lp", 1.0), ("socp4", 0.6)])
+def test_column_sharded_cuda_backend_matches_oracle(nccl_group, kind, mu):
+    """Column sharding with the CUDA backend (cf_plan_col_step, cf_apply_A_async, the
+    all-reduce of A x, cf_plan_row_update, global row norms) reaches the oracle's solve."""
+    from paper_2203_05027_b200 import GenSpec, SolverConfig, generate
+    from paper_2203_05027_b200.sharded import solve_col_sharded
+
+    p = generate(GenSpec(120, 400, 0.04, kind, seed=17))
+    cfg = SolverConfig(mu=mu, max_iters=3000, eps_prim=1e-5, eps_dual=1e-5, eps_gap=1e-5)
+    res = solve_col_sharded(p, cfg)
+    ox, olam, otrace, _ = oracle.solve(p, cfg)
+    assert [r.iter for r in res.trace] == [r["iter"] for r in otrace]
+    assert res.report.status == otrace[-1]["status"]
+    assert rel_err(res.x, ox) <= 1e-8 and rel_err(res.lam, olam) <= 1e-8

@@ -147,3 +147,110 @@ def test_partition_balanced_and_cone_aligned():
     nnz = np.bincount(p.A.rows, minlength=100)
     per = [nnz[rows[r]:rows[r + 1]].sum() for r in range(4)]
     assert max(per) - min(per) <= nnz.max() + 1     # balanced to within one row
+
+
+class NumpyColBackend:
+    """Test-only restatement of one column-sharded rank (cf_plan_col_step / cf_apply_A /
+    cf_plan_row_update / parts) on its column slice with all rows."""
+
+    def __init__(self, lp):
+        self.device = torch.device("cpu")
+        a = lp.A
+        order = np.lexsort((a.rows, a.cols))
+        self.rows, self.cols, self.vals = a.rows[order], a.cols[order], a.vals[order]
+        self.m, self.n = a.num_rows, a.num_cols
+        self.b = np.asarray(lp.b, dtype=np.float64)
+        self.c = np.asarray(lp.c, dtype=np.float64)
+        self.dloc = np.bincount(self.rows, weights=self.vals * self.vals, minlength=self.m)
+        self.lam, self.h = np.zeros(self.m), np.zeros(self.m)
+        self.x, self.z, self.d = np.zeros(self.n), np.zeros(self.n), np.zeros(self.n)
+        self.cnt = np.bincount(self.cols, minlength=self.n).astype(np.float64)   # all rows: true counts
+        self.sizes = np.asarray(lp.cones.block_sizes, dtype=np.int64)
+        self.ax_t = torch.zeros(self.m, dtype=torch.float64)
+
+    def row_norms(self):
+        return torch.tensor(self.dloc), torch.zeros(self.m, dtype=torch.float64)
+
+    def set_row_norms(self, d, am):
+        d = d.numpy()
+        self.fu, self.db = 1.0 / (1.0 + d), d * self.b
+
+    def col_step(self, mu):
+        ath = np.bincount(self.cols, weights=self.vals * self.h[self.rows], minlength=self.n)
+        fv = 1.0 / (1.0 + self.cnt)
+        dm = self.d / mu
+        xp = fv * ((((self.cnt * self.x) + ath) + self.z + dm) - self.c / mu)
+        w = xp - dm
+        zp = project_cones_host(self.sizes, w)
+        self.d = self.d + mu * (zp - xp)
+        self.x, self.z = xp, zp
+
+    def partial_Ax(self):
+        self.ax_t.copy_(torch.tensor(np.bincount(self.rows, weights=self.vals * self.x[self.cols], minlength=self.m)))
+        return self.ax_t
+
+    def row_update(self, mu, report):
+        ax = self.ax_t.numpy()
+        r = self.fu * (self.db + ax)
+        self.lam = self.lam + mu * (r - self.b)
+        self.h = (self.b - r) - self.lam / mu
+        self.ax = ax.copy()
+
+    def row_parts(self):
+        pr = self.ax - self.b
+        return np.array([np.sum(pr * pr), np.max(np.abs(pr)), np.max(np.abs(self.ax)), np.sum(self.b * self.lam),
+                         float(not np.isfinite(self.lam).all())])
+
+    def col_parts(self):
+        atl = np.bincount(self.cols, weights=self.vals * self.lam[self.rows], minlength=self.n)
+        dual = atl + self.c
+        stat = dual - self.d
+        if atl.size == 0:
+            return np.zeros(8)
+        return np.array([np.sum(dual * dual), np.max(np.abs(dual)), np.sum(stat * stat), np.max(np.abs(stat)),
+                         np.max(np.abs(atl)), np.sum(self.c * self.x), np.max(np.abs(self.x - self.z)),
+                         float(not (np.isfinite(self.x).all() and np.isfinite(self.z).all()))])
+
+    def x_slice(self):
+        return torch.tensor(self.x)
+
+    def lam_full(self):
+        return torch.tensor(self.lam)
+
+
+def _col_worker(rank, world, port, spec, cfg_kw, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2203_05027_b200.sharded import solve_col_sharded
+
+        p = generate(spec)
+        res = solve_col_sharded(p, SolverConfig(**cfg_kw), backend_factory=NumpyColBackend)
+        if rank == 0:
+            np.savez(out_path, x=res.x, lam=res.lam, iters=np.array([r.iter for r in res.trace]),
+                     status=np.array([r.status for r in res.trace]),
+                     pobj=np.array([r.pobj for r in res.trace]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,spec,cfg_kw", [
+    (2, GenSpec(40, 90, 0.06, "lp", seed=41), dict(eps_prim=1e-4, eps_dual=1e-4, eps_gap=1e-4, max_iters=4000)),
+    (3, GenSpec(30, 64, 0.08, "socp4", seed=42), dict(mu=0.7, max_iters=600, check_every=20)),
+])
+def test_column_sharded_matches_oracle(tmp_path, world, spec, cfg_kw):
+    """Column sharding (one all-reduce of A x per iteration) reaches the oracle's iterates."""
+    out = str(tmp_path / "res.npz")
+    port = _free_port()
+    mp.start_processes(_col_worker, args=(world, port, spec, cfg_kw, out), nprocs=world, join=True,
+                       start_method="spawn")
+    got = np.load(out)
+    p = generate(spec)
+    cfg = SolverConfig(**cfg_kw)
+    ox, olam, otrace, _ = oracle.solve(p, cfg)
+    assert list(got["iters"]) == [r["iter"] for r in otrace]
+    assert list(got["status"]) == [r["status"] for r in otrace]
+    assert rel_err(got["x"], ox) <= 1e-8
+    assert rel_err(got["lam"], olam) <= 1e-8
+    np.testing.assert_allclose(got["pobj"], [r["pobj"] for r in otrace], rtol=1e-9, atol=1e-9)
