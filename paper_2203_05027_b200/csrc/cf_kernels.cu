@@ -702,6 +702,14 @@ struct Medium : P {
     static constexpr int kMinBlocks = 4;
     static constexpr bool kStaged = CF_STAGED_SMALL;
 };
+// large passes over long segments (>= 16 nonzeros on average): 4 diagonals in flight,
+// 5 CTAs/SM (C3's row pass 0.258 -> 0.237 ms; C2's 10-long segments keep the default)
+template <class P>
+struct Long : P {
+    static constexpr int kUnroll = 4;
+    static constexpr int kMinBlocks = 5;
+};
+constexpr double kLongSegments = 16.0;
 #ifndef CF_MEDIUM_TILES
 #define CF_MEDIUM_TILES (148 * 12)
 #endif
@@ -720,12 +728,19 @@ int launch_variant(const Q& pol, const pass::Jds& L, const pass::Tiles& T, const
 
 template <class P>
 int launch_pass(const P& pol, const pass::Jds& L, const pass::Tiles& T, const int32_t* done, cudaStream_t st,
-                int* grid_out = nullptr) {
+                int* grid_out = nullptr, double avg_len = 0.0) {
     if (T.n_tiles == 0) return CF_OK;
     if (T.n_tiles <= kWideTiles) return launch_variant(Wide<P>{pol}, L, T, done, st, grid_out);
     if (T.n_tiles <= kMediumTiles) return launch_variant(Medium<P>{pol}, L, T, done, st, grid_out);
+    if constexpr (P::kUnroll < 4) {
+        if (avg_len >= kLongSegments) return launch_variant(Long<P>{pol}, L, T, done, st, grid_out);
+    }
     return launch_variant(pol, L, T, done, st, grid_out);
 }
+
+// average segment length of a pass: nonzeros / segments (rows per panel, columns per band)
+double row_avg_len(const cf_plan* p) { return p->m ? (double)p->o / ((double)p->n_panels * (double)p->m) : 0.0; }
+double col_avg_len(const cf_plan* p) { return p->n ? (double)p->o / ((double)p->n_bands * (double)p->n) : 0.0; }
 
 // the band fields of a column policy (seg_off/last/has_carry are set per launch)
 template <class P>
@@ -743,7 +758,8 @@ int launch_col_bands(cf_plan* p, P pol, const int32_t* done, int64_t* nl, int* g
         pol.seg_off = (int64_t)b * p->n;
         pol.last = (b == B - 1);
         pol.has_carry = b > 0;
-        CF_TRY(launch_pass(pol, col_jds(p), col_band_tiles(p, b), done, p->stream, pol.last ? grid_out : nullptr));
+        CF_TRY(launch_pass(pol, col_jds(p), col_band_tiles(p, b), done, p->stream, pol.last ? grid_out : nullptr,
+                           col_avg_len(p)));
         if (nl) ++*nl;
     }
     return CF_OK;
@@ -796,7 +812,7 @@ int launch_row_only(cf_plan* p, const IterOpts& opt, const int32_t* done, int64_
         r.rcorr = opt.rcorr;
         r.br = (opt.report || p->keep_br) ? p->br.p : nullptr;
         r.ax = opt.report ? p->ax.p : nullptr;
-        CF_TRY(launch_pass(r, row_jds(p), row_panel_tiles(p, pn), done, p->stream));
+        CF_TRY(launch_pass(r, row_jds(p), row_panel_tiles(p, pn), done, p->stream, nullptr, row_avg_len(p)));
         ++nl;
     }
     if (launches) *launches += nl;
@@ -878,7 +894,7 @@ int launch_spmv_rows(cf_plan* p, const double* x, double* y) {
         r.seg_off = (int64_t)pn * m;
         r.has_carry = pn > 0;
         r.y = y;
-        CF_TRY(launch_pass(r, row_jds(p), row_panel_tiles(p, pn), nullptr, p->stream));
+        CF_TRY(launch_pass(r, row_jds(p), row_panel_tiles(p, pn), nullptr, p->stream, nullptr, row_avg_len(p)));
     }
     return CF_OK;
 }
