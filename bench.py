@@ -440,7 +440,7 @@ def run_sharded_bench(args, spec, rank, world, local_rank):
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (per-rank GPU generator, reference recipe)",
             "config": {"workload": spec["workload"] if scale == 1.0 else f"C5 structure scaled by {scale}: m={m} n={n}",
-                       "m": m, "n": n, "o": o_total, "parallelism": f"row-sharded x{world} (NCCL reduce-scatter + all-gather)"},
+                       "m": m, "n": n, "o": o_total, "parallelism": f"row-sharded x{world} (per-slice NCCL reduce overlapped with the column pass + all-gather)"},
             # per iteration: partial A^T h, column update, row pass (per panel); + report kernels every 25
             "gpu_launches": args.steps * 4 + (args.steps // 25) * 5,
             "iteration_roofline": {"bytes_per_iteration_total": row_b + col_b,
