@@ -289,6 +289,10 @@ int cf_format_double(double x, char* out);
 int cf_coneprob_write(const char* path, int64_t m, int64_t n, int64_t nnz, const int64_t* rows, const int64_t* cols,
                       const double* vals, const double* b, const double* c, int64_t n_blocks, const int64_t* sizes,
                       int threads);
+/* write_solution (fileio.py:193-200) to a file: `head` (the STATUS and POBJ/DOBJ/ITERS
+ * lines, newline-terminated) followed by x then lam, one repr() per line */
+int cf_solution_write(const char* path, const char* head, const double* x, int64_t n, const double* lam, int64_t m,
+                      int threads);
 
 #ifdef __cplusplus
 }

@@ -17,6 +17,7 @@ from .api import (
     solve_batch,
 )
 from .binio import (
+    TRACE_COLUMNS,
     ParseError,
     parse_problem,
     read_problem,
@@ -24,6 +25,9 @@ from .binio import (
     write_problem,
     write_problem_binary,
     write_problem_file,
+    write_solution,
+    write_solution_file,
+    trace_csv,
 )
 from .engine import DevicePlan
 from .instances import GeneratedInstance, GenSpec, generate, generate_witnessed, shape_for_nnz
@@ -51,6 +55,10 @@ __all__ = [
     "write_problem",
     "write_problem_binary",
     "write_problem_file",
+    "write_solution",
+    "write_solution_file",
+    "trace_csv",
+    "TRACE_COLUMNS",
     "generate",
     "generate_witnessed",
     "shape_for_nnz",

@@ -127,6 +127,7 @@ SIGNATURES = {
     "cf_coneprob_body": (c_int, [_P, _P, _P, _P, _P, _P, c_int, _I64, c_char_p, c_int64]),
     "cf_format_double": (c_int, [c_double, c_char_p]),
     "cf_coneprob_write": (c_int, [c_char_p, c_int64, c_int64, c_int64, _P, _P, _P, _P, _P, c_int64, _P, c_int]),
+    "cf_solution_write": (c_int, [c_char_p, c_char_p, _P, c_int64, _P, c_int64, c_int]),
 }
 
 _lib = None

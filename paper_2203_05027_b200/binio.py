@@ -45,6 +45,10 @@ __all__ = [
     "format_float",
     "write_problem_binary",
     "read_problem_binary",
+    "write_solution",
+    "write_solution_file",
+    "TRACE_COLUMNS",
+    "trace_csv",
 ]
 
 CF_IO_PARSE = 6
@@ -282,6 +286,66 @@ def write_problem(p, threads: int = 0) -> str:
             return f.read()
     finally:
         os.unlink(path)
+
+
+def _solution_head(status: str, pobj: float, dobj: float, iters: int) -> str:
+    return f"STATUS {status}\nPOBJ {repr(float(pobj))} / DOBJ {repr(float(dobj))} / ITERS {iters}\n"
+
+
+def write_solution_file(path: str, status: str, pobj: float, dobj: float, iters: int, x, lam,
+                        threads: int = 0) -> None:
+    """write_solution (fileio.py:193-200) straight to `path`; the x and lam lines are
+    formatted by the native writer on all host cores."""
+    from ._lib import lib
+
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    lam = np.ascontiguousarray(lam, dtype=np.float64)
+    head = _solution_head(status, pobj, dobj, iters).encode("utf-8")
+    rc = lib().cf_solution_write(os.fsencode(path), head,
+                                 ctypes.c_void_p(x.ctypes.data) if x.size else ctypes.c_void_p(0), int(x.size),
+                                 ctypes.c_void_p(lam.ctypes.data) if lam.size else ctypes.c_void_p(0), int(lam.size),
+                                 int(threads))
+    if rc:
+        raise OSError(f"cannot write {path!r}")
+
+
+def write_solution(status: str, pobj: float, dobj: float, iters: int, x, lam) -> str:
+    """The solution text (fileio.py:193-200): STATUS, POBJ/DOBJ/ITERS, x, lam."""
+    fd, path = tempfile.mkstemp(prefix="conesol_", suffix=".txt")
+    os.close(fd)
+    try:
+        write_solution_file(path, status, pobj, dobj, iters, x, lam)
+        with open(path, encoding="utf-8") as f:
+            return f.read()
+    finally:
+        os.unlink(path)
+
+
+TRACE_COLUMNS = (
+    "iter",
+    "prim_res_inf",
+    "prim_res_2",
+    "dual_res_inf",
+    "dual_res_2",
+    "stat_res_inf",
+    "stat_res_2",
+    "cone_gap",
+    "pobj",
+    "dobj",
+    "gap",
+    "status",
+)
+
+
+def trace_csv(trace) -> str:
+    """Per-report CSV of a solve's trace (fileio.py:228-266), no timing columns."""
+    lines = [",".join(TRACE_COLUMNS)]
+    for rep in trace:
+        cells = [str(rep.iter)]
+        cells.extend(repr(float(getattr(rep, col))) for col in TRACE_COLUMNS[1:-1])
+        cells.append(rep.status)
+        lines.append(",".join(cells))
+    return "\n".join(lines) + "\n"
 
 
 # ---------------------------------------------------------------- binary format

@@ -768,4 +768,36 @@ int cf_coneprob_write(const char* path, int64_t m, int64_t n, int64_t nnz, const
     return ok ? CF_OK : CF_EINVAL;
 }
 
+int cf_solution_write(const char* path, const char* head, const double* x, int64_t n, const double* lam, int64_t m,
+                      int threads) {
+    if (!path || !head || n < 0 || m < 0) return CF_EINVAL;
+    FILE* f = fopen(path, "wb");
+    if (!f) return CF_EINVAL;
+    const size_t hl = strlen(head);
+    bool ok = fwrite(head, 1, hl, f) == hl;
+    // x then lam, one repr per line, formatted in parallel blocks (fileio.py:198-199)
+    const int64_t total = n + m;
+    const int T = n_threads(threads);
+    const int64_t block = 1 << 20;
+    std::vector<std::string> buf(T);
+    for (int64_t base = 0; base < total && ok; base += block * T) {
+        std::vector<std::thread> th;
+        for (int w = 0; w < T; ++w)
+            th.emplace_back([&, w]() {
+                std::string& s = buf[w];
+                s.clear();
+                const int64_t a = base + block * w, z = std::min(total, a + block);
+                char tmp[64];
+                for (int64_t k = a; k < z; ++k) {
+                    s.append(tmp, (size_t)cf_format_double(k < n ? x[k] : lam[k - n], tmp));
+                    s += '\n';
+                }
+            });
+        for (auto& t : th) t.join();
+        for (int w = 0; w < T && ok; ++w) ok = fwrite(buf[w].data(), 1, buf[w].size(), f) == buf[w].size();
+    }
+    ok = (fclose(f) == 0) && ok;
+    return ok ? CF_OK : CF_EINVAL;
+}
+
 }  // extern "C"

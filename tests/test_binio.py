@@ -113,3 +113,23 @@ def test_native_path_covers_ascii_cases():
     texts = [str(g["texts"][k]) for k in fallback]
     assert len(fallback) == 3
     assert all(any(ord(ch) > 127 for ch in t) or "99999999999999999999" in t for t in texts)
+
+
+def test_write_solution_and_trace_csv_format():
+    """write_solution (fileio.py:193-200) and trace_csv (:244-266): repr() per value."""
+    from types import SimpleNamespace
+
+    from paper_2203_05027_b200.binio import TRACE_COLUMNS, trace_csv, write_solution
+
+    rng = np.random.default_rng(5)
+    x = np.concatenate([rng.standard_normal(50) * 10.0 ** rng.integers(-30, 30, 50),
+                        [0.0, -0.0, 1e16, 1.5e-7, 123456789.0, np.inf, -np.inf, np.nan]])
+    lam = rng.standard_normal(7)
+    got = write_solution("solved", 1.25, -0.1, 42, x, lam)
+    want = "\n".join(["STATUS solved", "POBJ 1.25 / DOBJ -0.1 / ITERS 42"] +
+                     [repr(float(v)) for v in x] + [repr(float(v)) for v in lam]) + "\n"
+    assert got == want
+    rep = SimpleNamespace(iter=25, status="running", **{c: 0.1 * k for k, c in enumerate(TRACE_COLUMNS[1:-1])})
+    lines = trace_csv([rep, rep]).splitlines()
+    assert lines[0] == ",".join(TRACE_COLUMNS)
+    assert lines[1] == "25," + ",".join(repr(0.1 * k) for k in range(len(TRACE_COLUMNS) - 2)) + ",running"
