@@ -662,21 +662,30 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, 
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+// resident CTAs of k_pass<P> on the device (computed once, thread-safe: plans are
+// created and run from several host threads by solve_batch / run_bench)
+template <class P>
+int pass_capacity() {
+    static const int cap = [] {
+        int per_sm = 0, sms = 0, dev = 0;
+        bool ok = cudaFuncSetAttribute(pass::k_pass<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)pass::smem_bytes<P>()) == cudaSuccess;
+        ok = ok && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pass::k_pass<P>, pass::kPThreads,
+                                                                 pass::smem_bytes<P>()) == cudaSuccess;
+        ok = ok && cudaGetDevice(&dev) == cudaSuccess;
+        ok = ok && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess;
+        return ok ? std::max(per_sm, 1) * sms : 0;
+    }();
+    return cap;
+}
+
 template <class P>
 int persistent_grid(int n_tiles) {
-    static int per_sm = -1;
-    static int sms = 0;
-    if (per_sm < 0) {
-        CF_CUDA(cudaFuncSetAttribute(pass::k_pass<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)pass::smem_bytes<P>()));
-        CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pass::k_pass<P>, pass::kPThreads,
-                                                              pass::smem_bytes<P>()));
-        int dev = 0;
-        CF_CUDA(cudaGetDevice(&dev));
-        CF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        if (per_sm < 1) per_sm = 1;
+    const int g = pass_capacity<P>();
+    if (g <= 0) {
+        set_error("k_pass occupancy query failed");
+        return 0;
     }
-    const int g = per_sm * sms;
     return n_tiles < g ? (n_tiles > 0 ? n_tiles : 1) : g;
 }
 
@@ -720,6 +729,7 @@ template <class Q>
 int launch_variant(const Q& pol, const pass::Jds& L, const pass::Tiles& T, const int32_t* done, cudaStream_t st,
                    int* grid_out) {
     const int grid = persistent_grid<Q>(T.n_tiles);
+    if (grid <= 0) return CF_ECUDA;
     if (grid_out) *grid_out = grid;
     CF_CUDA(launch_pdl(pass::k_pass<Q>, (unsigned)grid, (unsigned)pass::kPThreads, pass::smem_bytes<Q>(), st, pol, L,
                        T, done));
