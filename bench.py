@@ -53,6 +53,11 @@ CONFIGS = {
                workload="C2: synthetic sparse LP m=5,000,000 n=10,000,000 o=100,000,000 (20 nnz/row) fp64"),
     "c3": dict(m=2_000_000, n=4_000_000, density=5e-6, cone_kind="socp4",
                workload="C3: synthetic SOCP m=2,000,000 n=4,000,000 o=40,000,000, 1,000,000 K4 cones fp64"),
+    "c3m": dict(m=3_000_000, n=5_000_000, density=2.6e-6, cone_kind="rls",
+                workload="C3 secondary (SURVEY §8d): robust least squares in SOC form, 1,000,000 K4 blocks "
+                         "(t_i, u_i) + x+/x- in R+^1,000,000; m=3,000,000 n=5,000,000 o=39,000,000 fp64",
+                data="synthetic (GPU generator devgen.rls_arrays: N(0,1) F with 6 distinct columns per row, "
+                     "g ~ N(0,1); same arrays for every arm)"),
     "c1": dict(m=1000, n=2000, density=0.01, cone_kind="lp",
                workload="C1: synthetic sparse LP m=1,000 n=2,000 o=20,000 fp64"),
     "c5": dict(m=50_000_000, n=100_000_000, density=2e-7, cone_kind="lp", sharded=True,
@@ -373,7 +378,8 @@ def run_ours(args, spec, rank, world, local_rank):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (GPU generator, reference recipe generate.py:103-140; same arrays for every arm)",
+            "data": spec.get("data", "synthetic (GPU generator, reference recipe generate.py:103-140; same arrays "
+                                     "for every arm)"),
             "config": {"workload": spec["workload"], "m": m, "n": n, "o": o, "mu": 1.0, "check_every": 25,
                        "parallelism": "replicas" if world > 1 else "single", "l2": "inputs larger than L2 "
                        f"({(row_b + col_b) / 1e9:.2f} GB streamed per iteration vs 126 MB L2)"},

@@ -21,6 +21,23 @@ constexpr int kThreads = 256;     // threads of the simple (non-pass) kernels
 #define CF_PSEG 256
 #endif
 constexpr int kTileNnz = CF_PCAP;  // nonzeros per tile (= pass::kPCap)
+#ifndef CF_PCAP_LARGE
+#define CF_PCAP_LARGE 8192
+#endif
+// Nonzeros per tile of a pass too large for the staged (Wide/Medium) dispatch: the
+// direct engine loads idx/val straight from HBM, so a tile may hold more than the
+// stage, and rows / columns longer than kTileNnz / kTileSeg then still fill all 8
+// warp blocks of a tile (C3's row pass 0.237 -> 0.209 ms, the robust-LS column
+// pass 0.48 -> 0.32 ms). The TMA ring stages every tile, so it keeps kTileNnz.
+#if defined(CF_TMA) && CF_TMA
+constexpr int kTileNnzLarge = CF_PCAP;
+#else
+constexpr int kTileNnzLarge = CF_PCAP_LARGE;
+#endif
+#ifndef CF_MEDIUM_TILES
+#define CF_MEDIUM_TILES (148 * 12)
+#endif
+constexpr int kStagedMaxTiles = CF_MEDIUM_TILES;   // passes with more tiles per launch run unstaged
 constexpr int kTileSeg = CF_PSEG;  // rows / columns per tile (= pass::kPSeg)
 constexpr int kTileDiag = 256;    // longest segment inside a multi-segment tile (= pass::kMaxDiag)
 constexpr int kSmallCone = kTileSeg;  // cones up to this size are projected inside the column tile
@@ -137,6 +154,7 @@ struct cf_plan {
     cf::DevBuf<double> rj_val, cj_val;
     cf::DevBuf<uint32_t> rj_pl, cj_pl;  // per segment position: perm (rank -> segment) | length << 5 | block start << 14
     int64_t row_tiles = 0, col_tiles = 0;
+    bool row_large_tiles = false, col_large_tiles = false;   // cut at kTileNnzLarge (never staged)
     // row-pass column panels: the CSR is stored panel-major (segment = panel*m + row)
     // so each row-pass launch gathers only one panel's slice of x (L2-resident)
     int32_t n_panels = 1;

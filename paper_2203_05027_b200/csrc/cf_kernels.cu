@@ -634,11 +634,11 @@ inline int grid_for(int64_t work, int threads) {
 
 pass::Tiles row_panel_tiles(const cf_plan* p, int panel) {
     const int64_t t0 = p->row_panel_tile[panel], t1 = p->row_panel_tile[panel + 1];
-    return pass::Tiles{p->row_tb.p + t0, (int32_t)(t1 - t0)};
+    return pass::Tiles{p->row_tb.p + t0, (int32_t)(t1 - t0), !p->row_large_tiles};
 }
 pass::Tiles col_band_tiles(const cf_plan* p, int band) {
     const int64_t t0 = p->col_band_tile[band], t1 = p->col_band_tile[band + 1];
-    return pass::Tiles{p->col_tb.p + t0, (int32_t)(t1 - t0)};
+    return pass::Tiles{p->col_tb.p + t0, (int32_t)(t1 - t0), !p->col_large_tiles};
 }
 pass::Jds row_jds(const cf_plan* p) { return pass::Jds{p->rj_idx.p, p->rj_val.p, p->rj_pl.p}; }
 pass::Jds col_jds(const cf_plan* p) { return pass::Jds{p->cj_idx.p, p->cj_val.p, p->cj_pl.p}; }
@@ -719,11 +719,8 @@ struct Long : P {
     static constexpr int kMinBlocks = 5;
 };
 constexpr double kLongSegments = 16.0;
-#ifndef CF_MEDIUM_TILES
-#define CF_MEDIUM_TILES (148 * 12)
-#endif
 constexpr int kWideTiles = 148 * 2;
-constexpr int kMediumTiles = CF_MEDIUM_TILES;
+constexpr int kMediumTiles = kStagedMaxTiles;
 
 template <class Q>
 int launch_variant(const Q& pol, const pass::Jds& L, const pass::Tiles& T, const int32_t* done, cudaStream_t st,
@@ -740,8 +737,8 @@ template <class P>
 int launch_pass(const P& pol, const pass::Jds& L, const pass::Tiles& T, const int32_t* done, cudaStream_t st,
                 int* grid_out = nullptr, double avg_len = 0.0) {
     if (T.n_tiles == 0) return CF_OK;
-    if (T.n_tiles <= kWideTiles) return launch_variant(Wide<P>{pol}, L, T, done, st, grid_out);
-    if (T.n_tiles <= kMediumTiles) return launch_variant(Medium<P>{pol}, L, T, done, st, grid_out);
+    if (T.stageable && T.n_tiles <= kWideTiles) return launch_variant(Wide<P>{pol}, L, T, done, st, grid_out);
+    if (T.stageable && T.n_tiles <= kMediumTiles) return launch_variant(Medium<P>{pol}, L, T, done, st, grid_out);
     if constexpr (P::kUnroll < 4) {
         if (avg_len >= kLongSegments) return launch_variant(Long<P>{pol}, L, T, done, st, grid_out);
     }
@@ -933,7 +930,8 @@ int launch_spmv_cols_range(cf_plan* p, const double* y, double* x, int64_t col_l
     ColSpmv c{};
     c.g_ = y;
     c.y = x;
-    return launch_pass(c, col_jds(p), pass::Tiles{p->col_tb.p + t0, (int32_t)(t1 - t0)}, nullptr, p->stream);
+    return launch_pass(c, col_jds(p), pass::Tiles{p->col_tb.p + t0, (int32_t)(t1 - t0), !p->col_large_tiles}, nullptr,
+                       p->stream);
 }
 
 int launch_report(cf_plan* p, double mu, bool ax_ready, const cf_config* cfg, int64_t k, int64_t slot,

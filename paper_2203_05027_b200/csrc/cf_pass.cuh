@@ -250,6 +250,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 struct Tiles {
     const int4* tb;
     int32_t n_tiles;
+    int32_t stageable = 1;   // every tile fits a TileStage (cut at kPCap nonzeros)
 };
 
 // The JDS layout of a pass: idx/val in warp-local jagged-diagonal order inside

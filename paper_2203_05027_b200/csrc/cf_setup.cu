@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(kTileSeg) k_build_jds(const int32_t* ptr, cons
 // segment gets a (long) tile of its own. `longs` lists the long segments in
 // increasing order; the nonzero budget is found by binary search on ptr.
 void tile_starts(const int32_t* ptr, int64_t s_begin, int64_t s_end, const std::vector<int64_t>& longs,
-                 std::vector<int64_t>& starts) {
+                 std::vector<int64_t>& starts, int32_t cap = kTileNnz) {
     size_t li = std::lower_bound(longs.begin(), longs.end(), s_begin) - longs.begin();
     int64_t s = s_begin;
     while (s < s_end) {
@@ -239,8 +239,8 @@ void tile_starts(const int32_t* ptr, int64_t s_begin, int64_t s_end, const std::
         }
         int64_t e = std::min<int64_t>(s_end, s + kTileSeg);
         if (li < longs.size()) e = std::min<int64_t>(e, longs[li]);
-        // last e with ptr[e] - ptr[s] <= kTileNnz (at least s + 1: a short segment fits alone)
-        const int32_t* hi = std::upper_bound(ptr + s + 1, ptr + e + 1, ptr[s] + kTileNnz);
+        // last e with ptr[e] - ptr[s] <= cap (at least s + 1: a short segment fits alone)
+        const int32_t* hi = std::upper_bound(ptr + s + 1, ptr + e + 1, ptr[s] + cap);
         s = std::max<int64_t>(s + 1, (int64_t)(hi - ptr) - 1);
     }
 }
@@ -342,11 +342,23 @@ int build_tiles(cf_plan* p, const int64_t* sizes, int64_t nb) {
     std::vector<int64_t> rstarts;
     rstarts.reserve(nsr / kTileSeg + 16);
     p->row_panel_tile.assign(p->n_panels + 1, 0);
-    for (int pn = 0; pn < p->n_panels; ++pn) {
-        p->row_panel_tile[pn] = (int64_t)rstarts.size();
-        tile_starts(rp, (int64_t)pn * m, (int64_t)(pn + 1) * m, rlong, rstarts);
-    }
-    p->row_panel_tile[p->n_panels] = (int64_t)rstarts.size();
+    auto cut_rows = [&](int32_t cap) {
+        rstarts.clear();
+        for (int pn = 0; pn < p->n_panels; ++pn) {
+            p->row_panel_tile[pn] = (int64_t)rstarts.size();
+            tile_starts(rp, (int64_t)pn * m, (int64_t)(pn + 1) * m, rlong, rstarts, cap);
+        }
+        p->row_panel_tile[p->n_panels] = (int64_t)rstarts.size();
+    };
+    // a pass whose launches get more tiles than the staged dispatch takes runs
+    // unstaged: cut it again with the larger nonzero budget
+    // (env: CF_NO_LARGE_TILES off, CF_FORCE_LARGE_TILES on whatever the size -- tests)
+    const bool large_ok = kTileNnzLarge > kTileNnz && !getenv("CF_NO_LARGE_TILES");
+    const bool large_force = large_ok && getenv("CF_FORCE_LARGE_TILES");
+    cut_rows(kTileNnz);
+    p->row_large_tiles =
+        large_force || (large_ok && (int64_t)rstarts.size() > (int64_t)kStagedMaxTiles * p->n_panels);
+    if (p->row_large_tiles) cut_rows(kTileNnzLarge);
     std::vector<int4> rtb;
     tile_table(rp, rstarts, nsr, rtb);
     p->row_tiles = (int64_t)rtb.size() - 1;
@@ -356,73 +368,81 @@ int build_tiles(cf_plan* p, const int64_t* sizes, int64_t nb) {
     // cp below is the LAST band's pointer array in column coordinates.
     std::vector<int64_t> cstarts;
     std::vector<int32_t> tcone, tbig, big, cone_ptr;
-    p->col_band_tile.assign(B + 1, 0);
-    for (int bd = 0; bd + 1 < B; ++bd) {
-        p->col_band_tile[bd] = (int64_t)cstarts.size();
-        tile_starts(cpall, (int64_t)bd * n, (int64_t)(bd + 1) * n, clong, cstarts);
-    }
-    p->col_band_tile[B - 1] = (int64_t)cstarts.size();
-    const int64_t last_off = (int64_t)(B - 1) * n;
-    const int32_t* cp = cpall + last_off;
-    const size_t last_first = cstarts.size();
-    std::vector<int64_t> clong_last;   // the last band's long segments in column coordinates
-    for (int64_t s : clong)
-        if (s >= last_off) clong_last.push_back(s - last_off);
-    std::vector<int64_t> lstarts;
-    if (p->all_unit) {
-        tile_starts(cp, 0, n, clong_last, lstarts);
-    } else {
-        cone_ptr.resize(nb + 1);
-        int64_t col = 0;
-        for (int64_t q = 0; q < nb; ++q) {
-            cone_ptr[q] = (int32_t)col;
-            col += sizes[q];
+    auto cut_cols = [&](int32_t cap) {
+        cstarts.clear();
+        tcone.clear();
+        tbig.clear();
+        big.clear();
+        cone_ptr.clear();
+        p->col_band_tile.assign(B + 1, 0);
+        for (int bd = 0; bd + 1 < B; ++bd) {
+            p->col_band_tile[bd] = (int64_t)cstarts.size();
+            tile_starts(cpall, (int64_t)bd * n, (int64_t)(bd + 1) * n, clong, cstarts, cap);
         }
-        cone_ptr[nb] = (int32_t)col;
-        int64_t q = 0;
-        while (q < nb) {
-            const int64_t c0 = cone_ptr[q];
-            if (sizes[q] > kSmallCone) {
-                const size_t before = lstarts.size();
-                tile_starts(cp, c0, c0 + sizes[q], clong_last, lstarts);
-                for (size_t t = before; t < lstarts.size(); ++t) {
-                    tcone.push_back((int32_t)q);
-                    tbig.push_back((int32_t)big.size());
-                }
-                big.push_back((int32_t)q);
-                ++q;
-                continue;
+        p->col_band_tile[B - 1] = (int64_t)cstarts.size();
+        const int64_t last_off = (int64_t)(B - 1) * n;
+        const int32_t* cp = cpall + last_off;
+        std::vector<int64_t> clong_last;   // the last band's long segments in column coordinates
+        for (int64_t s : clong)
+            if (s >= last_off) clong_last.push_back(s - last_off);
+        std::vector<int64_t> lstarts;
+        if (p->all_unit) {
+            tile_starts(cp, 0, n, clong_last, lstarts, cap);
+        } else {
+            cone_ptr.resize(nb + 1);
+            int64_t col = 0;
+            for (int64_t q = 0; q < nb; ++q) {
+                cone_ptr[q] = (int32_t)col;
+                col += sizes[q];
             }
-            int64_t q1 = q + 1;
-            auto cone_ok = [&](int64_t qq) {  // no column of the cone needs a long tile
-                for (int64_t c = cone_ptr[qq]; c < cone_ptr[qq] + sizes[qq]; ++c)
-                    if (cp[c + 1] - cp[c] > kTileDiag) return false;
-                return true;
-            };
-            if (!cone_ok(q)) {  // cone with a very long column: treat like a big cone (k_big_cone)
-                const size_t before = lstarts.size();
-                tile_starts(cp, c0, c0 + sizes[q], clong_last, lstarts);
-                for (size_t t = before; t < lstarts.size(); ++t) {
-                    tcone.push_back((int32_t)q);
-                    tbig.push_back((int32_t)big.size());
+            cone_ptr[nb] = (int32_t)col;
+            int64_t q = 0;
+            while (q < nb) {
+                const int64_t c0 = cone_ptr[q];
+                if (sizes[q] > kSmallCone) {
+                    const size_t before = lstarts.size();
+                    tile_starts(cp, c0, c0 + sizes[q], clong_last, lstarts, cap);
+                    for (size_t t = before; t < lstarts.size(); ++t) {
+                        tcone.push_back((int32_t)q);
+                        tbig.push_back((int32_t)big.size());
+                    }
+                    big.push_back((int32_t)q);
+                    ++q;
+                    continue;
                 }
-                big.push_back((int32_t)q);
-                ++q;
-                continue;
+                int64_t q1 = q + 1;
+                auto cone_ok = [&](int64_t qq) {  // no column of the cone needs a long tile
+                    for (int64_t c = cone_ptr[qq]; c < cone_ptr[qq] + sizes[qq]; ++c)
+                        if (cp[c + 1] - cp[c] > kTileDiag) return false;
+                    return true;
+                };
+                if (!cone_ok(q)) {  // cone with a very long column: treat like a big cone (k_big_cone)
+                    const size_t before = lstarts.size();
+                    tile_starts(cp, c0, c0 + sizes[q], clong_last, lstarts, cap);
+                    for (size_t t = before; t < lstarts.size(); ++t) {
+                        tcone.push_back((int32_t)q);
+                        tbig.push_back((int32_t)big.size());
+                    }
+                    big.push_back((int32_t)q);
+                    ++q;
+                    continue;
+                }
+                while (q1 < nb && sizes[q1] <= kSmallCone && cone_ptr[q1] + sizes[q1] - c0 <= kTileSeg &&
+                       cp[cone_ptr[q1] + sizes[q1]] - cp[c0] <= cap && cone_ok(q1))
+                    ++q1;
+                lstarts.push_back(c0);
+                tcone.push_back((int32_t)q);
+                tbig.push_back(-1);
+                q = q1;
             }
-            while (q1 < nb && sizes[q1] <= kSmallCone && cone_ptr[q1] + sizes[q1] - c0 <= kTileSeg &&
-                   cp[cone_ptr[q1] + sizes[q1]] - cp[c0] <= kTileNnz && cone_ok(q1))
-                ++q1;
-            lstarts.push_back(c0);
-            tcone.push_back((int32_t)q);
-            tbig.push_back(-1);
-            q = q1;
+            tcone.push_back((int32_t)nb);
         }
-        tcone.push_back((int32_t)nb);
-    }
-    for (int64_t s : lstarts) cstarts.push_back(s + last_off);
-    p->col_band_tile[B] = (int64_t)cstarts.size();
-    (void)last_first;
+        for (int64_t s : lstarts) cstarts.push_back(s + last_off);
+        p->col_band_tile[B] = (int64_t)cstarts.size();
+    };
+    cut_cols(kTileNnz);
+    p->col_large_tiles = large_force || (large_ok && (int64_t)cstarts.size() > (int64_t)kStagedMaxTiles * B);
+    if (p->col_large_tiles) cut_cols(kTileNnzLarge);
     std::vector<int4> ctb;
     tile_table(cpall, cstarts, nsc, ctb);
     p->col_tile_start.resize(ctb.size());

@@ -63,11 +63,63 @@ def _distinct_positions(torch, gen, total: int, count: int, device):
     return pos
 
 
+def rls_arrays(torch, gen, m: int, n: int, density: float, device):
+    """Robust least squares in SOC form (the secondary mixed-cone instance).
+
+    min sum_i t_i + 0.01 * 1^T (x+ + x-)   s.t.   u_i - F_i (x+ - x-) = -g_i,
+    (t_i, u_i) in K4 (i < K), x+, x- >= 0 (p each).
+
+    m = 3K rows (row 3i+r is component r of u_i); n = 4K + 2p columns: cone i owns
+    [4i, 4i+4), then x+ and x-. Each row holds u's 1.0 plus k F entries, each stored
+    twice (+f on x+, -f on x-), so density*n = 1 + 2k. The k columns of a row are
+    h, h+s, ..., h+(k-1)s mod p with s < p/k, hence distinct. The t columns have no
+    entries. Returns (rows, cols, vals, b, c, block_sizes) on `device`."""
+    K = m // 3
+    p2 = n - 4 * K
+    if m != 3 * K or K < 1 or p2 < 2 or p2 % 2:
+        raise ValueError("rls needs m = 3K and n = 4K + 2p, p >= 1")
+    p = p2 // 2
+    k = int(min(max(1, round((density * n - 1.0) / 2.0)), p))
+    r = torch.arange(m, device=device, dtype=torch.int64)
+    h = torch.randint(0, p, (m, 1), generator=gen, device=device, dtype=torch.int64)
+    s = torch.randint(1, max(2, p // k + 1), (m, 1), generator=gen, device=device, dtype=torch.int64)
+    j = (h + s * torch.arange(k, device=device, dtype=torch.int64)) % p            # [m, k] distinct per row
+    f = torch.randn(m, k, generator=gen, device=device, dtype=torch.float64)
+    while True:
+        zero = f == 0.0
+        nz = int(zero.sum())
+        if nz == 0:
+            break
+        f[zero] = torch.randn(nz, generator=gen, device=device, dtype=torch.float64)
+    u_col = 4 * (r // 3) + 1 + r % 3
+    rows = torch.cat([r, r.repeat_interleave(k), r.repeat_interleave(k)])
+    cols = torch.cat([u_col, (4 * K + j).reshape(-1), (4 * K + p + j).reshape(-1)])
+    vals = torch.cat([torch.ones(m, device=device, dtype=torch.float64), f.reshape(-1), -f.reshape(-1)])
+    b = -torch.randn(m, generator=gen, device=device, dtype=torch.float64)
+    c = torch.zeros(n, device=device, dtype=torch.float64)
+    c[0:4 * K:4] = 1.0
+    c[4 * K:] = 0.01
+    sizes = np.concatenate([np.full(K, 4, dtype=np.int64), np.ones(2 * p, dtype=np.int64)])
+    return rows, cols, vals, b, c, sizes
+
+
 def generate_device(m: int, n: int, density: float, cone_kind: str = "lp", seed: int = 0,
                     bounded_mode: bool = True, keep_plan: bool = True, stream: int | None = None) -> DeviceInstance:
     import torch
 
     dev = torch.device("cuda")
+    if cone_kind == "rls":
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(int(seed))
+        rows, cols, vals, b, c, sizes = rls_arrays(torch, gen, m, n, density, dev)
+        o = int(vals.numel())
+        torch.cuda.synchronize()
+        plan = DevicePlan.from_device(m, n, o, rows.data_ptr(), cols.data_ptr(), vals.data_ptr(), b.data_ptr(),
+                                      c.data_ptr(), sizes, stream=stream)
+        inst = DeviceInstance(m, n, o, cone_kind, rows, cols, vals, b, c, sizes, plan if keep_plan else None)
+        if not keep_plan:
+            plan.close()
+        return inst
     o = int(round(m * n * density))
     if o < 1:
         raise ValueError("instance has no nonzeros")

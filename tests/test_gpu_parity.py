@@ -429,6 +429,58 @@ def test_column_bands_solve_bit_identical(monkeypatch):
         assert banded.trace == ref.trace
 
 
+@pytest.mark.parametrize("case", ITERATE_CASES)
+def test_large_tiles_match_reference(case, monkeypatch):
+    """Tiles cut with the large nonzero budget (kTileNnzLarge, used by passes too big for
+    the staged dispatch; forced here on the golden cases) keep A x and A^T y bit-identical
+    and the iterates within the parity tolerance, for every cone layout."""
+    import torch
+
+    monkeypatch.setenv("CF_FORCE_LARGE_TILES", "1")
+    d = load_golden(f"iterates_{case}.npz")
+    p = problem_from(d)
+    f = oracle.build_factors(p.A)
+    rng = np.random.default_rng(21)
+    x, y = rng.standard_normal(f.n), rng.standard_normal(f.m)
+    mu = float(d["mu"])
+    with _plan(p) as plan:
+        ax = torch.empty(f.m, dtype=torch.float64, device="cuda")
+        aty = torch.empty(f.n, dtype=torch.float64, device="cuda")
+        plan.apply_A(_device_vec(x).data_ptr(), ax.data_ptr())
+        plan.apply_At(_device_vec(y).data_ptr(), aty.data_ptr())
+        np.testing.assert_array_equal(ax.cpu().numpy(), oracle.apply_U(f, oracle.apply_Vt(f, x)))
+        np.testing.assert_array_equal(aty.cpu().numpy(), oracle.apply_V(f, oracle.apply_Ut(f, y)))
+        plan.set_state(mu, init_from(d))
+        done = 0
+        for k in d["keep"]:
+            plan.iterate(mu, int(k) - done)
+            done = int(k)
+            st = plan.get_state()
+            for key in STATE_KEYS:
+                assert rel_err(st[key], d[f"k{k}_{key}"]) <= ITER_TOL, (case, int(k), key)
+
+
+def test_large_tiles_solve_bit_identical(monkeypatch):
+    """A solve on large tiles returns exactly the default tiling's iterates. Report norms
+    sum per-CTA partials, whose grouping follows the tiling, so they agree to rounding."""
+    from paper_2203_05027_b200 import GenSpec, SolverConfig, generate, solve
+
+    for kind in ("lp", "socp4"):
+        q = generate(GenSpec(300, 900, 0.05, kind, seed=14))   # ~45 nonzeros per row
+        cfg = SolverConfig(max_iters=500)
+        monkeypatch.setenv("CF_FORCE_LARGE_TILES", "1")
+        large = solve(q, cfg)
+        monkeypatch.delenv("CF_FORCE_LARGE_TILES")
+        ref = solve(q, cfg)
+        np.testing.assert_array_equal(large.x, ref.x)
+        np.testing.assert_array_equal(large.lam, ref.lam)
+        assert len(large.trace) == len(ref.trace)
+        for a, b in zip(large.trace, ref.trace):
+            assert a.status == b.status and a.iter == b.iter
+            for fld in REPORT_FIELDS[1:]:
+                assert _scalar_rel(getattr(a, fld), getattr(b, fld)) <= 1e-12
+
+
 @pytest.mark.parametrize("shape", ["no_nonzeros", "1x1", "one_dense_row", "one_dense_column", "empty_rows_cols"])
 def test_degenerate_shapes_match_oracle(shape):
     """Shapes at the edges of the tiling: no nonzeros, 1x1, one dense row / column (long

@@ -1,0 +1,58 @@
+"""The robust-least-squares SOC instance (SURVEY §8d secondary mixed-cone config, bench c3m).
+
+CPU: the generator's structure. GPU: solve() on a small instance against the oracle
+(same iteration count, x/lam to rel_err 1e-8, as the other solve parity tests)."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import rel_err
+
+from paper_2203_05027_b200.devgen import rls_arrays
+from paper_2203_05027_b200.problem import ConeSpec, ProblemInstance, TripletMatrix, validate
+
+
+def _instance(K, seed=0, per_row=13):
+    m, n = 3 * K, 5 * K
+    g = torch.Generator()
+    g.manual_seed(seed)
+    rows, cols, vals, b, c, sizes = rls_arrays(torch, g, m, n, per_row / n, "cpu")
+    return ProblemInstance(TripletMatrix(m, n, rows.numpy(), cols.numpy(), vals.numpy()), b.numpy(), c.numpy(),
+                           ConeSpec(sizes))
+
+
+def test_rls_structure():
+    K = 500
+    p = _instance(K)
+    assert validate(p).ok                      # distinct cells, nonzero finite values, cone sum = n
+    a = p.A
+    assert a.nnz == 3 * K * 13
+    sizes = np.asarray(p.cones.block_sizes)
+    assert (sizes[:K] == 4).all() and (sizes[K:] == 1).all() and sizes.sum() == 5 * K
+    cols = np.asarray(a.cols)
+    assert not np.isin(np.arange(0, 4 * K, 4), cols).any()     # the t columns are free of A
+    np.testing.assert_array_equal(p.c[0:4 * K:4], 1.0)
+    # +f on x+ and -f on x- for every F entry
+    rows, vals = np.asarray(a.rows), np.asarray(a.vals)
+    plus = cols >= 4 * K
+    xp = plus & (cols < 4 * K + K // 2)
+    xm = cols >= 4 * K + K // 2
+    key_p = rows[xp] * K + (cols[xp] - 4 * K)
+    key_m = rows[xm] * K + (cols[xm] - 4 * K - K // 2)
+    op, om = np.argsort(key_p), np.argsort(key_m)
+    np.testing.assert_array_equal(key_p[op], key_m[om])
+    np.testing.assert_array_equal(vals[xp][op], -vals[xm][om])
+
+
+@pytest.mark.gpu
+def test_rls_solve_matches_oracle():
+    import oracle
+    from paper_2203_05027_b200 import SolverConfig, solve
+
+    p = _instance(400, seed=3)
+    cfg = SolverConfig(eps_prim=1e-4, eps_dual=1e-4, eps_gap=1e-4, max_iters=20000)
+    ox, olam, otr, _ = oracle.solve(p, cfg)
+    res = solve(p, cfg)
+    assert res.report.iter == otr[-1]["iter"] and res.report.status == otr[-1]["status"] == "solved"
+    assert rel_err(res.x, ox) <= 1e-8 and rel_err(res.lam, olam) <= 1e-8
