@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Benchmark of the B200 iteration engine on BASELINE.json's headline workload.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c1] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c3m|c1|c4|c5] [--impl ours|reference]
 
 A *step* is one ADMM iteration (solver.py:313-317) of the C2 LP
 (m=5M, n=10M, o=100M, fp64) with the solve loop's report cadence
