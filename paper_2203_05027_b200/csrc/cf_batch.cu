@@ -206,8 +206,12 @@ __global__ void __launch_bounds__(kBT, CF_BATCH_MINB) k_batch(const BatchArgs a)
         __syncthreads();
         int nrep = 0;
         cf_report last{};
+        // reports at k % check_every == 0 or k == max_iters (solver.py:319), tracked by a
+        // countdown instead of a 64-bit modulo (a software division) per iteration
+        int64_t next_report = cfg.check_every < cfg.max_iters ? cfg.check_every : cfg.max_iters;
         for (int64_t k = 1; k <= cfg.max_iters; ++k) {
-            const bool report = (k % cfg.check_every == 0) || (k == cfg.max_iters);
+            const bool report = k == next_report;
+            if (report) next_report = (k + cfg.check_every < cfg.max_iters) ? k + cfg.check_every : cfg.max_iters;
             // ---- column pass: x_update, z_update, delta update (solver.py:168-176,186-188,196)
             for (int j = t; j < n; j += kBT) {
                 const int p0 = colptr[j], p1 = colptr[j + 1];
