@@ -100,6 +100,43 @@ def test_library_exports_every_header_symbol():
     assert lib.cf_abi_version() == 1
 
 
+def test_plan_create_argument_checks():
+    """cf_plan_create rejects bad sizes before touching CUDA: negative sizes, the int32 limit
+    of the tile indices (m, n, o < 2^31), NULL arrays and cone sizes that do not sum to n."""
+    import ctypes
+
+    L = _lib.lib()
+    out = ctypes.c_void_p()
+    chk = _lib.CfChecks()
+    sizes = (ctypes.c_int64 * 2)(2, 2)
+    one = (ctypes.c_int64 * 1)(0)
+    val = (ctypes.c_double * 1)(1.0)
+    cvec = (ctypes.c_double * 5)(1.0, 1.0, 1.0, 1.0, 1.0)   # c for every n below
+
+    def create(m, n, o, rows, vals, nb, bs):
+        return L.cf_plan_create(m, n, o, rows, rows, vals, vals, cvec, nb, bs, 0, None, ctypes.byref(chk),
+                                ctypes.byref(out))
+
+    cases = [
+        ((-1, 1, 1, one, val, 0, None), "negative size"),
+        ((1, 2 ** 31, 1, one, val, 0, None), "< 2\\^31"),
+        ((1, 1, 2 ** 31 - 1, one, val, 0, None), "< 2\\^31"),
+        ((1, 1, 1, None, val, 0, None), "NULL input array"),
+        ((1, 4, 1, one, val, 2, ctypes.cast(sizes, ctypes.c_void_p)), None),   # sums to 4: passes the checks
+        ((1, 5, 1, one, val, 2, ctypes.cast(sizes, ctypes.c_void_p)), "cone sizes sum 4 != n=5"),
+    ]
+    for args, msg in cases:
+        rc = create(*args)
+        if msg is None:
+            assert rc != _lib.CF_EINVAL or "cone" not in _lib.last_error()
+            if rc == 0:
+                L.cf_plan_destroy(out)
+            continue
+        assert rc == _lib.CF_EINVAL, (args, rc)
+        assert re.search(msg, _lib.last_error()), (msg, _lib.last_error())
+        assert not out.value
+
+
 def test_no_gpu_fails_loudly():
     if _lib.device_count() > 0:
         pytest.skip("a GPU is visible")
