@@ -419,7 +419,8 @@ def run_sharded_bench(args, spec, rank, world, local_rank):
     o_t = torch.tensor([float(o_local)], dtype=torch.float64, device="cuda")
     dist.all_reduce(o_t)
     warm = SolverConfig(max_iters=max(args.warmup, 1), check_every=25, eps_prim=0.0, eps_dual=0.0, eps_gap=0.0)
-    run_sharded(be, row_cuts, col_cuts, warm, bn, cn, gather_result=False)
+    p2p = args.c5_mode == "p2p"
+    run_sharded(be, row_cuts, col_cuts, warm, bn, cn, gather_result=False, p2p=p2p)
     # fresh state for the timed run
     be.close()
     del be
@@ -430,7 +431,7 @@ def run_sharded_bench(args, spec, rank, world, local_rank):
     dist.barrier()
     torch.cuda.synchronize()
     tim = {}
-    res = run_sharded(be, row_cuts, col_cuts, cfg, bn, cn, timing=tim, gather_result=False)
+    res = run_sharded(be, row_cuts, col_cuts, cfg, bn, cn, timing=tim, gather_result=False, p2p=p2p)
     torch.cuda.synchronize()
     assert tim["iters"] == args.steps and res.report.status == "max_iters", (tim, res.report)
     ms = torch.tensor([tim["loop_ms"]], dtype=torch.float64, device="cuda")
@@ -446,7 +447,9 @@ def run_sharded_bench(args, spec, rank, world, local_rank):
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (per-rank GPU generator, reference recipe)",
             "config": {"workload": spec["workload"] if scale == 1.0 else f"C5 structure scaled by {scale}: m={m} n={n}",
-                       "m": m, "n": n, "o": o_total, "parallelism": f"row-sharded x{world} (per-slice NCCL reduce overlapped with the column pass + all-gather)"},
+                       "m": m, "n": n, "o": o_total, "parallelism": f"row-sharded x{world} " + (
+                           "(fused P2P step: partial A^T h in peer memory, one reduce+update+broadcast kernel)"
+                           if p2p else "(per-slice NCCL reduce overlapped with the column pass + all-gather)")},
             # per iteration: partial A^T h, column update, row pass (per panel); + report kernels every 25
             "gpu_launches": args.steps * 4 + (args.steps // 25) * 5,
             "iteration_roofline": {"bytes_per_iteration_total": row_b + col_b,
@@ -599,7 +602,7 @@ def main():
     ap.add_argument("--e2e-max-iters", type=int, default=0)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--c5-scale", type=float, default=1.0, help="shrink C5 (m, n) by this factor (same nnz/row)")
-    ap.add_argument("--c5-mode", choices=("rows", "cols"), default="rows",
+    ap.add_argument("--c5-mode", choices=("rows", "cols", "p2p"), default="rows",
                     help="C5: split A's rows (exchange n-vectors) or columns (all-reduce the m-vector A x)")
     args = ap.parse_args()
     if args.warmup < 3:

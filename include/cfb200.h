@@ -249,6 +249,25 @@ int cf_plan_row_parts(cf_plan* plan, double* out5);
 int cf_column_update(int64_t n, const double* ath, const double* cnt, const double* c, double* x,
                      double* z, double* delta, double mu, int64_t n_blocks, const int32_t* cone_ptr,
                      void* stream);
+/* cf_column_update fused with its collectives for the row-sharded step over NVLink peer
+ * memory (SURVEY §8e "fused" row; replaces reduce-scatter -> cf_column_update ->
+ * all-gather, solver.py:168-176,186-188,196). parts: device array of `world` pointers to
+ * each rank's partial A^T h at this slice (P2P-readable, summed in rank order); x_dst:
+ * device array of n_dst pointers to the x replicas at this slice, each receiving x+.
+ * The caller orders the partials before and the replicas after with a cross-rank barrier. */
+int cf_column_update_p2p(int64_t n, const double* const* parts, int32_t world, const double* cnt,
+                         const double* c, double* x, double* z, double* delta, double mu, int64_t n_blocks,
+                         const int32_t* cone_ptr, double* const* x_dst, int32_t n_dst, void* stream);
+/* Peer memory for the fused step: a cudaMalloc'ed buffer (+64 bytes slack, zeroed) and its
+ * 64-byte cudaIpcMemHandle_t; open / close a peer's buffer in this process. */
+int cf_ipc_alloc(int64_t bytes, void** dev_ptr, void* handle64);
+int cf_ipc_free(void* dev_ptr);
+int cf_ipc_open(const void* handle64, void** dev_ptr);
+int cf_ipc_close(void* dev_ptr);
+/* Run the plan on an external x buffer (n doubles + 64 bytes, e.g. from cf_ipc_alloc, so
+ * peers can store x+ into it); the current x is copied over. NULL: back to the plan's own
+ * buffer (copied back). The external buffer stays the caller's. */
+int cf_plan_bind_x(cf_plan* plan, double* x_ext);
 /* column part of compute_report on a slice from the reduced A^T lam: out = {sum dual^2,
  * max|dual|, sum stat^2, max|stat|, max|A^T lam|, sum c*x, max|x-z|, nonfinite} (host, 8) */
 int cf_column_parts(int64_t n, const double* atl, const double* c, const double* x, const double* z,

@@ -128,6 +128,13 @@ SIGNATURES = {
     "cf_format_double": (c_int, [c_double, c_char_p]),
     "cf_coneprob_write": (c_int, [c_char_p, c_int64, c_int64, c_int64, _P, _P, _P, _P, _P, c_int64, _P, c_int]),
     "cf_solution_write": (c_int, [c_char_p, c_char_p, _P, c_int64, _P, c_int64, c_int]),
+    "cf_column_update_p2p": (c_int, [c_int64, _P, c_int32, _P, _P, _P, _P, _P, c_double, c_int64, _P, _P, c_int32,
+                                     _P]),
+    "cf_ipc_alloc": (c_int, [c_int64, POINTER(c_void_p), c_void_p]),
+    "cf_ipc_free": (c_int, [_P]),
+    "cf_ipc_open": (c_int, [c_void_p, POINTER(c_void_p)]),
+    "cf_ipc_close": (c_int, [_P]),
+    "cf_plan_bind_x": (c_int, [_P, _P]),
 }
 
 _lib = None

@@ -112,6 +112,7 @@ int cf_plan_destroy(cf_plan* p) {
     if (p->ev1) cudaEventDestroy(p->ev1);
     for (cudaEvent_t e : p->prof_events) cudaEventDestroy(e);
     cudaStream_t st = p->own_stream ? p->stream : nullptr;
+    if (p->x_own) p->x.p = p->x_own;   // an external x (cf_plan_bind_x) belongs to the caller
     delete p;  // DevBuf destructors free device memory
     if (st) cudaStreamDestroy(st);
     return CF_OK;
@@ -491,6 +492,70 @@ int cf_column_update(int64_t n, const double* ath, const double* cnt, const doub
                      double* delta, double mu, int64_t n_blocks, const int32_t* cone_ptr, void* stream) {
     CF_TRY(check_mu(mu, "cf_column_update"));
     CF_TRY(launch_col_update(n, ath, cnt, c, x, z, delta, mu, n_blocks, cone_ptr, (cudaStream_t)stream));
+    return CF_OK;
+}
+
+int cf_column_update_p2p(int64_t n, const double* const* parts, int32_t world, const double* cnt, const double* c,
+                         double* x, double* z, double* delta, double mu, int64_t n_blocks, const int32_t* cone_ptr,
+                         double* const* x_dst, int32_t n_dst, void* stream) {
+    CF_TRY(check_mu(mu, "cf_column_update_p2p"));
+    if (world < 1 || n_dst < 0 || !parts || (n_dst > 0 && !x_dst)) {
+        set_error("cf_column_update_p2p: world >= 1 partials and n_dst >= 0 destinations required");
+        return CF_EINVAL;
+    }
+    CF_TRY(launch_col_update_p2p(n, parts, world, cnt, c, x, z, delta, mu, n_blocks, cone_ptr, x_dst, n_dst,
+                                 (cudaStream_t)stream));
+    return CF_OK;
+}
+
+int cf_ipc_alloc(int64_t bytes, void** dev_ptr, void* handle) {
+    if (!dev_ptr || !handle || bytes < 0) {
+        set_error("cf_ipc_alloc: NULL output or negative size");
+        return CF_EINVAL;
+    }
+    *dev_ptr = nullptr;
+    CF_CUDA(cudaMalloc(dev_ptr, (size_t)bytes + 64));   // +64: the pass engine reads 16-byte supersets
+    CF_CUDA(cudaMemset(*dev_ptr, 0, (size_t)bytes + 64));
+    cudaIpcMemHandle_t h;
+    CF_CUDA(cudaIpcGetMemHandle(&h, *dev_ptr));
+    memcpy(handle, &h, sizeof(h));
+    return CF_OK;
+}
+
+int cf_ipc_free(void* dev_ptr) {
+    if (dev_ptr) CF_CUDA(cudaFree(dev_ptr));
+    return CF_OK;
+}
+
+int cf_ipc_open(const void* handle, void** dev_ptr) {
+    if (!dev_ptr || !handle) {
+        set_error("cf_ipc_open: NULL argument");
+        return CF_EINVAL;
+    }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    CF_CUDA(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return CF_OK;
+}
+
+int cf_ipc_close(void* dev_ptr) {
+    if (dev_ptr) CF_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+    return CF_OK;
+}
+
+int cf_plan_bind_x(cf_plan* p, double* x_ext) {
+    CF_TRY(check_plan(p, "cf_plan_bind_x"));
+    const size_t bytes = (size_t)std::max<int64_t>(p->n, 1) * sizeof(double);
+    if (x_ext) {
+        if (!p->x_own) p->x_own = p->x.p;
+        if (x_ext != p->x.p) CF_CUDA(cudaMemcpyAsync(x_ext, p->x.p, bytes, cudaMemcpyDeviceToDevice, p->stream));
+        p->x.p = x_ext;
+    } else if (p->x_own) {
+        CF_CUDA(cudaMemcpyAsync(p->x_own, p->x.p, bytes, cudaMemcpyDeviceToDevice, p->stream));
+        p->x.p = p->x_own;
+        p->x_own = nullptr;
+    }
+    CF_CUDA(cudaStreamSynchronize(p->stream));
     return CF_OK;
 }
 

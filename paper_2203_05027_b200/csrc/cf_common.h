@@ -188,6 +188,7 @@ struct cf_plan {
     cf::DevBuf<double> part_row, part_col;     // per-CTA partials
     cf::DevBuf<cf_report> report_slot;         // device report ring
     cf::DevBuf<int32_t> done;                  // device early-exit flag
+    double* x_own = nullptr;                   // cf_plan_bind_x: the plan's own x while x.p is external
     cf::DevBuf<int32_t> nf_flag;               // report: non-finite implicit y/gamma
     cf_report* host_reports = nullptr;         // pinned ring
     int64_t host_ring = 0;
@@ -248,6 +249,11 @@ int max_col_report_ctas();
 // row-sharded building blocks
 int launch_col_update(int64_t n, const double* ath, const double* cnt, const double* c, double* x, double* z,
                       double* delta, double mu, int64_t n_blocks, const int32_t* cone_ptr, cudaStream_t st);
+// the same update fed by `world` peer partials (summed in rank order) and storing x+ into
+// every rank's x replica (P2P over NVLink): reduce-scatter + update + all-gather in one kernel
+int launch_col_update_p2p(int64_t n, const double* const* parts, int world, const double* cnt, const double* c,
+                          double* x, double* z, double* delta, double mu, int64_t n_blocks, const int32_t* cone_ptr,
+                          double* const* x_dst, int n_dst, cudaStream_t st);
 int launch_col_parts(int64_t n, const double* atl, const double* c, const double* x, const double* z,
                      const double* delta, double* out8_dev, cudaStream_t st);
 int launch_row_parts(cf_plan* p, double* out5_dev);

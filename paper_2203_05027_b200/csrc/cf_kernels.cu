@@ -1078,6 +1078,34 @@ __global__ void k_col_update(int64_t n, const double* ath, const double* cnt, co
         }
     }
 }
+// k_col_update with the reduce and the broadcast fused in: A^T h of the slice is the sum of
+// the `world` ranks' partials read over P2P in rank order (deterministic), and x+ goes to
+// every rank's x replica. Only x crosses the link on the way out; z and delta stay local.
+__global__ void k_col_update_p2p(int64_t n, const double* const* parts, int world, const double* cnt,
+                                 const double* c, double* x, double* z, double* delta, double mu,
+                                 const int32_t* cone_ptr, double* wbuf, double* const* x_dst, int n_dst) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        double ath = parts[0][j];
+        for (int s = 1; s < world; ++s) ath = __dadd_rn(ath, parts[s][j]);
+        const double cj = cnt[j];
+        const double fv = 1.0 / (1.0 + cj);
+        const double xj = x[j], zj = z[j], dj = delta[j];
+        const double dm = dj / mu;
+        const double v = __dadd_rn(__dmul_rn(cj, xj), ath);
+        const double xp = fv * (((v + zj) + dm) - c[j] / mu);
+        const double w = xp - dm;
+        x[j] = xp;
+        for (int s = 0; s < n_dst; ++s) x_dst[s][j] = xp;
+        if (!cone_ptr) {
+            const double zp = w > 0.0 ? w : 0.0;
+            z[j] = zp;
+            delta[j] = dj + mu * (zp - xp);
+        } else {
+            wbuf[j] = w;
+        }
+    }
+    __threadfence_system();   // peer stores performed before the kernel retires
+}
 __global__ void k_cone_update(int64_t n_blocks, const int32_t* cone_ptr, const double* wbuf, const double* x,
                               double* z, double* delta, double mu) {
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n_blocks;
@@ -1161,6 +1189,23 @@ int launch_col_update(int64_t n, const double* ath, const double* cnt, const dou
     DevBuf<double> w;
     if (cone_ptr) CF_TRY(w.alloc(n));
     k_col_update<<<grid_for(n, 256), 256, 0, st>>>(n, ath, cnt, c, x, z, delta, mu, n_blocks, cone_ptr, w.p);
+    CF_LAUNCHED();
+    if (cone_ptr) {
+        k_cone_update<<<grid_for(n_blocks, 128), 128, 0, st>>>(n_blocks, cone_ptr, w.p, x, z, delta, mu);
+        CF_LAUNCHED();
+        CF_CUDA(cudaStreamSynchronize(st));  // w is released at return
+    }
+    return CF_OK;
+}
+
+int launch_col_update_p2p(int64_t n, const double* const* parts, int world, const double* cnt, const double* c,
+                          double* x, double* z, double* delta, double mu, int64_t n_blocks, const int32_t* cone_ptr,
+                          double* const* x_dst, int n_dst, cudaStream_t st) {
+    if (n == 0) return CF_OK;
+    DevBuf<double> w;
+    if (cone_ptr) CF_TRY(w.alloc(n));
+    k_col_update_p2p<<<grid_for(n, 256), 256, 0, st>>>(n, parts, world, cnt, c, x, z, delta, mu, cone_ptr, w.p,
+                                                       x_dst, n_dst);
     CF_LAUNCHED();
     if (cone_ptr) {
         k_cone_update<<<grid_for(n_blocks, 128), 128, 0, st>>>(n_blocks, cone_ptr, w.p, x, z, delta, mu);

@@ -182,6 +182,85 @@ class CudaRankBackend:
                                              self.n_blocks, self._p(self.cone_ptr) if self.cone_ptr is not None
                                              else None, self.stream.cuda_stream))
 
+    # -------------------------------------------------------------- fused P2P step
+    def enable_p2p(self, group, col_cuts):
+        """Peer buffers for the fused step: this rank's partial A^T h and x replica live in
+        cudaMalloc'ed, IPC-exported memory; every rank opens every other rank's pair. The plan
+        then runs on the replica (cf_plan_bind_x), which peers fill with their x+ slices."""
+        import ctypes
+
+        import torch.distributed as dist
+
+        from . import _lib
+
+        if getattr(self, "_p2p_own", None):
+            return
+        torch = self.torch
+        world = dist.get_world_size(group)
+        rank = dist.get_rank(group)
+        self._p2p_own, handles = [], []
+        for _ in range(2):   # partial, x replica
+            ptr, h = ctypes.c_void_p(), ctypes.create_string_buffer(64)
+            _lib.check(self.lib.cf_ipc_alloc(8 * max(self.n, 1), ctypes.byref(ptr), h))
+            self._p2p_own.append(ptr.value)
+            handles.append(h.raw)
+        everyone = [None] * world
+        if world > 1:
+            dist.all_gather_object(everyone, handles, group=group)
+        else:
+            everyone = [handles]
+        self._p2p_opened = []
+        peers = []
+        for s in range(world):
+            if s == rank:
+                peers.append(tuple(self._p2p_own))
+                continue
+            pair = []
+            for h in everyone[s]:
+                ptr = ctypes.c_void_p()
+                _lib.check(self.lib.cf_ipc_open(ctypes.create_string_buffer(h, 64), ctypes.byref(ptr)))
+                self._p2p_opened.append(ptr.value)
+                pair.append(ptr.value)
+            peers.append(tuple(pair))
+        off = 8 * self.lo
+        self.p2p_parts = torch.tensor([peers[s][0] + off for s in range(world)], dtype=torch.int64,
+                                      device=self.device)
+        self.p2p_xdst = torch.tensor([peers[s][1] + off for s in range(world)], dtype=torch.int64,
+                                     device=self.device)
+        self.p2p_world = world
+        self.p2p_partial = torch.as_tensor(_DevArray(self._p2p_own[0], self.n), device=self.device)
+        _lib.check(self.lib.cf_plan_bind_x(self.plan.handle, ctypes.c_void_p(self._p2p_own[1])))
+        self.x_full = torch.as_tensor(_DevArray(self._p2p_own[1], self.n), device=self.device)
+
+    def column_update_p2p(self, mu: float):
+        """Reduce (rank-order sum of the peers' partials) + column update + broadcast of x+
+        to every replica, one kernel (cf_column_update_p2p)."""
+        from . import _lib
+
+        _lib.check(self.lib.cf_column_update_p2p(
+            self.xs.numel(), self._p(self.p2p_parts), self.p2p_world, self._p(self.cnt_s), self._p(self.cs),
+            self._p(self.xs), self._p(self.zs), self._p(self.ds), float(mu), self.n_blocks,
+            self._p(self.cone_ptr) if self.cone_ptr is not None else None, self._p(self.p2p_xdst), self.p2p_world,
+            self.stream.cuda_stream))
+
+    def disable_p2p(self):
+        import ctypes
+
+        if not getattr(self, "_p2p_own", None):
+            return
+        from . import _lib
+
+        self.torch.cuda.synchronize()
+        _lib.check(self.lib.cf_plan_bind_x(self.plan.handle, None))
+        for ptr in self._p2p_opened:
+            self.lib.cf_ipc_close(ctypes.c_void_p(ptr))
+        for ptr in self._p2p_own:
+            self.lib.cf_ipc_free(ctypes.c_void_p(ptr))
+        self._p2p_own, self._p2p_opened = [], []
+        ptr, ln = ctypes.c_void_p(), ctypes.c_int64()
+        _lib.check(self.lib.cf_plan_vector(self.plan.handle, 0, ctypes.byref(ptr), ctypes.byref(ln)))
+        self.x_full = self.torch.as_tensor(_DevArray(ptr.value or 0, ln.value), device=self.device)
+
     def x_slice(self):
         return self.xs
 
@@ -219,6 +298,7 @@ class CudaRankBackend:
         return self.lam
 
     def close(self):
+        self.disable_p2p()
         self.plan.close()
 
 
@@ -231,10 +311,12 @@ def _cone_ptr_slice(p, lo: int, hi: int):
     return (starts[q0:q1 + 1] - lo).astype(np.int32)
 
 
-def solve_sharded(p, cfg: SolverConfig | None = None, group=None, backend_factory=None) -> SolveResult:
+def solve_sharded(p, cfg: SolverConfig | None = None, group=None, backend_factory=None,
+                  p2p: bool = False) -> SolveResult:
     """solve() with A's rows split over the ranks of ``group`` (every rank passes the same problem).
 
-    Cold start only. Returns the same SolveResult on every rank."""
+    Cold start only. Returns the same SolveResult on every rank. ``p2p``: the fused
+    peer-memory step (run_sharded) instead of NCCL reduce-scatter + all-gather."""
     import torch.distributed as dist
 
     cfg = cfg or SolverConfig()
@@ -247,19 +329,23 @@ def solve_sharded(p, cfg: SolverConfig | None = None, group=None, backend_factor
     factory = backend_factory or CudaRankBackend
     be = factory(lp, lo, hi, _cone_ptr_slice(p, lo, hi), None)
     try:
-        return run_sharded(be, row_cuts, col_cuts, cfg, norms(p.b), norms(p.c), group)
+        return run_sharded(be, row_cuts, col_cuts, cfg, norms(p.b), norms(p.c), group, p2p=p2p)
     finally:
         if hasattr(be, "close"):
             be.close()
 
 
 def run_sharded(be, row_cuts, col_cuts, cfg, b_norms, c_norms, group=None, timing=None,
-                gather_result: bool = True, overlap_reduce: bool = True) -> SolveResult:
+                gather_result: bool = True, overlap_reduce: bool = True, p2p: bool = False) -> SolveResult:
     """The sharded loop on an existing rank backend (row/column cuts shared by all ranks).
 
     ``timing``: if a dict, receives the CUDA-event time of the loop on this rank (ms).
     ``overlap_reduce``: NCCL + CUDA backend: reduce A^T h slice by slice, overlapped with the
-    next slice's column pass (else one reduce-scatter after the whole pass)."""
+    next slice's column pass (else one reduce-scatter after the whole pass).
+    ``p2p``: CUDA backend: the fused step instead. A^T h is computed into peer-visible memory,
+    then a barrier, then one kernel per rank that sums its slice over the peers in rank order,
+    updates it and stores x+ into every rank's x replica over NVLink, then a barrier. That
+    replaces the reduce-scatter, the column update and the all-gather."""
     import torch
     import torch.distributed as dist
 
@@ -331,17 +417,37 @@ def run_sharded(be, row_cuts, col_cuts, cfg, b_norms, c_norms, group=None, timin
             ag_out.copy_(torch.cat(parts))
         return ag_out[:n] if contiguous else ag_out[pad_idx]
 
+    use_p2p = p2p and fast and hasattr(be, "enable_p2p")
+    bar = torch.zeros(1, dtype=torch.float64, device=torch_dev)
+
+    def barrier():
+        # stream-ordered cross-rank barrier: the all-reduce finishes on any rank only after
+        # every rank's earlier work on its stream (partials written / replicas filled)
+        if world > 1:
+            dist.all_reduce(bar, group=group)
+
     # global column counts (uv.py:82 uses counts over ALL rows)
     be.cnt_s = reduce_scatter(be.local_counts).clone()
+    if use_p2p:
+        be.enable_p2p(group, col_cuts)
     trace = []
     x_full = None
     if timing is not None and torch_dev.type == "cuda":
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
     for k in range(1, cfg.max_iters + 1):
-        ath = reduce_scatter_partial("h")
-        be.column_update(ath, cfg.mu)
-        if fast:
+        if use_p2p:
+            be.partial_into("h", be.p2p_partial)
+            barrier()
+            be.column_update_p2p(cfg.mu)
+            barrier()
+            x_full = be.x_full
+        else:
+            ath = reduce_scatter_partial("h")
+            be.column_update(ath, cfg.mu)
+        if use_p2p:
+            pass
+        elif fast:
             dist.all_gather_into_tensor(be.x_full, be.xs, group=group)
             x_full = be.x_full
         else:

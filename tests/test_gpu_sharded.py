@@ -163,3 +163,106 @@ def test_column_sharded_cuda_backend_matches_oracle(nccl_group, kind, mu):
     assert [r.iter for r in res.trace] == [r["iter"] for r in otrace]
     assert res.report.status == otrace[-1]["status"]
     assert rel_err(res.x, ox) <= 1e-8 and rel_err(res.lam, olam) <= 1e-8
+
+
+@pytest.mark.parametrize("kind", ["lp", "socp4"])
+def test_sharded_p2p_step_equals_nccl_step(nccl_group, kind):
+    """The fused peer-memory step (cf_column_update_p2p on IPC-exported buffers; with one
+    rank the peers are the rank itself) == reduce-scatter + update + all-gather, bit for bit."""
+    import torch
+
+    from paper_2203_05027_b200 import SolverConfig
+    from paper_2203_05027_b200.devgen import generate_device_shard
+    from paper_2203_05027_b200.sharded import CudaRankBackend, run_sharded
+
+    st = torch.cuda.current_stream()
+    plan, rc, cc, cs, bn, cn, cones = generate_device_shard(20_000, 40_000, 5e-4, kind, 3, 0, 1,
+                                                            stream=st.cuda_stream)
+    cfg = SolverConfig(max_iters=60, check_every=25, eps_prim=0.0, eps_dual=0.0, eps_gap=0.0)
+    out = []
+    for p2p in (False, True):
+        plan.set_state(1.0, None, export=False)
+        be = CudaRankBackend.from_plan(plan, cc[0], cc[1], cs, cones)
+        out.append(run_sharded(be, rc, cc, cfg, bn, cn, p2p=p2p))
+        be.disable_p2p()
+    assert np.array_equal(out[0].x, out[1].x) and np.array_equal(out[0].lam, out[1].lam)
+    assert out[0].trace == out[1].trace
+    plan.close()
+
+
+@pytest.mark.parametrize("cones", [False, True])
+def test_p2p_update_kernel_two_sources(cones):
+    """cf_column_update_p2p with two partial sources and two x destinations (here both on
+    this GPU) == cf_column_update on their rank-order sum, and every destination gets x+."""
+    import ctypes
+
+    import torch
+
+    from paper_2203_05027_b200 import _lib
+
+    L = _lib.lib()
+    n = 12_000
+    g = torch.Generator(device="cuda")
+    g.manual_seed(7)
+
+    def rnd():
+        return torch.randn(n, generator=g, device="cuda", dtype=torch.float64)
+
+    a, b, c, x, z, d = rnd(), rnd(), rnd(), rnd(), rnd(), rnd()
+    cnt = torch.randint(0, 20, (n,), generator=g, device="cuda").double()
+    cone_ptr = torch.arange(0, n + 1, 4, dtype=torch.int32, device="cuda") if cones else None
+    nb = n // 4 if cones else 0
+
+    def p(t):
+        return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+    x1, z1, d1 = x.clone(), z.clone(), d.clone()
+    ath = a + b
+    _lib.check(L.cf_column_update(n, p(ath), p(cnt), p(c), p(x1), p(z1), p(d1), 0.7, nb, p(cone_ptr), None))
+    x2, z2, d2 = x.clone(), z.clone(), d.clone()
+    dst1, dst2 = torch.zeros(n, dtype=torch.float64, device="cuda"), torch.full((n,), 5.0, dtype=torch.float64,
+                                                                                 device="cuda")
+    parts = torch.tensor([a.data_ptr(), b.data_ptr()], dtype=torch.int64, device="cuda")
+    dsts = torch.tensor([dst1.data_ptr(), dst2.data_ptr()], dtype=torch.int64, device="cuda")
+    _lib.check(L.cf_column_update_p2p(n, p(parts), 2, p(cnt), p(c), p(x2), p(z2), p(d2), 0.7, nb, p(cone_ptr),
+                                      p(dsts), 2, None))
+    torch.cuda.synchronize()
+    assert torch.equal(x1, x2) and torch.equal(z1, z2) and torch.equal(d1, d2)
+    assert torch.equal(dst1, x2) and torch.equal(dst2, x2)
+
+
+def test_ipc_buffer_opens_in_another_process():
+    """cf_ipc_alloc's handle opens in another process (cf_ipc_open) and shows the same bytes."""
+    import ctypes
+    import subprocess
+    import sys
+
+    import torch
+
+    from paper_2203_05027_b200 import _lib
+    from paper_2203_05027_b200.sharded import _DevArray
+
+    L = _lib.lib()
+    ptr, h = ctypes.c_void_p(), ctypes.create_string_buffer(64)
+    _lib.check(L.cf_ipc_alloc(8 * 64, ctypes.byref(ptr), h))
+    try:
+        view = torch.as_tensor(_DevArray(ptr.value, 64), device="cuda")
+        view.copy_(torch.arange(64, dtype=torch.float64, device="cuda") * 1.5)
+        torch.cuda.synchronize()
+        child = (
+            "import ctypes, sys, torch\n"
+            "from paper_2203_05027_b200 import _lib\n"
+            "from paper_2203_05027_b200.sharded import _DevArray\n"
+            "torch.cuda.init()\n"
+            "L = _lib.lib(); ptr = ctypes.c_void_p()\n"
+            "_lib.check(L.cf_ipc_open(ctypes.create_string_buffer(bytes.fromhex(sys.argv[1]), 64), ctypes.byref(ptr)))\n"
+            "v = torch.as_tensor(_DevArray(ptr.value, 64), device='cuda').cpu()\n"
+            "print(float(v.sum()), float(v[63]))\n"
+            "L.cf_ipc_close(ptr)\n")
+        out = subprocess.run([sys.executable, "-c", child, h.raw.hex()], capture_output=True, text=True, timeout=300,
+                             cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        assert out.returncode == 0, out.stderr[-2000:]
+        total, last = (float(v) for v in out.stdout.split())
+        assert total == float(sum(1.5 * k for k in range(64))) and last == 94.5
+    finally:
+        L.cf_ipc_free(ptr)
