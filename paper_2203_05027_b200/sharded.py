@@ -243,6 +243,10 @@ class CudaRankBackend:
             self._p(self.cone_ptr) if self.cone_ptr is not None else None, self._p(self.p2p_xdst), self.p2p_world,
             self.stream.cuda_stream))
 
+    def x_replica(self):
+        """This rank's full x (torch), filled by every rank's fused step."""
+        return self.x_full
+
     def disable_p2p(self):
         import ctypes
 
@@ -417,7 +421,7 @@ def run_sharded(be, row_cuts, col_cuts, cfg, b_norms, c_norms, group=None, timin
             ag_out.copy_(torch.cat(parts))
         return ag_out[:n] if contiguous else ag_out[pad_idx]
 
-    use_p2p = p2p and fast and hasattr(be, "enable_p2p")
+    use_p2p = p2p and hasattr(be, "enable_p2p") and hasattr(be, "partial_into")
     bar = torch.zeros(1, dtype=torch.float64, device=torch_dev)
 
     def barrier():
@@ -441,7 +445,7 @@ def run_sharded(be, row_cuts, col_cuts, cfg, b_norms, c_norms, group=None, timin
             barrier()
             be.column_update_p2p(cfg.mu)
             barrier()
-            x_full = be.x_full
+            x_full = be.x_replica()
         else:
             ath = reduce_scatter_partial("h")
             be.column_update(ath, cfg.mu)

@@ -96,6 +96,52 @@ class NumpyRankBackend:
     def lam_local(self):
         return torch.tensor(self.lam)
 
+    # the fused peer-memory step, with POSIX shared memory standing in for NVLink peer buffers
+    def enable_p2p(self, group, col_cuts):
+        from multiprocessing import shared_memory
+
+        if getattr(self, "_shm", None):
+            return
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        nbytes = 8 * max(self.n, 1)
+        self._shm = [shared_memory.SharedMemory(create=True, size=nbytes) for _ in range(2)]
+        names = [None] * world
+        dist.all_gather_object(names, [s.name for s in self._shm], group=group)
+        self._peer_shm = [self._shm if s == rank else [shared_memory.SharedMemory(name=nm) for nm in names[s]]
+                          for s in range(world)]
+        self._peers = [[np.ndarray((self.n,), np.float64, buffer=s.buf) for s in pair] for pair in self._peer_shm]
+        own_partial, own_x = self._peers[rank]
+        own_x[:] = self.x_full
+        self.p2p_partial = torch.from_numpy(own_partial)
+        self.x_full = own_x                       # row_step reads the replica the peers fill
+        self.x_full_t = torch.from_numpy(own_x)
+
+    def x_replica(self):
+        return self.x_full_t
+
+    def partial_into(self, which, out):
+        out.copy_(self.partial_At(which))
+
+    def column_update_p2p(self, mu):
+        lo, hi = self.lo, self.hi
+        ath = self._peers[0][0][lo:hi].copy()
+        for s in range(1, len(self._peers)):
+            ath = ath + self._peers[s][0][lo:hi]          # rank order, as cf_column_update_p2p
+        self.column_update(torch.from_numpy(ath), mu)
+        for pair in self._peers:
+            pair[1][lo:hi] = self.xs                     # x+ into every replica
+
+    def close(self):
+        self.x_full = np.array(self.x_full)
+        self.p2p_partial = self.x_full_t = None
+        self._peers = None
+        for pair in getattr(self, "_peer_shm", []) or []:
+            for s in pair:
+                s.close()
+        for s in getattr(self, "_shm", []) or []:
+            s.unlink()
+        self._shm = self._peer_shm = None
+
 
 def _free_port():
     with socket.socket() as s:
@@ -103,7 +149,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, spec, cfg_kw, out_path):
+def _worker(rank, world, port, spec, cfg_kw, out_path, p2p=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -111,7 +157,7 @@ def _worker(rank, world, port, spec, cfg_kw, out_path):
         p = generate(spec)
         cfg = SolverConfig(**cfg_kw)
 
-        res = solve_sharded(p, cfg, backend_factory=NumpyRankBackend)
+        res = solve_sharded(p, cfg, backend_factory=NumpyRankBackend, p2p=p2p)
         if rank == 0:
             np.savez(out_path, x=res.x, lam=res.lam, iters=np.array([r.iter for r in res.trace]),
                      status=np.array([r.status for r in res.trace]),
@@ -120,14 +166,18 @@ def _worker(rank, world, port, spec, cfg_kw, out_path):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,spec,cfg_kw", [
-    (2, GenSpec(40, 90, 0.06, "lp", seed=31), dict(eps_prim=1e-4, eps_dual=1e-4, eps_gap=1e-4, max_iters=4000)),
-    (3, GenSpec(30, 64, 0.08, "socp4", seed=32), dict(mu=0.7, max_iters=600, check_every=20)),
+@pytest.mark.parametrize("world,spec,cfg_kw,p2p", [
+    (2, GenSpec(40, 90, 0.06, "lp", seed=31), dict(eps_prim=1e-4, eps_dual=1e-4, eps_gap=1e-4, max_iters=4000), False),
+    (3, GenSpec(30, 64, 0.08, "socp4", seed=32), dict(mu=0.7, max_iters=600, check_every=20), False),
+    # the fused peer-memory step's ordering (partials -> barrier -> reduce+update+broadcast -> barrier)
+    (2, GenSpec(40, 90, 0.06, "lp", seed=31), dict(eps_prim=1e-4, eps_dual=1e-4, eps_gap=1e-4, max_iters=4000), True),
+    (3, GenSpec(30, 64, 0.08, "socp4", seed=32), dict(mu=0.7, max_iters=600, check_every=20), True),
 ])
-def test_sharded_matches_oracle(tmp_path, world, spec, cfg_kw):
+def test_sharded_matches_oracle(tmp_path, world, spec, cfg_kw, p2p):
     out = str(tmp_path / "res.npz")
     port = _free_port()
-    mp.start_processes(_worker, args=(world, port, spec, cfg_kw, out), nprocs=world, join=True, start_method="spawn")
+    mp.start_processes(_worker, args=(world, port, spec, cfg_kw, out, p2p), nprocs=world, join=True,
+                       start_method="spawn")
     got = np.load(out)
     p = generate(spec)
     cfg = SolverConfig(**cfg_kw)
