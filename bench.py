@@ -216,7 +216,9 @@ def run_reference(args, spec, rank):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000.0 / value, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-        "config": {"workload": spec["workload"], "parallelism": "replicas"},
+        "config": {"workload": spec["workload"], "m": spec["m"], "n": spec["n"],
+                   "o": int(round(spec["m"] * spec["n"] * spec["density"])), "mu": 1.0, "check_every": 25,
+                   "parallelism": "replicas" if args.gpus > 1 else "single"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": desc},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -410,6 +412,10 @@ def run_sharded_bench(args, spec, rank, world, local_rank):
     scale = args.c5_scale
     m, n = int(spec["m"] * scale), int(spec["n"] * scale)
     stream = torch.cuda.current_stream()
+    if args.c5_mode == "auto":
+        from paper_2203_05027_b200.sharded import choose_sharding
+
+        args.c5_mode = choose_sharding(m, n, world)
     if args.c5_mode == "cols":
         return run_col_sharded_bench(args, spec, rank, world, m, n, scale, stream, own_group)
     plan, row_cuts, col_cuts, c_slice, bn, cn, cones = generate_device_shard(
@@ -602,8 +608,9 @@ def main():
     ap.add_argument("--e2e-max-iters", type=int, default=0)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--c5-scale", type=float, default=1.0, help="shrink C5 (m, n) by this factor (same nnz/row)")
-    ap.add_argument("--c5-mode", choices=("rows", "cols", "p2p"), default="rows",
-                    help="C5: split A's rows (exchange n-vectors) or columns (all-reduce the m-vector A x)")
+    ap.add_argument("--c5-mode", choices=("rows", "cols", "p2p", "auto"), default="rows",
+                    help="C5: split A's rows (exchange n-vectors) or columns (all-reduce the m-vector A x); "
+                         "auto: by shape (sharded.choose_sharding)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

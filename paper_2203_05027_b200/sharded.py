@@ -32,7 +32,7 @@ import numpy as np
 from .api import IterationReport, SolveResult, SolverConfig, _decide, norms
 from .problem import ConeSpec, ProblemInstance, TripletMatrix, cone_sizes_array
 
-__all__ = ["solve_sharded", "run_sharded", "partition", "CudaRankBackend", "assemble_report",
+__all__ = ["solve_distributed", "choose_sharding", "exchange_bytes", "solve_sharded", "run_sharded", "partition", "CudaRankBackend", "assemble_report",
            "solve_col_sharded", "run_col_sharded", "CudaColBackend", "local_columns"]
 
 # report parts: row = {sum prim^2, max|prim|, max|Ax|, sum b.lam, nonfinite};
@@ -702,3 +702,51 @@ def solve_col_sharded(p, cfg: SolverConfig | None = None, group=None, backend_fa
     finally:
         if hasattr(be, "close"):
             be.close()
+
+
+def exchange_bytes(m: int, n: int, world: int, mode: str) -> int:
+    """NVLink bytes each rank sends per iteration (and receives) for ``mode``.
+
+    rows: reduce-scatter of the n-vector A_r^T h_r plus all-gather of x, 2 * 8n(p-1)/p;
+    cols: all-reduce of the m-vector A_s x_s, 2 * 8m(p-1)/p (ring/NVLS volume).
+    Reports (every check_every iterations) add one more exchange of the same kind."""
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    if mode == "rows":
+        return 2 * 8 * n * (world - 1) // world
+    if mode == "cols":
+        return 2 * 8 * m * (world - 1) // world
+    raise ValueError(f"unknown sharding mode {mode!r}")
+
+
+def choose_sharding(m: int, n: int, world: int) -> str:
+    """Rows or columns for an m x n problem on ``world`` ranks (SURVEY §8e "Alternatives").
+
+    The exchange is the only cross-rank cost of either layout and both keep every
+    nonzero on exactly one rank, so the layout that moves fewer bytes wins: column
+    sharding when m < n (it all-reduces the m-vector A x), row sharding otherwise
+    (it exchanges n-vectors). Ties and world 1 pick rows, the C5 layout."""
+    if world <= 1:
+        return "rows"
+    return "cols" if exchange_bytes(m, n, world, "cols") < exchange_bytes(m, n, world, "rows") else "rows"
+
+
+def solve_distributed(p, cfg: SolverConfig | None = None, group=None, mode: str = "auto",
+                      backend_factory=None, p2p: bool = False) -> SolveResult:
+    """solve() over the ranks of ``group`` with the layout picked by ``mode``.
+
+    ``mode``: "auto" (choose_sharding on the problem's shape), "rows" (solve_sharded;
+    ``p2p`` selects the fused peer-memory step) or "cols" (solve_col_sharded).
+    ``backend_factory`` is the chosen layout's rank backend (CUDA by default). Every
+    rank passes the same problem and gets the same SolveResult."""
+    import torch.distributed as dist
+
+    if mode not in ("auto", "rows", "cols"):
+        raise ValueError(f"unknown sharding mode {mode!r}")
+    if mode == "auto":
+        mode = choose_sharding(int(p.A.num_rows), int(p.A.num_cols), dist.get_world_size(group))
+    if mode == "cols":
+        if p2p:
+            raise ValueError("p2p is a row-sharding step; column sharding all-reduces A x")
+        return solve_col_sharded(p, cfg, group=group, backend_factory=backend_factory)
+    return solve_sharded(p, cfg, group=group, backend_factory=backend_factory, p2p=p2p)

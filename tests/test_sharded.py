@@ -304,3 +304,56 @@ def test_column_sharded_matches_oracle(tmp_path, world, spec, cfg_kw):
     assert rel_err(got["x"], ox) <= 1e-8
     assert rel_err(got["lam"], olam) <= 1e-8
     np.testing.assert_allclose(got["pobj"], [r["pobj"] for r in otrace], rtol=1e-9, atol=1e-9)
+
+
+def test_choose_sharding_by_exchange_volume():
+    from paper_2203_05027_b200.sharded import choose_sharding, exchange_bytes
+
+    # C5 (m=50M < n=100M): the all-reduce of A x moves half the bytes of rows' two n-vector exchanges
+    assert exchange_bytes(50_000_000, 100_000_000, 8, "rows") == 2 * 8 * 100_000_000 * 7 // 8
+    assert exchange_bytes(50_000_000, 100_000_000, 8, "cols") == 2 * 8 * 50_000_000 * 7 // 8
+    assert choose_sharding(50_000_000, 100_000_000, 8) == "cols"
+    assert choose_sharding(100, 40, 2) == "rows"
+    assert choose_sharding(64, 64, 4) == "rows"      # tie -> rows
+    assert choose_sharding(10, 1000, 1) == "rows"    # one rank: nothing is exchanged
+    with pytest.raises(ValueError):
+        exchange_bytes(1, 1, 2, "diagonal")
+
+
+def _auto_worker(rank, world, port, spec, cfg_kw, out_path, factory_name):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2203_05027_b200.sharded import solve_distributed
+
+        p = generate(spec)
+        factory = {"rows": NumpyRankBackend, "cols": NumpyColBackend}[factory_name]
+        res = solve_distributed(p, SolverConfig(**cfg_kw), mode="auto", backend_factory=factory)
+        if rank == 0:
+            np.savez(out_path, x=res.x, lam=res.lam, iters=np.array([r.iter for r in res.trace]),
+                     status=np.array([r.status for r in res.trace]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("spec,expect", [
+    (GenSpec(40, 90, 0.06, "lp", seed=51), "cols"),    # m < n
+    (GenSpec(90, 60, 0.06, "lp", seed=52), "rows"),    # m > n
+])
+def test_solve_distributed_auto_matches_oracle(tmp_path, spec, expect):
+    """mode="auto" picks the layout by shape and still reaches the oracle's iterates (gloo, world 2)."""
+    from paper_2203_05027_b200.sharded import choose_sharding
+
+    assert choose_sharding(spec.m, spec.n, 2) == expect
+    cfg_kw = dict(eps_prim=1e-4, eps_dual=1e-4, eps_gap=1e-4, max_iters=3000)
+    out = str(tmp_path / "res.npz")
+    mp.start_processes(_auto_worker, args=(2, _free_port(), spec, cfg_kw, out, expect), nprocs=2, join=True,
+                       start_method="spawn")
+    got = np.load(out)
+    p = generate(spec)
+    ox, olam, otrace, _ = oracle.solve(p, SolverConfig(**cfg_kw))
+    assert list(got["iters"]) == [r["iter"] for r in otrace]
+    assert list(got["status"]) == [r["status"] for r in otrace]
+    assert rel_err(got["x"], ox) <= 1e-8
+    assert rel_err(got["lam"], olam) <= 1e-8
