@@ -293,6 +293,25 @@ def run_ours(args, spec, rank, world, local_rank):
     ms_max = float(ms_t.item())
     value = world * args.steps / (ms_max / 1000.0)
 
+    # ---------------- small problems: solve() runs them in the cluster-resident kernel
+    # (k_cluster, one launch for the whole loop). Its device time over the same K
+    # iterations is the headline then; the plan engine's number stays on the line.
+    engine = {"name": "plan (k_pass chain)"}
+    if world == 1 and o < 1_000_000:
+        from paper_2203_05027_b200 import api as _api
+
+        hp = to_host_problem(inst)
+        if _api._cluster_candidate(hp):
+            _api._solve_cluster(hp, SolverConfig(max_iters=args.warmup, eps_prim=0.0, eps_dual=0.0, eps_gap=0.0))
+            ct = {}
+            cres = _api._solve_cluster(hp, timed_cfg, timing=ct)
+            if cres is not None and cres.report.iter == args.steps:
+                engine = {"name": f"cluster (k_cluster, {ct['cluster']} CTAs, distributed shared memory)",
+                          "ms_per_step": ct["kernel_ms"] / args.steps,
+                          "plan_engine": {"value": value, "ms_per_step": ms_max / args.steps}}
+                ms_max = ct["kernel_ms"]
+                value = args.steps / (ms_max / 1000.0)
+
     # ---------------- roofline of the dominant pass (per-pass events inside the timed region)
     row_b, col_b = algorithmic_bytes(m, n, o)
     peak, peak_src = hbm_peak()
@@ -385,7 +404,8 @@ def run_ours(args, spec, rank, world, local_rank):
             "config": {"workload": spec["workload"], "m": m, "n": n, "o": o, "mu": 1.0, "check_every": 25,
                        "parallelism": "replicas" if world > 1 else "single", "l2": "inputs larger than L2 "
                        f"({(row_b + col_b) / 1e9:.2f} GB streamed per iteration vs 126 MB L2)"},
-            "gpu_launches": tim["launches"], "roofline": roofline, "iteration_roofline": iteration_roofline,
+            "gpu_launches": 1 if engine["name"].startswith("cluster") else tim["launches"], "engine": engine,
+            "roofline": roofline, "iteration_roofline": iteration_roofline,
             "time_to_tol": ttt, "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
             "gather_bound": gather_bound(o, dms, clocks),
         }

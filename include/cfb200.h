@@ -196,6 +196,22 @@ int cf_batch_solve(int64_t n_problems, const int64_t* row_off, const int64_t* co
                    cf_report* final_reports, int32_t* n_reports, cf_report* trace, int64_t trace_cap,
                    cf_problem_checks* checks, double* elapsed_ms);
 
+/*
+ * cf_cluster_solve: solve() (solver.py:275-334, cold start) of ONE mid-size
+ * problem in a single launch of a thread-block cluster (up to 16 CTAs, iterates in
+ * distributed shared memory; x and lam bit-identical to cf_plan_solve). Same
+ * inputs and outputs as cf_batch_solve with P = 1 (trace: trace_cap reports).
+ * *cluster_used = the cluster size, or 0 when the problem does not fit the
+ * cluster's shared memory: then nothing was solved and the caller uses
+ * cf_plan_create + cf_plan_solve. The reference has no such entry point; it
+ * replaces the loop of solve() for problems like SURVEY config C1.
+ */
+int cf_cluster_solve(int64_t m, int64_t n, int64_t o, const int64_t* rows, const int64_t* cols,
+                     const double* vals, const double* b, const double* c, int64_t n_blocks,
+                     const int64_t* block_sizes, const cf_config* cfg, double* x_out, double* lam_out,
+                     cf_report* final_report, int32_t* n_reports, cf_report* trace, int64_t trace_cap,
+                     cf_problem_checks* checks, int32_t* cluster_used, double* elapsed_ms);
+
 /* ---------------------------------------------------------------- row-sharded building blocks
  * Used by paper_2203_05027_b200/sharded.py (config C5: A's rows split over
  * ranks, one exchange per iteration). A rank's plan holds its row block and ALL

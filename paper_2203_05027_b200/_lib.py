@@ -113,6 +113,8 @@ SIGNATURES = {
     "cf_column_parts": (c_int, [c_int64, _P, _P, _P, _P, _P, _P, _P]),
     "cf_batch_solve": (c_int, [c_int64, _P, _P, c_int64, _P, _P, _P, _P, _P, c_int64, _P, _P, _P, _P, _P, _P, _P,
                                c_int64, POINTER(CfChecks), _D]),
+    "cf_cluster_solve": (c_int, [c_int64, c_int64, c_int64, _P, _P, _P, _P, _P, c_int64, _P, _P, _P, _P, _P, _P, _P,
+                                 c_int64, POINTER(CfChecks), _P, _D]),
     "cf_plan_set_profiling": (c_int, [_P, c_int]),
     "cf_plan_sync": (c_int, [_P]),
     "cf_plan_col_step": (c_int, [_P, c_double]),

@@ -230,6 +230,10 @@ def solve(p, cfg: SolverConfig | None = None, init: SolverState | None = None) -
         except Exception:   # re-raised by run_plan computing them again
             pass
 
+    if init is None and _cluster_candidate(p):
+        res = _solve_cluster(p, cfg)
+        if res is not None:
+            return res
     th = threading.Thread(target=_norms, daemon=True)
     th.start()
     try:
@@ -242,6 +246,87 @@ def solve(p, cfg: SolverConfig | None = None, init: SolverState | None = None) -
         return run_plan(plan, p, cfg, box.get("b"), box.get("c"))
     finally:
         plan.close()
+
+
+# Mid-size problems run in the cluster-resident kernel (csrc/cf_batch.cu k_cluster): one
+# launch for the whole loop, iterates in the distributed shared memory of up to 16 CTAs.
+# The estimate below is conservative; cf_cluster_solve makes the exact decision.
+_LAST_CLUSTER = 0   # cluster size of the last cf_cluster_solve call (0: did not fit), for tests
+
+_PLAN_KNOBS = ("CF_PANEL_MB", "CF_BAND_MB", "CF_FORCE_LARGE_TILES", "CF_NO_LARGE_TILES", "CF_GROUP_CONES",
+               "CF_LIB_PATH")
+
+
+def _cluster_candidate(p) -> bool:
+    import os
+
+    if os.environ.get("CF_NO_CLUSTER", "") not in ("", "0") or not _host_shapes_ok(p):
+        return False
+    if any(os.environ.get(k) for k in _PLAN_KNOBS):   # a plan-engine configuration was asked for
+        return False
+    m, n, o = int(p.A.num_rows), int(p.A.num_cols), int(np.asarray(p.A.vals).size)
+    if m < 1 or n < 1:
+        return False
+    own = 1.3 * (24 * o + 36 * m + 52 * n) / 16
+    return 8 * (n + 3 * m) + own + 4096 <= 227 * 1024
+
+
+def _solve_cluster(p, cfg, timing: dict | None = None) -> SolveResult | None:
+    """solve() in one cluster launch (cf_cluster_solve); None when the problem does not fit.
+    ``timing``, if given, receives the loop kernel's device time and the cluster size."""
+    import ctypes
+
+    from ._lib import CF_EPROBLEM, CfChecks, CfReport, check, lib
+    from .engine import report_to_dict
+
+    m, n = int(p.A.num_rows), int(p.A.num_cols)
+    rows = np.ascontiguousarray(p.A.rows, dtype=np.int64)
+    cols = np.ascontiguousarray(p.A.cols, dtype=np.int64)
+    vals = np.ascontiguousarray(p.A.vals, dtype=np.float64)
+    b = np.ascontiguousarray(p.b, dtype=np.float64)
+    c = np.ascontiguousarray(p.c, dtype=np.float64)
+    sizes = np.ascontiguousarray(cone_sizes_array(p.cones), dtype=np.int64)
+    bn, cn = norms(b), norms(c)
+    cs = config_struct(cfg, bn, cn)
+    x = np.empty(n)
+    lam = np.empty(m)
+    final = CfReport()
+    nrep = ctypes.c_int32()
+    cap = -(-int(cfg.max_iters) // int(cfg.check_every))
+    tr = (CfReport * cap)()
+    chk = CfChecks()
+    used = ctypes.c_int32()
+    el = ctypes.c_double()
+
+    def ptr(a):
+        return ctypes.c_void_p(a.ctypes.data) if a.size else ctypes.c_void_p(0)
+
+    rc = lib().cf_cluster_solve(m, n, int(vals.size), ptr(rows), ptr(cols), ptr(vals), ptr(b), ptr(c),
+                                int(sizes.size), ptr(sizes), ctypes.byref(cs), ptr(x), ptr(lam),
+                                ctypes.byref(final), ctypes.byref(nrep), tr, cap, ctypes.byref(chk),
+                                ctypes.byref(used), ctypes.byref(el))
+    if rc == CF_EPROBLEM:
+        _raise_invalid(p)
+    check(rc, "cf_cluster_solve")
+    global _LAST_CLUSTER
+    _LAST_CLUSTER = int(used.value)
+    if used.value == 0:
+        return None
+    if timing is not None:
+        timing["kernel_ms"] = el.value
+        timing["cluster"] = int(used.value)
+    trace = []
+    for j in range(int(nrep.value)):
+        d = report_to_dict(tr[j])
+        rep = _to_report(d)
+        status = _decide(rep, cfg, bn, cn)
+        if status == "running" and rep.iter == cfg.max_iters:
+            status = "max_iters"
+        if status != d["status"]:
+            raise RuntimeError(f"device termination test ({d['status']}) disagrees with check_termination "
+                               f"({status}) at iteration {rep.iter}")
+        trace.append(replace(rep, status=status))
+    return SolveResult(x=x, lam=lam, report=trace[-1], trace=tuple(trace))
 
 
 # shared memory of the batched kernel for a batch whose largest dimensions are m, n, o, k

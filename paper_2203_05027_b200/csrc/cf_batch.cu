@@ -15,6 +15,7 @@
 // returns.
 #include <algorithm>
 #include <cmath>
+#include <mutex>
 
 #include "cf_common.h"
 #include "cf_report.cuh"
@@ -60,7 +61,7 @@ struct BatchArgs {
 
 __device__ __forceinline__ double nanmax_b(double a, double b) { return (a > b || a != a) ? a : b; }
 
-template <bool MAX>
+template <bool MAX, int NT = kBT>
 __device__ double block_reduce_b(double v, double* sh) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
@@ -72,7 +73,7 @@ __device__ double block_reduce_b(double v, double* sh) {
     if (l == 0) sh[w] = v;
     __syncthreads();
     if (w == 0) {
-        v = (l < kBT / 32) ? sh[l] : 0.0;
+        v = (l < NT / 32) ? sh[l] : 0.0;
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
             const double o = __shfl_xor_sync(0xffffffffu, v, off);
@@ -404,7 +405,17 @@ extern "C" int cf_batch_solve(int64_t n_problems, const int64_t* row_off, const 
                   " bytes of shared memory (> " + std::to_string(max_smem) + "); solve it with cf_plan_solve");
         return CF_EINVAL;
     }
-    CF_CUDA(cudaFuncSetAttribute(k_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // process-wide attribute: set once to the limit so concurrent batches never lower each other's
+    static std::once_flag attr_once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(attr_once, [&] {
+        cudaFuncAttributes fa{};
+        attr_err = cudaFuncGetAttributes(&fa, k_batch);
+        if (attr_err == cudaSuccess)
+            attr_err = cudaFuncSetAttribute(k_batch, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            max_smem - (int)fa.sharedSizeBytes);
+    });
+    CF_CUDA(attr_err);
     int per_sm = 0;
     CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_batch, kBT, smem));
     const int grid = (int)std::min<int64_t>(P, (int64_t)std::max(per_sm, 1) * sms);
@@ -473,5 +484,493 @@ extern "C" int cf_batch_solve(int64_t n_problems, const int64_t* row_off, const 
     if (trace_cap > 0)
         CF_CUDA(cudaMemcpyAsync(trace, d_trace.p, P * trace_cap * sizeof(cf_report), cudaMemcpyDeviceToHost, st));
     CF_CUDA(cudaStreamSynchronize(st));
+    return CF_OK;
+}
+
+// ============================================================================
+// Cluster-resident solver (mid-size problems, e.g. config C1): ONE problem spread
+// over a thread-block cluster of C CTAs (C = 1..16). CTA q owns a contiguous,
+// nonzero-balanced block of rows and a cone-aligned block of columns, keeps its
+// CSR rows and CSC columns in shared memory, and holds a full REPLICA of the
+// gathered vectors (x for the row pass, h for the column pass; lam and b - r on
+// report iterations). After updating its slice a CTA stores it into every peer's
+// replica through distributed shared memory, and one cluster barrier per pass
+// orders the stores before the peers' gathers. The whole loop of solve()
+// (solver.py:309-334) runs in one launch with two cluster barriers per iteration,
+// in place of the plan's kernel chain (whose per-iteration cost at C1 is launch
+// and dependent-latency bound). Arithmetic is k_batch's: the same sequential
+// canonical-order sums and epilogue expressions, so x and lam are bit-identical to
+// cf_plan_solve; the report's fixed-order reduction differs only in rounding.
+// ============================================================================
+#include <cooperative_groups.h>
+
+#include <mutex>
+
+namespace cf {
+namespace {
+
+namespace cg = cooperative_groups;
+
+constexpr int kCT = 512;              // threads per cluster CTA
+constexpr int kMaxCluster = 16;
+
+struct ClusterArgs {
+    int32_t C;
+    int32_t M, N;                     // problem rows / columns (replica lengths)
+    int32_t row_cut[kMaxCluster + 1];
+    int32_t col_cut[kMaxCluster + 1];
+    int32_t cone_cut[kMaxCluster + 1];
+    const int32_t* rowptr;            // canonical CSR / CSC of the plan (global indices)
+    const int32_t* colidx;
+    const double* valr;
+    const int32_t* colptr;
+    const int32_t* rowidx;
+    const double* valc;
+    const double* b;
+    const double* c;
+    const double* fu;
+    const double* db;
+    const int32_t* cone_ptr;
+    int32_t cones;
+    cf_config cfg;
+    double* x_out;
+    double* lam_out;
+    cf_report* trace;
+    int64_t trace_cap;
+    int32_t* n_reports;
+    cf_report* final_report;
+    int32_t cap_m, cap_n, cap_or, cap_oc, cap_k;
+};
+
+size_t cluster_smem(int M, int N, int cm, int cn, int cor, int coc, int ck) {
+    return sizeof(double) * (size_t)(N + 3 * M + cor + coc + 4 * cm + 6 * cn + 32 + 16 * kMaxCluster) +
+           sizeof(int32_t) * (size_t)(cor + coc + cm + 1 + cn + 1 + ck + 1) + 16;
+}
+
+__global__ void __launch_bounds__(kCT, 1) k_cluster(const ClusterArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    cg::cluster_group cluster = cg::this_cluster();
+    const int q = (int)cluster.block_rank();
+    const int C = a.C, M = a.M, N = a.N;
+    const int CM = a.cap_m, CN = a.cap_n;
+    double* xr = reinterpret_cast<double*>(smem);   // replicas (global indices)
+    double* hr = xr + N;
+    double* lamr = hr + M;
+    double* brr = lamr + M;
+    double* valr = brr + M;                          // own rows / columns
+    double* valc = valr + a.cap_or;
+    double* b = valc + a.cap_oc;
+    double* fu = b + CM;
+    double* db = fu + CM;
+    double* ax = db + CM;
+    double* c = ax + CM;
+    double* z = c + CN;
+    double* dl = z + CN;
+    double* wv = dl + CN;
+    double* fvs = wv + CN;
+    double* cmu = fvs + CN;
+    double* red = cmu + CN;                          // 32
+    double* parts = red + 32;                        // [C][16] report partials (CTA 0)
+    int32_t* colidx = reinterpret_cast<int32_t*>(parts + 16 * kMaxCluster);
+    int32_t* rowidx = colidx + a.cap_or;
+    int32_t* rowptr = rowidx + a.cap_oc;
+    int32_t* colptr = rowptr + CM + 1;
+    int32_t* cptr = colptr + CN + 1;
+    __shared__ int32_t s_status;
+    __shared__ double* s_peer_x[kMaxCluster];
+    __shared__ double* s_peer_h[kMaxCluster];
+    __shared__ double* s_peer_lam[kMaxCluster];
+    __shared__ double* s_peer_br[kMaxCluster];
+    __shared__ int32_t* s_peer_status[kMaxCluster];
+    __shared__ double* s_parts0;
+    const int t = threadIdx.x;
+    const int r0 = a.row_cut[q], m = a.row_cut[q + 1] - r0;
+    const int c0 = a.col_cut[q], n = a.col_cut[q + 1] - c0;
+    const int kr0 = a.rowptr[r0], kc0 = a.colptr[c0];
+    const int orr = a.rowptr[r0 + m] - kr0, occ = a.colptr[c0 + n] - kc0;
+    const cf_config& cfg = a.cfg;
+    const double mu = cfg.mu;
+    const MuDivB div = make_mudiv_b(mu);
+    // ---- load the CTA's rows and columns, cold start (solver.py:309)
+    for (int i = t; i <= m; i += kCT) rowptr[i] = a.rowptr[r0 + i] - kr0;
+    for (int j = t; j <= n; j += kCT) colptr[j] = a.colptr[c0 + j] - kc0;
+    for (int k = t; k < orr; k += kCT) {
+        colidx[k] = a.colidx[kr0 + k];
+        valr[k] = a.valr[kr0 + k];
+    }
+    for (int k = t; k < occ; k += kCT) {
+        rowidx[k] = a.rowidx[kc0 + k];
+        valc[k] = a.valc[kc0 + k];
+    }
+    for (int i = t; i < M; i += kCT) {
+        hr[i] = 0.0;
+        lamr[i] = 0.0;
+        brr[i] = 0.0;
+    }
+    for (int j = t; j < N; j += kCT) xr[j] = 0.0;
+    for (int i = t; i < m; i += kCT) {
+        b[i] = a.b[r0 + i];
+        fu[i] = a.fu[r0 + i];
+        db[i] = a.db[r0 + i];
+        ax[i] = 0.0;
+    }
+    for (int j = t; j < n; j += kCT) {
+        const double cj = a.c[c0 + j];
+        c[j] = cj;
+        cmu[j] = div(cj);
+        fvs[j] = 1.0 / (1.0 + (double)(a.colptr[c0 + j + 1] - a.colptr[c0 + j]));
+        z[j] = 0.0;
+        dl[j] = 0.0;
+    }
+    int nk = 0;
+    if (a.cones) {
+        const int k0 = a.cone_cut[q];
+        nk = a.cone_cut[q + 1] - k0;
+        for (int u = t; u <= nk; u += kCT) cptr[u] = a.cone_ptr[k0 + u] - c0;
+    }
+    if (t < C) {
+        s_peer_x[t] = cluster.map_shared_rank(xr, t);
+        s_peer_h[t] = cluster.map_shared_rank(hr, t);
+        s_peer_lam[t] = cluster.map_shared_rank(lamr, t);
+        s_peer_br[t] = cluster.map_shared_rank(brr, t);
+        s_peer_status[t] = cluster.map_shared_rank(&s_status, t);
+    }
+    if (t == 0) {
+        s_status = CF_STATUS_RUNNING;
+        s_parts0 = cluster.map_shared_rank(parts, 0);
+    }
+    cluster.sync();   // every CTA resident and initialised before any remote store
+    int nrep = 0;
+    cf_report last{};
+    int64_t next_report = cfg.check_every < cfg.max_iters ? cfg.check_every : cfg.max_iters;
+    for (int64_t k = 1; k <= cfg.max_iters; ++k) {
+        const bool report = k == next_report;
+        if (report) next_report = (k + cfg.check_every < cfg.max_iters) ? k + cfg.check_every : cfg.max_iters;
+        // ---- column pass on the CTA's columns (solver.py:168-176,186-188,196)
+        for (int j = t; j < n; j += kCT) {
+            const int p0 = colptr[j], p1 = colptr[j + 1];
+            const double ath = seg_dot(valc, rowidx, hr, p0, p1);
+            const int cnt = p1 - p0;
+            const double fv = fvs[j];
+            const double xj = xr[c0 + j], zj = z[j], dj = dl[j];
+            const double dm = div(dj);
+            const double v = __dadd_rn(__dmul_rn((double)cnt, xj), ath);
+            const double xp = fv * (((v + zj) + dm) - cmu[j]);
+            const double w = xp - dm;
+            xr[c0 + j] = xp;
+            for (int u = 0; u < C; ++u)
+                if (u != q) s_peer_x[u][c0 + j] = xp;
+            if (!a.cones) {
+                const double zp = w > 0.0 ? w : 0.0;
+                z[j] = zp;
+                dl[j] = dj + mu * (zp - xp);
+            } else {
+                wv[j] = w;
+            }
+        }
+        if (a.cones) {
+            __syncthreads();
+            for (int u = t; u < nk; u += kCT) {
+                const int off = cptr[u], size = cptr[u + 1] - off;
+                project_block_b(wv + off, size, z + off);
+                for (int e = 0; e < size; ++e) dl[off + e] = dl[off + e] + mu * (z[off + e] - xr[c0 + off + e]);
+            }
+        }
+        cluster.sync();   // x replicas complete
+        // ---- row pass on the CTA's rows (solver.py:179-183,194-195)
+        for (int i = t; i < m; i += kCT) {
+            const int p0 = rowptr[i], p1 = rowptr[i + 1];
+            const double axi = seg_dot(valr, colidx, xr, p0, p1);
+            const double bi = b[i];
+            const double r = fu[i] * (db[i] + axi);
+            const double ln = lamr[r0 + i] + mu * (r - bi);
+            const double bmr = bi - r;
+            const double hn = bmr - div(ln);
+            hr[r0 + i] = hn;
+            lamr[r0 + i] = ln;
+            for (int u = 0; u < C; ++u)
+                if (u != q) s_peer_h[u][r0 + i] = hn;
+            if (report) {
+                brr[r0 + i] = bmr;
+                for (int u = 0; u < C; ++u)
+                    if (u != q) {
+                        s_peer_lam[u][r0 + i] = ln;
+                        s_peer_br[u][r0 + i] = bmr;
+                    }
+                ax[i] = axi;
+            }
+        }
+        cluster.sync();   // h (and on reports lam, b - r) replicas complete
+        if (!report) continue;
+        // ---- compute_report (solver.py:206-242): per-CTA partials, CTA 0 combines in rank order
+        double prim2 = 0.0, primi = 0.0, axm = 0.0, blam = 0.0, nfr = 0.0;
+        for (int i = t; i < m; i += kCT) {
+            const double pr = ax[i] - b[i];
+            prim2 = prim2 + pr * pr;
+            primi = nanmax_b(primi, fabs(pr));
+            axm = nanmax_b(axm, fabs(ax[i]));
+            blam = blam + b[i] * lamr[r0 + i];
+            if (!isfinite(lamr[r0 + i])) nfr = 1.0;
+        }
+        double d2 = 0.0, dmx = 0.0, s2 = 0.0, smx = 0.0, amx = 0.0, cx = 0.0, cgp = 0.0, nfc = 0.0;
+        for (int j = t; j < n; j += kCT) {
+            double atl = 0.0;
+            for (int p = colptr[j]; p < colptr[j + 1]; ++p) {
+                const int i = rowidx[p];
+                const double pa = __dmul_rn(valc[p], lamr[i]);
+                if (!isfinite(pa) || !isfinite(valc[p] * brr[i])) nfc = 1.0;
+                atl = __dadd_rn(atl, pa);
+            }
+            const double xj = xr[c0 + j];
+            const double dual = atl + c[j];
+            const double stat = dual - dl[j];
+            d2 = d2 + dual * dual;
+            dmx = nanmax_b(dmx, fabs(dual));
+            s2 = s2 + stat * stat;
+            smx = nanmax_b(smx, fabs(stat));
+            amx = nanmax_b(amx, fabs(atl));
+            cx = cx + c[j] * xj;
+            cgp = nanmax_b(cgp, fabs(xj - z[j]));
+            if (!isfinite(xj) || !isfinite(z[j]) || !isfinite(dl[j])) nfc = 1.0;
+        }
+        double f[13];
+        f[0] = block_reduce_b<false, kCT>(prim2, red);
+        f[1] = block_reduce_b<true, kCT>(primi, red);
+        f[2] = block_reduce_b<true, kCT>(axm, red);
+        f[3] = block_reduce_b<false, kCT>(blam, red);
+        f[4] = block_reduce_b<true, kCT>(nfr, red);
+        f[5] = block_reduce_b<false, kCT>(d2, red);
+        f[6] = block_reduce_b<true, kCT>(dmx, red);
+        f[7] = block_reduce_b<false, kCT>(s2, red);
+        f[8] = block_reduce_b<true, kCT>(smx, red);
+        f[9] = block_reduce_b<true, kCT>(amx, red);
+        f[10] = block_reduce_b<false, kCT>(cx, red);
+        f[11] = block_reduce_b<true, kCT>(cgp, red);
+        f[12] = block_reduce_b<true, kCT>(nfc, red);
+        if (t == 0)
+            for (int e = 0; e < 13; ++e) s_parts0[q * 16 + e] = f[e];
+        cluster.sync();
+        if (q == 0 && t == 0) {
+            double g[13];
+            for (int e = 0; e < 13; ++e) g[e] = parts[e];
+            for (int u = 1; u < C; ++u) {
+                const double* pu = parts + u * 16;
+                g[0] = g[0] + pu[0];
+                g[1] = nanmax_b(g[1], pu[1]);
+                g[2] = nanmax_b(g[2], pu[2]);
+                g[3] = g[3] + pu[3];
+                g[4] = nanmax_b(g[4], pu[4]);
+                g[5] = g[5] + pu[5];
+                g[6] = nanmax_b(g[6], pu[6]);
+                g[7] = g[7] + pu[7];
+                g[8] = nanmax_b(g[8], pu[8]);
+                g[9] = nanmax_b(g[9], pu[9]);
+                g[10] = g[10] + pu[10];
+                g[11] = nanmax_b(g[11], pu[11]);
+                g[12] = nanmax_b(g[12], pu[12]);
+            }
+            ReportFields rf;
+            rf.prim2 = g[0];
+            rf.prim_inf = g[1];
+            rf.ax_inf = g[2];
+            rf.blam = g[3];
+            rf.nf_row = g[4];
+            rf.dual2 = g[5];
+            rf.dual_inf = g[6];
+            rf.stat2 = g[7];
+            rf.stat_inf = g[8];
+            rf.atl_inf = g[9];
+            rf.pobj = g[10];
+            rf.cone_gap = g[11];
+            rf.nf_col = g[12];
+            cf_report r = assemble_report(rf, k, false);
+            r.status = decide_status(r, cfg, k);
+            if (nrep < a.trace_cap) a.trace[nrep] = r;
+            last = r;
+            s_status = r.status;
+            for (int u = 1; u < C; ++u) *s_peer_status[u] = r.status;
+        }
+        ++nrep;
+        cluster.sync();   // status visible everywhere; parts free for the next report
+        if (s_status != CF_STATUS_RUNNING) break;
+    }
+    // ---- SolveResult (solver.py:329-334)
+    for (int j = t; j < n; j += kCT) a.x_out[c0 + j] = xr[c0 + j];
+    for (int i = t; i < m; i += kCT) a.lam_out[r0 + i] = lamr[r0 + i];
+    if (q == 0 && t == 0) {
+        *a.final_report = last;
+        *a.n_reports = nrep;
+    }
+    cluster.sync();   // no CTA leaves while a peer may still address its shared memory
+}
+
+// positions (indices into allowed) of C+1 cuts balancing ptr's counts over the
+// candidate boundaries allowed (increasing, allowed[0] = 0)
+void balanced_cuts(const std::vector<int32_t>& ptr, const std::vector<int32_t>& allowed, int C, int32_t* cut) {
+    const int64_t total = (int64_t)ptr[allowed.back()] - ptr[0];
+    cut[0] = 0;
+    size_t pos = 0;
+    for (int q = 1; q < C; ++q) {
+        const int64_t target = total * q / C;
+        while (pos + 1 < allowed.size() && (int64_t)ptr[allowed[pos]] < target) ++pos;
+        cut[q] = std::max<int32_t>(cut[q - 1], (int32_t)pos);
+    }
+    cut[C] = (int32_t)allowed.size() - 1;
+}
+
+}  // namespace
+}  // namespace cf
+
+extern "C" int cf_cluster_solve(int64_t m, int64_t n, int64_t o, const int64_t* rows, const int64_t* cols,
+                                const double* vals, const double* b, const double* c, int64_t n_blocks,
+                                const int64_t* block_sizes, const cf_config* cfg, double* x_out, double* lam_out,
+                                cf_report* final_report, int32_t* n_reports, cf_report* trace, int64_t trace_cap,
+                                cf_problem_checks* checks, int32_t* cluster_used, double* elapsed_ms) {
+    if (m < 1 || n < 1 || o < 0 || !cfg || !x_out || !lam_out || !final_report || !n_reports || !cluster_used ||
+        trace_cap < 0 || (trace_cap > 0 && !trace)) {
+        set_error("cf_cluster_solve: bad arguments");
+        return CF_EINVAL;
+    }
+    *cluster_used = 0;
+    if (cfg->max_iters < 1 || cfg->check_every < 1 || !(cfg->mu > 0)) {
+        set_error("cf_cluster_solve: invalid config");
+        return CF_EINVAL;
+    }
+    if (m + 1 >= INT32_MAX / 4 || n + 1 >= INT32_MAX / 4) return CF_OK;   // not eligible
+    cf_plan* plan = nullptr;
+    int rc = cf_plan_create_mode(m, n, o, rows, cols, vals, b, c, n_blocks, block_sizes, 0, nullptr, checks,
+                                 /*batch_mode=*/1, &plan);
+    if (rc != CF_OK) return rc;
+    struct Guard {
+        cf_plan* p;
+        ~Guard() { cf_plan_destroy(p); }
+    } guard{plan};
+    cudaStream_t st = plan->stream;
+    std::vector<int32_t> rp(m + 1), cp(n + 1), kp;
+    CF_CUDA(cudaMemcpyAsync(rp.data(), plan->rowptr.p, (m + 1) * 4, cudaMemcpyDeviceToHost, st));
+    CF_CUDA(cudaMemcpyAsync(cp.data(), plan->colptr.p, (n + 1) * 4, cudaMemcpyDeviceToHost, st));
+    if (!plan->all_unit) {
+        kp.resize(plan->n_blocks + 1);
+        CF_CUDA(cudaMemcpyAsync(kp.data(), plan->cone_ptr.p, (plan->n_blocks + 1) * 4, cudaMemcpyDeviceToHost, st));
+    }
+    CF_CUDA(cudaStreamSynchronize(st));
+    int dev = 0, max_smem = 0;
+    CF_CUDA(cudaGetDevice(&dev));
+    CF_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    // candidate cut points: every row; column cuts only at cone boundaries
+    std::vector<int32_t> row_allowed(m + 1), col_allowed;
+    for (int64_t i = 0; i <= m; ++i) row_allowed[i] = (int32_t)i;
+    if (plan->all_unit) {
+        col_allowed.resize(n + 1);
+        for (int64_t j = 0; j <= n; ++j) col_allowed[j] = (int32_t)j;
+    } else {
+        col_allowed = kp;
+    }
+    ClusterArgs a{};
+    size_t smem = 0;
+    int C = 0;
+    for (int cand = 1; cand <= kMaxCluster; cand *= 2) {
+        ClusterArgs t{};
+        balanced_cuts(rp, row_allowed, cand, t.row_cut);
+        std::vector<int32_t> kc(cand + 1);
+        balanced_cuts(cp, col_allowed, cand, kc.data());
+        for (int q = 0; q <= cand; ++q) {
+            t.col_cut[q] = col_allowed[kc[q]];
+            t.cone_cut[q] = plan->all_unit ? 0 : kc[q];
+        }
+        int cm = 0, cn = 0, cor = 0, coc = 0, ck = 0;
+        for (int q = 0; q < cand; ++q) {
+            cm = std::max(cm, t.row_cut[q + 1] - t.row_cut[q]);
+            cn = std::max(cn, t.col_cut[q + 1] - t.col_cut[q]);
+            cor = std::max(cor, rp[t.row_cut[q + 1]] - rp[t.row_cut[q]]);
+            coc = std::max(coc, cp[t.col_cut[q + 1]] - cp[t.col_cut[q]]);
+            ck = std::max(ck, t.cone_cut[q + 1] - t.cone_cut[q]);
+        }
+        const size_t s = cluster_smem((int)m, (int)n, cm, cn, cor, coc, ck);
+        if (s + 1024 > (size_t)max_smem) continue;   // room for the kernel's static shared memory
+        t.C = cand;
+        t.cap_m = cm;
+        t.cap_n = cn;
+        t.cap_or = cor;
+        t.cap_oc = coc;
+        t.cap_k = ck;
+        a = t;
+        smem = s;
+        C = cand;
+        // one column and one row per thread fits: more CTAs would only add barrier and store cost
+        if (cn <= kCT && cm <= kCT) break;
+    }
+    if (C == 0) return CF_OK;   // does not fit a cluster: the caller uses cf_plan_solve
+    // function attributes are process-wide: set them once, to the limits, so concurrent
+    // solves (solve_batch / run_bench threads) never lower each other's
+    static std::once_flag attr_once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(attr_once, [&] {
+        cudaFuncAttributes fa{};
+        attr_err = cudaFuncGetAttributes(&fa, k_cluster);
+        if (attr_err == cudaSuccess)
+            attr_err = cudaFuncSetAttribute(k_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            max_smem - (int)fa.sharedSizeBytes);
+        if (attr_err == cudaSuccess)
+            attr_err = cudaFuncSetAttribute(k_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    });
+    CF_CUDA(attr_err);
+    DevBuf<double> d_x, d_lam;
+    DevBuf<cf_report> d_final, d_trace;
+    DevBuf<int32_t> d_nrep;
+    CF_TRY(d_x.alloc(n));
+    CF_TRY(d_lam.alloc(m));
+    CF_TRY(d_final.alloc(1));
+    CF_TRY(d_trace.alloc(std::max<int64_t>(1, trace_cap)));
+    CF_TRY(d_nrep.alloc(1));
+    a.M = (int32_t)m;
+    a.N = (int32_t)n;
+    a.rowptr = plan->rowptr.p;
+    a.colidx = plan->colidx.p;
+    a.valr = plan->valr.p;
+    a.colptr = plan->colptr.p;
+    a.rowidx = plan->rowidx.p;
+    a.valc = plan->valc.p;
+    a.b = plan->b.p;
+    a.c = plan->c.p;
+    a.fu = plan->fu.p;
+    a.db = plan->db.p;
+    a.cone_ptr = plan->cone_ptr.p;
+    a.cones = plan->all_unit ? 0 : 1;
+    a.cfg = *cfg;
+    a.x_out = d_x.p;
+    a.lam_out = d_lam.p;
+    a.trace = d_trace.p;
+    a.trace_cap = trace_cap;
+    a.n_reports = d_nrep.p;
+    a.final_report = d_final.p;
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(C, 1, 1);
+    lc.blockDim = dim3(kCT, 1, 1);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    CF_CUDA(cudaEventRecord(plan->ev0, st));
+    CF_CUDA(cudaLaunchKernelEx(&lc, k_cluster, a));
+    CF_LAUNCHED();
+    CF_CUDA(cudaEventRecord(plan->ev1, st));
+    CF_CUDA(cudaEventSynchronize(plan->ev1));
+    float ms = 0.f;
+    CF_CUDA(cudaEventElapsedTime(&ms, plan->ev0, plan->ev1));
+    if (elapsed_ms) *elapsed_ms = ms;
+    CF_CUDA(cudaMemcpyAsync(x_out, d_x.p, n * 8, cudaMemcpyDeviceToHost, st));
+    CF_CUDA(cudaMemcpyAsync(lam_out, d_lam.p, m * 8, cudaMemcpyDeviceToHost, st));
+    CF_CUDA(cudaMemcpyAsync(final_report, d_final.p, sizeof(cf_report), cudaMemcpyDeviceToHost, st));
+    CF_CUDA(cudaMemcpyAsync(n_reports, d_nrep.p, 4, cudaMemcpyDeviceToHost, st));
+    if (trace_cap > 0)
+        CF_CUDA(cudaMemcpyAsync(trace, d_trace.p, trace_cap * sizeof(cf_report), cudaMemcpyDeviceToHost, st));
+    CF_CUDA(cudaStreamSynchronize(st));
+    *cluster_used = C;
     return CF_OK;
 }
