@@ -15,6 +15,7 @@
 // returns.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <mutex>
 
 #include "cf_common.h"
@@ -869,7 +870,10 @@ extern "C" int cf_cluster_solve(int64_t m, int64_t n, int64_t o, const int64_t* 
     ClusterArgs a{};
     size_t smem = 0;
     int C = 0;
+    const char* force = getenv("CF_CLUSTER_SIZE");   // experiments: try only this cluster size
+    const int only = force ? atoi(force) : 0;
     for (int cand = 1; cand <= kMaxCluster; cand *= 2) {
+        if (only > 0 && cand != only) continue;
         ClusterArgs t{};
         balanced_cuts(rp, row_allowed, cand, t.row_cut);
         std::vector<int32_t> kc(cand + 1);
@@ -897,8 +901,10 @@ extern "C" int cf_cluster_solve(int64_t m, int64_t n, int64_t o, const int64_t* 
         a = t;
         smem = s;
         C = cand;
-        // one column and one row per thread fits: more CTAs would only add barrier and store cost
-        if (cn <= kCT && cm <= kCT) break;
+        // Measured (tools/cluster_sizes.py): a larger cluster shortens each CTA's
+        // passes but adds barrier and remote-store cost. Take the smallest size with at most
+        // ~2,800 nonzeros and 1,024 rows or columns per CTA, and at least 4 CTAs once o >= 2,000.
+        if (cor <= 2800 && coc <= 2800 && cm <= 1024 && cn <= 1024 && (cand >= 4 || o < 2000)) break;
     }
     if (C == 0) return CF_OK;   // does not fit a cluster: the caller uses cf_plan_solve
     // function attributes are process-wide: set them once, to the limits, so concurrent

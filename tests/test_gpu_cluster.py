@@ -49,7 +49,7 @@ def _same(got, ref):
     (("lp", 1000, 2000, 0.01, 0), dict(eps_prim=1e-4, eps_dual=1e-4, eps_gap=1e-4), None),   # C1
     (("lp", 300, 500, 0.02, 5), dict(mu=0.3, max_iters=4000, check_every=10), None),
     (("socp4", 400, 800, 0.01, 7), dict(mu=0.7, max_iters=3000), None),
-    (("lp", 1500, 6000, 0.0017, 9), dict(max_iters=2000, check_every=25), 16),           # 16-CTA cluster
+    (("lp", 1500, 6000, 0.0017, 9), dict(max_iters=2000, check_every=25), None),
     (("lp", 5, 9, 0.4, 99), dict(eps_prim=1e-4, eps_dual=1e-4, eps_gap=1e-4, max_iters=5000), None),
 ])
 def test_cluster_equals_plan(spec, cfg_kw, cluster, monkeypatch):
@@ -113,4 +113,16 @@ def test_cluster_declines_large_and_degenerate(monkeypatch):
     a = TripletMatrix(6, 5, np.array([0, 0, 3, 5]), np.array([1, 4, 1, 0]), np.array([2.0, -1.0, 0.5, 3.0]))
     q = ProblemInstance(a, np.arange(6.0), np.ones(5), ConeSpec((1, 1, 1, 1, 1)))
     got, ref, used = _both(q, SolverConfig(max_iters=300, check_every=7), monkeypatch)
+    _same(got, ref)
+
+
+@pytest.mark.parametrize("size", [1, 2, 4, 8, 16])
+def test_every_cluster_size_equals_plan(size, monkeypatch):
+    """CF_CLUSTER_SIZE forces the cluster size: every size gives the plan's iterates."""
+    from paper_2203_05027_b200 import GenSpec, SolverConfig, generate
+
+    p = generate(GenSpec(300, 640, 0.02, "socp4" if size % 2 else "lp", seed=20 + size))
+    monkeypatch.setenv("CF_CLUSTER_SIZE", str(size))
+    got, ref, used = _both(p, SolverConfig(mu=0.8, max_iters=1500, check_every=15), monkeypatch)
+    assert used == size
     _same(got, ref)
