@@ -24,6 +24,9 @@
 namespace cf {
 namespace {
 
+#ifndef CF_CLUSTER_SEG
+#define CF_CLUSTER_SEG 8   // loads in flight per batch in the cluster kernel's segment sums
+#endif
 #ifndef CF_BATCH_THREADS
 #define CF_BATCH_THREADS 256
 #endif
@@ -98,6 +101,32 @@ __device__ __forceinline__ MuDivB make_mudiv_b(double mu) {
 
 // sequential sum of val[q] * g[idx[q]] over [p0, p1) in order, four independent
 // shared-memory loads in flight (the adds stay in canonical order)
+// seg_dot with every load of a batch of kB issued before the batch's adds, the tail
+// predicated instead of a one-by-one remainder loop: the dependent chain of a short
+// segment is ceil(len/kB) x (idx -> gather) + len adds. Same sequential order of the same
+// __dadd_rn/__dmul_rn, so bit-identical to seg_dot (the cluster kernel's passes are
+// latency chains, not issue-bound like the batched kernel's).
+template <int kB>
+__device__ __forceinline__ double seg_dot_pf(const double* __restrict__ val, const int32_t* __restrict__ idx,
+                                             const double* __restrict__ g, int p0, int p1) {
+    double acc = 0.0;
+    for (int q = p0; q < p1; q += kB) {
+        int ii[kB];
+        double vv[kB], gg[kB];
+#pragma unroll
+        for (int e = 0; e < kB; ++e) {
+            ii[e] = q + e < p1 ? idx[q + e] : 0;
+            vv[e] = q + e < p1 ? val[q + e] : 0.0;
+        }
+#pragma unroll
+        for (int e = 0; e < kB; ++e) gg[e] = q + e < p1 ? g[ii[e]] : 0.0;
+#pragma unroll
+        for (int e = 0; e < kB; ++e)
+            if (q + e < p1) acc = __dadd_rn(acc, __dmul_rn(vv[e], gg[e]));
+    }
+    return acc;
+}
+
 __device__ __forceinline__ double seg_dot(const double* __restrict__ val, const int32_t* __restrict__ idx,
                                           const double* __restrict__ g, int p0, int p1) {
     double acc = 0.0;
@@ -650,7 +679,7 @@ __global__ void __launch_bounds__(kCT, 1) k_cluster(const ClusterArgs a) {
         // ---- column pass on the CTA's columns (solver.py:168-176,186-188,196)
         for (int j = t; j < n; j += kCT) {
             const int p0 = colptr[j], p1 = colptr[j + 1];
-            const double ath = seg_dot(valc, rowidx, hr, p0, p1);
+            const double ath = seg_dot_pf<CF_CLUSTER_SEG>(valc, rowidx, hr, p0, p1);
             const int cnt = p1 - p0;
             const double fv = fvs[j];
             const double xj = xr[c0 + j], zj = z[j], dj = dl[j];
@@ -681,7 +710,7 @@ __global__ void __launch_bounds__(kCT, 1) k_cluster(const ClusterArgs a) {
         // ---- row pass on the CTA's rows (solver.py:179-183,194-195)
         for (int i = t; i < m; i += kCT) {
             const int p0 = rowptr[i], p1 = rowptr[i + 1];
-            const double axi = seg_dot(valr, colidx, xr, p0, p1);
+            const double axi = seg_dot_pf<CF_CLUSTER_SEG>(valr, colidx, xr, p0, p1);
             const double bi = b[i];
             const double r = fu[i] * (db[i] + axi);
             const double ln = lamr[r0 + i] + mu * (r - bi);
