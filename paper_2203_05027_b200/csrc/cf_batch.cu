@@ -160,6 +160,18 @@ __device__ __forceinline__ void project_block_b(const double* w, int q, double* 
     }
 }
 
+#ifndef CF_BATCH_SEG
+#define CF_BATCH_SEG 0   // 0: seg_dot (unrolled by 4); N: seg_dot_pf<N>
+#endif
+__device__ __forceinline__ double batch_seg_dot(const double* __restrict__ val, const int32_t* __restrict__ idx,
+                                                const double* __restrict__ g, int p0, int p1) {
+#if CF_BATCH_SEG
+    return seg_dot_pf<CF_BATCH_SEG>(val, idx, g, p0, p1);
+#else
+    return seg_dot(val, idx, g, p0, p1);
+#endif
+}
+
 __global__ void __launch_bounds__(kBT, CF_BATCH_MINB) k_batch(const BatchArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int CM = a.cap_m, CN = a.cap_n, CO = a.cap_o;
@@ -246,7 +258,7 @@ __global__ void __launch_bounds__(kBT, CF_BATCH_MINB) k_batch(const BatchArgs a)
             // ---- column pass: x_update, z_update, delta update (solver.py:168-176,186-188,196)
             for (int j = t; j < n; j += kBT) {
                 const int p0 = colptr[j], p1 = colptr[j + 1];
-                const double ath = seg_dot(valc, rowidx, h, p0, p1);
+                const double ath = batch_seg_dot(valc, rowidx, h, p0, p1);
                 const int cnt = p1 - p0;
                 const double fv = fvs[j];
                 const double xj = x[j], zj = z[j], dj = dl[j];
@@ -275,7 +287,7 @@ __global__ void __launch_bounds__(kBT, CF_BATCH_MINB) k_batch(const BatchArgs a)
             // ---- row pass: y_update + lam/gamma of dual_update (solver.py:179-183,194-195)
             for (int i = t; i < m; i += kBT) {
                 const int p0 = rowptr[i], p1 = rowptr[i + 1];
-                const double axi = seg_dot(valr, colidx, x, p0, p1);
+                const double axi = batch_seg_dot(valr, colidx, x, p0, p1);
                 const double bi = b[i];
                 const double r = fu[i] * (db[i] + axi);
                 const double ln = lam[i] + mu * (r - bi);
