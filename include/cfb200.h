@@ -153,11 +153,17 @@ int cf_plan_report(cf_plan* plan, double mu, cf_report* out);
 /* The whole loop of solve() (solver.py:309-334) from the current state:
  * reports every check_every iterations and at max_iters, device-side
  * termination (check_termination, solver.py:245-272) with early exit.
- * trace: caller buffer of trace_cap reports; *n_reports = entries written
- * (the last one is the SolveResult.report). x_out (n), lam_out (m): host. */
+ * trace: caller buffer of trace_cap reports (any size >= 0): the first
+ * min(trace_cap, *n_reports) reports are written there; *n_reports = reports
+ * of the whole solve (the last one is the SolveResult.report). The plan keeps
+ * every report (growing one per check, like solver.py:310, 325), so a caller
+ * with a small buffer fetches the rest with cf_plan_trace. x_out (n),
+ * lam_out (m): host. */
 int cf_plan_solve(cf_plan* plan, const cf_config* cfg,
                   double* x_out, double* lam_out,
                   cf_report* trace, int64_t trace_cap, int64_t* n_reports);
+/* Reports [start, start + count) of the last cf_plan_solve on this plan. */
+int cf_plan_trace(cf_plan* plan, int64_t start, int64_t count, cf_report* out);
 
 /* ---------------------------------------------------------------- operators
  * Matrix-free products on device vectors (uv.py:106-131 composed):

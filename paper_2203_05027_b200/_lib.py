@@ -99,6 +99,7 @@ SIGNATURES = {
     "cf_plan_iterate": (c_int, [_P, c_double, c_int64]),
     "cf_plan_report": (c_int, [_P, c_double, POINTER(CfReport)]),
     "cf_plan_solve": (c_int, [_P, POINTER(CfConfig), _P, _P, POINTER(CfReport), c_int64, _I64]),
+    "cf_plan_trace": (c_int, [_P, c_int64, c_int64, POINTER(CfReport)]),
     "cf_apply_A": (c_int, [_P, _P, _P]),
     "cf_apply_At": (c_int, [_P, _P, _P]),
     "cf_apply_At_async": (c_int, [_P, _P, _P]),

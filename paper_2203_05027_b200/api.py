@@ -251,6 +251,7 @@ def solve(p, cfg: SolverConfig | None = None, init: SolverState | None = None) -
 # Mid-size problems run in the cluster-resident kernel (csrc/cf_batch.cu k_cluster): one
 # launch for the whole loop, iterates in the distributed shared memory of up to 16 CTAs.
 # The estimate below is conservative; cf_cluster_solve makes the exact decision.
+_CLUSTER_TRACE_MAX = 1 << 16   # cf_batch.cu kMaxClusterTrace
 _LAST_CLUSTER = 0   # cluster size of the last cf_cluster_solve call (0: did not fit), for tests
 
 _PLAN_KNOBS = ("CF_PANEL_MB", "CF_BAND_MB", "CF_FORCE_LARGE_TILES", "CF_NO_LARGE_TILES", "CF_GROUP_CONES",
@@ -293,6 +294,8 @@ def _solve_cluster(p, cfg, timing: dict | None = None) -> SolveResult | None:
     final = CfReport()
     nrep = ctypes.c_int32()
     cap = -(-int(cfg.max_iters) // int(cfg.check_every))
+    if cap > _CLUSTER_TRACE_MAX:   # the cluster kernel keeps its trace on the device: plan path
+        return None
     tr = (CfReport * cap)()
     chk = CfChecks()
     used = ctypes.c_int32()

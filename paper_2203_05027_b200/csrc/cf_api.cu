@@ -291,11 +291,12 @@ int cf_plan_solve(cf_plan* p, const cf_config* cfg, double* x_out, double* lam_o
         return CF_EINVAL;
     }
     const int64_t n_chunks = (cfg->max_iters + cfg->check_every - 1) / cfg->check_every;
-    if (trace_cap < n_chunks) {
-        set_error("cf_plan_solve: trace_cap < ceil(max_iters / check_every)");
+    if (trace_cap < 0) {
+        set_error("cf_plan_solve: trace_cap < 0");
         return CF_EINVAL;
     }
     *n_reports = 0;
+    p->trace_all.clear();
     cudaStream_t st = p->stream;
     p->export_mu = cfg->mu;
     prof_reset(p);
@@ -311,7 +312,9 @@ int cf_plan_solve(cf_plan* p, const cf_config* cfg, double* x_out, double* lam_o
     auto consume = [&](int64_t c) -> int {
         CF_CUDA(cudaEventSynchronize(evs[c % kDepth]));
         const cf_report& r = p->host_reports[c % p->host_ring];
-        trace[read++] = r;
+        p->trace_all.push_back(r);
+        if (read < trace_cap) trace[read] = r;
+        ++read;
         if (r.status != CF_STATUS_RUNNING) {
             finished = true;
             k_final = r.iter;
@@ -360,6 +363,16 @@ int cf_plan_solve(cf_plan* p, const cf_config* cfg, double* x_out, double* lam_o
     if (x_out && p->n) CF_CUDA(cudaMemcpyAsync(x_out, p->x.p, p->n * 8, cudaMemcpyDeviceToHost, st));
     if (lam_out && p->m) CF_CUDA(cudaMemcpyAsync(lam_out, p->lam.p, p->m * 8, cudaMemcpyDeviceToHost, st));
     CF_CUDA(cudaStreamSynchronize(st));
+    return CF_OK;
+}
+
+int cf_plan_trace(cf_plan* p, int64_t start, int64_t count, cf_report* out) {
+    CF_TRY(check_plan(p, "cf_plan_trace"));
+    if (start < 0 || count < 0 || start + count > (int64_t)p->trace_all.size() || (count > 0 && !out)) {
+        set_error("cf_plan_trace: range outside the last solve's trace");
+        return CF_EINVAL;
+    }
+    for (int64_t i = 0; i < count; ++i) out[i] = p->trace_all[start + i];
     return CF_OK;
 }
 

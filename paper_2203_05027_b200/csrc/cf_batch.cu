@@ -99,8 +99,6 @@ __device__ __forceinline__ MuDivB make_mudiv_b(double mu) {
     return MuDivB{mu, 1.0 / mu, fr == 0.5 && e > -1000 && e < 1000};
 }
 
-// sequential sum of val[q] * g[idx[q]] over [p0, p1) in order, four independent
-// shared-memory loads in flight (the adds stay in canonical order)
 // seg_dot with every load of a batch of kB issued before the batch's adds, the tail
 // predicated instead of a one-by-one remainder loop: the dependent chain of a short
 // segment is ceil(len/kB) x (idx -> gather) + len adds. Same sequential order of the same
@@ -127,6 +125,8 @@ __device__ __forceinline__ double seg_dot_pf(const double* __restrict__ val, con
     return acc;
 }
 
+// sequential sum of val[q] * g[idx[q]] over [p0, p1) in order, four independent
+// shared-memory loads in flight (the adds stay in canonical order)
 __device__ __forceinline__ double seg_dot(const double* __restrict__ val, const int32_t* __restrict__ idx,
                                           const double* __restrict__ g, int p0, int p1) {
     double acc = 0.0;
@@ -555,6 +555,9 @@ namespace cg = cooperative_groups;
 
 constexpr int kCT = 512;              // threads per cluster CTA
 constexpr int kMaxCluster = 16;
+// reports the cluster kernel keeps on the device (112 B each); larger max_iters/check_every
+// ratios go to the plan path, whose host trace grows one report at a time
+constexpr int64_t kMaxClusterTrace = 1 << 16;
 
 struct ClusterArgs {
     int32_t C;
@@ -585,8 +588,11 @@ struct ClusterArgs {
 };
 
 size_t cluster_smem(int M, int N, int cm, int cn, int cor, int coc, int ck) {
-    return sizeof(double) * (size_t)(N + 3 * M + cor + coc + 4 * cm + 6 * cn + 32 + 16 * kMaxCluster) +
-           sizeof(int32_t) * (size_t)(cor + coc + cm + 1 + cn + 1 + ck + 1) + 16;
+    // every term in size_t: m and n may reach INT32_MAX / 4 through the C ABI
+    const size_t nd = (size_t)N + 3 * (size_t)M + (size_t)cor + (size_t)coc + 4 * (size_t)cm + 6 * (size_t)cn + 32 +
+                      16 * (size_t)kMaxCluster;
+    const size_t ni = (size_t)cor + (size_t)coc + (size_t)cm + 1 + (size_t)cn + 1 + (size_t)ck + 1;
+    return sizeof(double) * nd + sizeof(int32_t) * ni + 16;
 }
 
 __global__ void __launch_bounds__(kCT, 1) k_cluster(const ClusterArgs a) {
@@ -879,30 +885,43 @@ extern "C" int cf_cluster_solve(int64_t m, int64_t n, int64_t o, const int64_t* 
         return CF_EINVAL;
     }
     if (m + 1 >= INT32_MAX / 4 || n + 1 >= INT32_MAX / 4) return CF_OK;   // not eligible
-    cf_plan* plan = nullptr;
-    int rc = cf_plan_create_mode(m, n, o, rows, cols, vals, b, c, n_blocks, block_sizes, 0, nullptr, checks,
-                                 /*batch_mode=*/1, &plan);
-    if (rc != CF_OK) return rc;
-    struct Guard {
-        cf_plan* p;
-        ~Guard() { cf_plan_destroy(p); }
-    } guard{plan};
-    cudaStream_t st = plan->stream;
-    std::vector<int32_t> rp(m + 1), cp(n + 1), kp;
-    CF_CUDA(cudaMemcpyAsync(rp.data(), plan->rowptr.p, (m + 1) * 4, cudaMemcpyDeviceToHost, st));
-    CF_CUDA(cudaMemcpyAsync(cp.data(), plan->colptr.p, (n + 1) * 4, cudaMemcpyDeviceToHost, st));
-    if (!plan->all_unit) {
-        kp.resize(plan->n_blocks + 1);
-        CF_CUDA(cudaMemcpyAsync(kp.data(), plan->cone_ptr.p, (plan->n_blocks + 1) * 4, cudaMemcpyDeviceToHost, st));
+    {
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+            (void)cudaGetLastError();
+            set_error("cf_cluster_solve: no CUDA device visible (libcfb200 has no CPU path)");
+            return CF_ECUDA;
+        }
     }
-    CF_CUDA(cudaStreamSynchronize(st));
+    // Decide the fit from host-side row/column counts BEFORE any device setup, so a problem
+    // that does not fit costs one O(o) count here and the caller builds its plan only once.
+    // Out-of-range entries are skipped; an invalid problem fails in cf_plan_create_mode below.
+    std::vector<int32_t> rp(m + 1, 0), cp(n + 1, 0), kp;
+    for (int64_t k = 0; k < o; ++k) {
+        if (rows[k] >= 0 && rows[k] < m) ++rp[rows[k] + 1];
+        if (cols[k] >= 0 && cols[k] < n) ++cp[cols[k] + 1];
+    }
+    for (int64_t i = 0; i < m; ++i) rp[i + 1] += rp[i];
+    for (int64_t j = 0; j < n; ++j) cp[j + 1] += cp[j];
+    int64_t maxsize = 0, ksum = 0;
+    for (int64_t q = 0; q < n_blocks; ++q) maxsize = std::max<int64_t>(maxsize, block_sizes[q]);
+    const bool all_unit = (n_blocks == 0 || maxsize == 1);
+    if (!all_unit) {
+        kp.resize(n_blocks + 1);
+        kp[0] = 0;
+        for (int64_t q = 0; q < n_blocks; ++q) {
+            ksum += std::max<int64_t>(0, block_sizes[q]);
+            if (ksum > n) return CF_OK;   // invalid cones: the plan path reports it
+            kp[q + 1] = (int32_t)ksum;
+        }
+    }
     int dev = 0, max_smem = 0;
     CF_CUDA(cudaGetDevice(&dev));
     CF_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     // candidate cut points: every row; column cuts only at cone boundaries
     std::vector<int32_t> row_allowed(m + 1), col_allowed;
     for (int64_t i = 0; i <= m; ++i) row_allowed[i] = (int32_t)i;
-    if (plan->all_unit) {
+    if (all_unit) {
         col_allowed.resize(n + 1);
         for (int64_t j = 0; j <= n; ++j) col_allowed[j] = (int32_t)j;
     } else {
@@ -921,7 +940,7 @@ extern "C" int cf_cluster_solve(int64_t m, int64_t n, int64_t o, const int64_t* 
         balanced_cuts(cp, col_allowed, cand, kc.data());
         for (int q = 0; q <= cand; ++q) {
             t.col_cut[q] = col_allowed[kc[q]];
-            t.cone_cut[q] = plan->all_unit ? 0 : kc[q];
+            t.cone_cut[q] = all_unit ? 0 : kc[q];
         }
         int cm = 0, cn = 0, cor = 0, coc = 0, ck = 0;
         for (int q = 0; q < cand; ++q) {
@@ -948,6 +967,16 @@ extern "C" int cf_cluster_solve(int64_t m, int64_t n, int64_t o, const int64_t* 
         if (cor <= 2800 && coc <= 2800 && cm <= 1024 && cn <= 1024 && (cand >= 4 || o < 2000)) break;
     }
     if (C == 0) return CF_OK;   // does not fit a cluster: the caller uses cf_plan_solve
+    if (trace_cap > kMaxClusterTrace) return CF_OK;   // huge max_iters: the plan path streams its trace
+    cf_plan* plan = nullptr;
+    int rc = cf_plan_create_mode(m, n, o, rows, cols, vals, b, c, n_blocks, block_sizes, 0, nullptr, checks,
+                                 /*batch_mode=*/1, &plan);
+    if (rc != CF_OK) return rc;
+    struct Guard {
+        cf_plan* p;
+        ~Guard() { cf_plan_destroy(p); }
+    } guard{plan};
+    cudaStream_t st = plan->stream;
     // function attributes are process-wide: set them once, to the limits, so concurrent
     // solves (solve_batch / run_bench threads) never lower each other's
     static std::once_flag attr_once;
@@ -961,15 +990,16 @@ extern "C" int cf_cluster_solve(int64_t m, int64_t n, int64_t o, const int64_t* 
         if (attr_err == cudaSuccess)
             attr_err = cudaFuncSetAttribute(k_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     });
-    CF_CUDA(attr_err);
+    if (attr_err != cudaSuccess) return CF_OK;   // cannot configure the kernel here: plan path
     DevBuf<double> d_x, d_lam;
     DevBuf<cf_report> d_final, d_trace;
     DevBuf<int32_t> d_nrep;
-    CF_TRY(d_x.alloc(n));
-    CF_TRY(d_lam.alloc(m));
-    CF_TRY(d_final.alloc(1));
-    CF_TRY(d_trace.alloc(std::max<int64_t>(1, trace_cap)));
-    CF_TRY(d_nrep.alloc(1));
+    // an out-of-memory here means "does not fit": decline, the plan path allocates its own
+    if (d_x.alloc(n) != CF_OK || d_lam.alloc(m) != CF_OK || d_final.alloc(1) != CF_OK ||
+        d_trace.alloc(std::max<int64_t>(1, trace_cap)) != CF_OK || d_nrep.alloc(1) != CF_OK) {
+        (void)cudaGetLastError();
+        return CF_OK;
+    }
     a.M = (int32_t)m;
     a.N = (int32_t)n;
     a.rowptr = plan->rowptr.p;
@@ -1003,8 +1033,23 @@ extern "C" int cf_cluster_solve(int64_t m, int64_t n, int64_t o, const int64_t* 
     attr[0].val.clusterDim.z = 1;
     lc.attrs = attr;
     lc.numAttrs = 1;
+    // a cluster of C CTAs with this much shared memory may not be schedulable (MPS, an
+    // SM-limited context, a busy GPU): treat that like "does not fit"
+    int active = 0;
+    if (cudaOccupancyMaxActiveClusters(&active, k_cluster, &lc) != cudaSuccess || active < 1) {
+        (void)cudaGetLastError();
+        return CF_OK;
+    }
     CF_CUDA(cudaEventRecord(plan->ev0, st));
-    CF_CUDA(cudaLaunchKernelEx(&lc, k_cluster, a));
+    {
+        const cudaError_t le = cudaLaunchKernelEx(&lc, k_cluster, a);
+        if (le == cudaErrorLaunchOutOfResources ||
+            le == cudaErrorMemoryAllocation || le == cudaErrorInvalidClusterSize) {
+            (void)cudaGetLastError();
+            return CF_OK;
+        }
+        CF_CUDA(le);
+    }
     CF_LAUNCHED();
     CF_CUDA(cudaEventRecord(plan->ev1, st));
     CF_CUDA(cudaEventSynchronize(plan->ev1));

@@ -191,6 +191,7 @@ struct cf_plan {
     double* x_own = nullptr;                   // cf_plan_bind_x: the plan's own x while x.p is external
     cf::DevBuf<int32_t> nf_flag;               // report: non-finite implicit y/gamma
     cf_report* host_reports = nullptr;         // pinned ring
+    std::vector<cf_report> trace_all;          // every report of the last cf_plan_solve (grows per report)
     int64_t host_ring = 0;
 
     // timing

@@ -175,15 +175,23 @@ class DevicePlan:
 
     def run(self, cfg: CfConfig, want_x: bool = True):
         """The solve() loop; returns (x, lam, list of report dicts)."""
+        # a bounded first buffer; a longer trace is fetched afterwards (the plan keeps every
+        # report), so max_iters=10**9 costs nothing until the reports exist
         n_chunks = -(-int(cfg.max_iters) // int(cfg.check_every))
-        trace = (CfReport * max(n_chunks, 1))()
+        cap = max(1, min(n_chunks, 4096))
+        trace = (CfReport * cap)()
         nrep = c_int64()
         x = np.empty(self.n) if want_x else None
         lam = np.empty(self.m) if want_x else None
         check(lib().cf_plan_solve(self.handle, byref(cfg), _ptr(x) if want_x else None,
-                                  _ptr(lam) if want_x else None, trace, n_chunks, byref(nrep)),
+                                  _ptr(lam) if want_x else None, trace, cap, byref(nrep)),
               "cf_plan_solve")
-        return x, lam, [report_to_dict(trace[i]) for i in range(nrep.value)]
+        out = [report_to_dict(trace[i]) for i in range(min(cap, nrep.value))]
+        if nrep.value > cap:
+            rest = (CfReport * (nrep.value - cap))()
+            check(lib().cf_plan_trace(self.handle, cap, nrep.value - cap, rest), "cf_plan_trace")
+            out.extend(report_to_dict(r) for r in rest)
+        return x, lam, out
 
     def last_timing(self) -> dict:
         ms, rms, cms = c_double(), c_double(), c_double()

@@ -195,6 +195,7 @@ class CudaRankBackend:
 
         if getattr(self, "_p2p_own", None):
             return
+        self._p2p_group = group
         torch = self.torch
         world = dist.get_world_size(group)
         rank = dist.get_rank(group)
@@ -258,6 +259,12 @@ class CudaRankBackend:
         _lib.check(self.lib.cf_plan_bind_x(self.plan.handle, None))
         for ptr in self._p2p_opened:
             self.lib.cf_ipc_close(ctypes.c_void_p(ptr))
+        # every peer must have closed its mapping of our buffers before we free them (freeing
+        # exported memory before the importer's cudaIpcCloseMemHandle is undefined)
+        import torch.distributed as dist
+
+        if dist.is_available() and dist.is_initialized():
+            dist.barrier(group=getattr(self, "_p2p_group", None))
         for ptr in self._p2p_own:
             self.lib.cf_ipc_free(ctypes.c_void_p(ptr))
         self._p2p_own, self._p2p_opened = [], []

@@ -389,58 +389,6 @@ def coneprob_cases():
     print("coneprob_cases:", len(texts), "cases,", sum(1 for x in lines if x >= 0), "errors")
 
 
-CLI_CASES = (
-    # (argv with {d} for the scratch directory, needs a GPU on our side)
-    ("generate --m 30 --n 60 --density 0.1 --cone lp --seed 3 --out {d}/g_lp.txt", False),
-    ("generate --m 40 --n 80 --density 0.08 --cone socp4 --seed 5 --raw-c --out {d}/g_soc.txt", False),
-    ("solve {d}/g_lp.txt --eps 1e-4 --trace {d}/t_lp.csv", True),
-    ("solve {d}/g_soc.txt --term osqp --max-iters 3000 --check-every 50 --out {d}/s_soc.sol --trace {d}/t_soc.csv", True),
-    ("solve {d}/g_lp.txt --max-iters 60 --check-every 7 --out {d}/s_max.sol", True),
-    ("solve {d}/g_lp.txt --term target --target-prim 1e-3 --target-gap 1e-3 --mu 0.5 --out {d}/s_tgt.sol", True),
-    ("bench --sizes 2e3,5e3 --densities 0.05,0.1 --cone lp --seed 2 --out {d}/b.csv --workers 1", True),
-    ("bench --sizes 2e3 --densities x --cone lp --seed 2 --out {d}/b2.csv", False),
-    ("bench --sizes 2e3 --densities 0.1 --cone qp --seed 2 --out {d}/b3.csv", False),
-    ("solve {d}/missing.txt", False),
-    ("solve {d}/g_lp.txt --mu -1", False),
-    ("solve {d}/g_lp.txt --term target", False),
-    ("solve {d}/bad.txt", False),
-    ("frobnicate", False),
-)
-
-
-def cli_cases():
-    """The reference CLI (cli.py) run on each CLI_CASES argv: exit code, stdout, stderr, output files."""
-    import contextlib
-    import io
-    import tempfile
-
-    from conefree.cli import run_cli
-
-    argvs, rcs, outs, errs, gpu, fcase, fname, ftext = [], [], [], [], [], [], [], []
-    with tempfile.TemporaryDirectory() as d:
-        with open(os.path.join(d, "bad.txt"), "w") as f:
-            f.write("CONEPROB 1\n2 2 1\nCONES 1 2\n0 5 1.0\n1.0\n2.0\n1.0\n1.0\n")
-        for i, (argv, needs_gpu) in enumerate(CLI_CASES):
-            before = set(os.listdir(d))
-            so, se = io.StringIO(), io.StringIO()
-            with contextlib.redirect_stdout(so), contextlib.redirect_stderr(se):
-                rc = run_cli(argv.replace("{d}", d).split())
-            argvs.append(argv)
-            rcs.append(rc)
-            outs.append(so.getvalue().replace(d, "{d}"))
-            errs.append(se.getvalue().replace(d, "{d}"))
-            gpu.append(needs_gpu)
-            for name in sorted(set(os.listdir(d)) - before):
-                with open(os.path.join(d, name), encoding="utf-8") as f:
-                    fcase.append(i)
-                    fname.append(name)
-                    ftext.append(f.read())
-    np.savez_compressed(os.path.join(OUT, "cli_cases.npz"), argv=np.array(argvs), rc=np.array(rcs),
-                        stdout=np.array(outs), stderr=np.array(errs), gpu=np.array(gpu),
-                        file_case=np.array(fcase), file_name=np.array(fname), file_text=np.array(ftext))
-    print("cli_cases:", len(argvs), "runs,", len(fname), "files, exit codes", rcs)
-
-
 if __name__ == "__main__":
     np.seterr(all="ignore")
     example1()
@@ -451,7 +399,6 @@ if __name__ == "__main__":
     generator()
     bench_rows()
     coneprob_cases()
-    cli_cases()
     for fn in sorted(os.listdir(OUT)):
         if fn.endswith(".npz"):
             print(fn, os.path.getsize(os.path.join(OUT, fn)))
