@@ -305,6 +305,18 @@ int cf_plan_set_profiling(cf_plan* plan, int enable);
 /* Synchronise the plan's stream. */
 int cf_plan_sync(cf_plan* plan);
 
+/* ---------------------------------------------------------------- instance generator (bench tooling)
+ * Counter-based draws for the large synthetic configs, bit-identical to the numpy
+ * restatement paper_2203_05027_b200/cfgen.py (which replaces the PCG64 stream of the
+ * reference generator, generate.py:82-140, with H(seed, stream, k)). Asynchronous on
+ * cuda_stream (a cudaStream_t, NULL = legacy default). */
+/* out[i] = AS241 normal of draw start+i of `stream` */
+int cf_gen_normal(uint64_t seed, uint64_t stream, int64_t start, int64_t count, double* out_dev, void* cuda_stream);
+/* out[i] = draw start+i of stream 0, mod total (cell candidates) */
+int cf_gen_cells(uint64_t seed, int64_t start, int64_t count, int64_t total, int64_t* out_dev, void* cuda_stream);
+/* out[i] = draw start+i of `stream` >> 1 (non-negative sort keys) */
+int cf_gen_keys(uint64_t seed, uint64_t stream, int64_t start, int64_t count, int64_t* out_dev, void* cuda_stream);
+
 /* ---------------------------------------------------------------- CONEPROB text I/O (host)
  * Replaces parse_problem / write_problem (conefree/fileio.py:56-190) with a
  * multi-threaded native reader/writer. Errors reproduce

@@ -138,6 +138,9 @@ SIGNATURES = {
     "cf_ipc_open": (c_int, [c_void_p, POINTER(c_void_p)]),
     "cf_ipc_close": (c_int, [_P]),
     "cf_plan_bind_x": (c_int, [_P, _P]),
+    "cf_gen_normal": (c_int, [ctypes.c_uint64, ctypes.c_uint64, c_int64, c_int64, _P, _P]),
+    "cf_gen_cells": (c_int, [ctypes.c_uint64, c_int64, c_int64, c_int64, _P, _P]),
+    "cf_gen_keys": (c_int, [ctypes.c_uint64, ctypes.c_uint64, c_int64, c_int64, _P, _P]),
 }
 
 _lib = None

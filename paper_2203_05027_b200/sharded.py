@@ -32,7 +32,7 @@ import numpy as np
 from .api import IterationReport, SolveResult, SolverConfig, _decide, norms
 from .problem import ConeSpec, ProblemInstance, TripletMatrix, cone_sizes_array
 
-__all__ = ["solve_distributed", "choose_sharding", "exchange_bytes", "solve_sharded", "run_sharded", "partition", "CudaRankBackend", "assemble_report",
+__all__ = ["solve_distributed", "choose_sharding", "column_cuts", "row_cuts_from_counts", "exchange_bytes", "solve_sharded", "run_sharded", "partition", "CudaRankBackend", "assemble_report",
            "solve_col_sharded", "run_col_sharded", "CudaColBackend", "local_columns"]
 
 # report parts: row = {sum prim^2, max|prim|, max|Ax|, sum b.lam, nonfinite};
@@ -44,23 +44,29 @@ def partition(p, world: int):
 
     Returns (row_cuts[world+1], col_cuts[world+1])."""
     m, n = int(p.A.num_rows), int(p.A.num_cols)
-    counts = np.bincount(np.asarray(p.A.rows, dtype=np.int64), minlength=m)
+    row_cuts = row_cuts_from_counts(np.bincount(np.asarray(p.A.rows, dtype=np.int64), minlength=m), world)
+    return row_cuts, column_cuts(cone_sizes_array(p.cones), n, world)
+
+
+def row_cuts_from_counts(counts, world: int):
+    """Row blocks balanced by nonzeros from per-row counts (numpy or a device tensor's copy)."""
+    counts = np.asarray(counts, dtype=np.int64)
+    m = counts.size
     cum = np.concatenate(([0], np.cumsum(counts)))
-    total = cum[-1]
-    row_cuts = [0]
-    for r in range(1, world):
-        row_cuts.append(int(np.searchsorted(cum, r * total / world, side="left")))
-    row_cuts.append(m)
-    row_cuts = list(np.maximum.accumulate(np.minimum(row_cuts, m)))
-    sizes = cone_sizes_array(p.cones)
+    cuts = [0] + [int(np.searchsorted(cum, r * cum[-1] / world, side="left")) for r in range(1, world)] + [m]
+    return [int(v) for v in np.maximum.accumulate(np.minimum(cuts, m))]
+
+
+def column_cuts(sizes, n: int, world: int):
+    """Cone-aligned column slices of equal-ish size (no cone crosses a slice)."""
+    sizes = np.asarray(sizes, dtype=np.int64)
     starts = np.concatenate(([0], np.cumsum(sizes))) if sizes.size else np.array([0, n])
     col_cuts = [0]
     for r in range(1, world):
         k = int(np.searchsorted(starts, r * n / world, side="left"))
         col_cuts.append(int(starts[min(k, len(starts) - 1)]))
     col_cuts.append(n)
-    col_cuts = list(np.maximum.accumulate(np.minimum(col_cuts, n)))
-    return [int(v) for v in row_cuts], [int(v) for v in col_cuts]
+    return [int(v) for v in np.maximum.accumulate(np.minimum(col_cuts, n))]
 
 
 def local_problem(p, r0: int, r1: int):

@@ -26,10 +26,11 @@ def _close(got, want, scale):
 def test_full_size_report_and_cone_properties(which):
     import torch
 
-    from paper_2203_05027_b200.devgen import c2_spec, c3_spec, generate_device
+    from paper_2203_05027_b200 import cfgen
+    from paper_2203_05027_b200.devgen import c2_spec, c3_spec
 
     spec = c2_spec() if which == "c2" else c3_spec()
-    inst = generate_device(spec["m"], spec["n"], spec["density"], spec["cone_kind"], seed=0)
+    inst = cfgen.generate_device(spec["m"], spec["n"], spec["density"], spec["cone_kind"], 0)   # the bench instance
     plan = inst.plan
     try:
         plan.set_state(1.0, None, export=False)
