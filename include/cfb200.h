@@ -100,6 +100,9 @@ typedef struct cf_problem_checks {
 /* ---------------------------------------------------------------- basics */
 const char* cf_last_error(void);
 int cf_abi_version(void);
+/* Checked build only (libcfb200_checked.so, -DCF_CHECKED=1): device buffers found written
+ * past their end when released (guard canaries); -1 in the product build. */
+long long cf_debug_guard_violations(void);
 /* number of visible CUDA devices (0 on a CPU-only host; never an error) */
 int cf_device_count(int* count);
 

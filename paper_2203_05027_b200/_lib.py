@@ -87,6 +87,7 @@ _I64 = POINTER(c_int64)
 SIGNATURES = {
     "cf_last_error": (c_char_p, []),
     "cf_abi_version": (c_int, []),
+    "cf_debug_guard_violations": (ctypes.c_longlong, []),
     "cf_device_count": (c_int, [POINTER(c_int)]),
     "cf_plan_create": (c_int, [c_int64, c_int64, c_int64, _P, _P, _P, _P, _P, c_int64, _P, c_int, _P,
                                POINTER(CfChecks), POINTER(c_void_p)]),

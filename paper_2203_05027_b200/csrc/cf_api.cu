@@ -1,6 +1,10 @@
 // C ABI of libcfb200 (include/cfb200.h): plan lifetime, warm start / state
 // export, the iteration loop of solve() (solver.py:309-334) with device-side
 // termination, and the matrix-free operators.
+#include <nvtx3/nvToolsExt.h>
+#include <atomic>
+#include <cstdio>
+#include <vector>
 #include <algorithm>
 #include <cstring>
 #include <string>
@@ -37,6 +41,28 @@ void pool_free(void* p) {
     // callers synchronise the plan stream before releasing (plan destroy, scoped setup scratch)
     cudaFreeAsync(p, 0);
     cudaStreamSynchronize(0);
+}
+
+// checked build: canary bytes behind every DevBuf (cf_common.h kGuardBytes)
+static std::atomic<long long> g_guard_violations{0};
+void guard_fill(void* p, size_t used, size_t total) {
+    cudaMemset(static_cast<char*>(p) + used, 0xA5, total - used);
+    cudaDeviceSynchronize();
+}
+void guard_check(const void* p, size_t used, size_t total) {
+    std::vector<unsigned char> h(total - used);
+    cudaDeviceSynchronize();
+    if (cudaMemcpy(h.data(), static_cast<const char*>(p) + used, h.size(), cudaMemcpyDeviceToHost) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    for (size_t i = 0; i < h.size(); ++i) {
+        if (h[i] != 0xA5) {
+            fprintf(stderr, "CF_CHECKED: device buffer of %zu bytes written at byte %zu past its end\n", used, i);
+            ++g_guard_violations;
+            return;
+        }
+    }
 }
 
 int cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
@@ -93,6 +119,8 @@ extern "C" {
 const char* cf_last_error(void) { return g_last_error.c_str(); }
 
 int cf_abi_version(void) { return CF_ABI_VERSION; }
+
+long long cf_debug_guard_violations(void) { return CF_CHECKED ? cf::g_guard_violations.load() : -1; }
 
 int cf_device_count(int* count) {
     int n = 0;
@@ -324,6 +352,10 @@ int cf_plan_solve(cf_plan* p, const cf_config* cfg, double* x_out, double* lam_o
     for (int64_t c = 0; c < n_chunks && !finished; ++c) {
         const int64_t k0 = c * cfg->check_every;
         const int64_t nit = std::min(cfg->check_every, cfg->max_iters - k0);
+        nvtxRangePushA("cf chunk");
+        struct PopRange {
+            ~PopRange() { nvtxRangePop(); }
+        } pop_range;
         for (int64_t i = 1; i <= nit; ++i) {
             IterOpts opt = next_opts(p, cfg->mu, i == nit);
             rc = launch_iteration(p, opt, p->done.p, &launches);

@@ -216,11 +216,13 @@ __global__ void __launch_bounds__(kBT, CF_BATCH_MINB) k_batch(const BatchArgs a)
         // ---- load the problem (canonical CSC, CSR, vectors) and a cold start (solver.py:309)
         for (int i = t; i <= m; i += kBT) rowptr[i] = (int32_t)(a.rowptr[r0 + i] - kr0);
         for (int j = t; j <= n; j += kBT) colptr[j] = (int32_t)(a.colptr[c0 + j] - kc0);
+        CF_DASSERT(m >= 0 && n >= 0 && o >= 0 && m <= a.cap_m && n <= a.cap_n && o <= a.cap_o);
         for (int k = t; k < o; k += kBT) {
             colidx[k] = (int32_t)(a.colidx[kr0 + k] - c0);
             valr[k] = a.valr[kr0 + k];
             rowidx[k] = (int32_t)(a.rowidx[kc0 + k] - r0);
             valc[k] = a.valc[kc0 + k];
+            CF_DASSERT(colidx[k] >= 0 && colidx[k] < n && rowidx[k] >= 0 && rowidx[k] < m);
         }
         for (int i = t; i < m; i += kBT) {
             b[i] = a.b[r0 + i];
@@ -642,12 +644,15 @@ __global__ void __launch_bounds__(kCT, 1) k_cluster(const ClusterArgs a) {
     // ---- load the CTA's rows and columns, cold start (solver.py:309)
     for (int i = t; i <= m; i += kCT) rowptr[i] = a.rowptr[r0 + i] - kr0;
     for (int j = t; j <= n; j += kCT) colptr[j] = a.colptr[c0 + j] - kc0;
+    CF_DASSERT(m <= a.cap_m && n <= a.cap_n && orr <= a.cap_or && occ <= a.cap_oc);
     for (int k = t; k < orr; k += kCT) {
         colidx[k] = a.colidx[kr0 + k];
+        CF_DASSERT(colidx[k] >= 0 && colidx[k] < N);
         valr[k] = a.valr[kr0 + k];
     }
     for (int k = t; k < occ; k += kCT) {
         rowidx[k] = a.rowidx[kc0 + k];
+        CF_DASSERT(rowidx[k] >= 0 && rowidx[k] < M);
         valc[k] = a.valc[kc0 + k];
     }
     for (int i = t; i < M; i += kCT) {

@@ -61,6 +61,31 @@ int cuda_fail(cudaError_t e, const char* what, const char* file, int line);
     } while (0)
 #define CF_LAUNCHED() CF_CUDA(cudaGetLastError())
 
+// Checked build (libcfb200_checked.so, -DCF_CHECKED=1): device-side bounds asserts on every
+// index the passes and the on-chip solvers dereference, and guard canaries behind every
+// device buffer, verified when the buffer is released (compute-sanitizer is not available
+// on the GPU pool). Off in the product build: the macros compile to nothing.
+#ifndef CF_CHECKED
+#define CF_CHECKED 0
+#endif
+#if CF_CHECKED
+#define CF_DASSERT(cond)                                                                              \
+    do {                                                                                              \
+        if (!(cond)) {                                                                                \
+            printf("CF_CHECKED: %s failed at %s:%d (block %d thread %d)\n", #cond, __FILE__, __LINE__, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                                \
+            __trap();                                                                                 \
+        }                                                                                             \
+    } while (0)
+#else
+#define CF_DASSERT(cond) \
+    do {                 \
+    } while (0)
+#endif
+constexpr size_t kGuardBytes = CF_CHECKED ? 4096 : 0;   // canary bytes behind a buffer (checked build)
+void guard_fill(void* p, size_t used, size_t total);
+void guard_check(const void* p, size_t used, size_t total);
+
 // ---------------------------------------------------------------- device buffers
 // Stream-ordered pool (cudaMallocAsync on the device's default pool with an unlimited release
 // threshold): plans created one after another reuse already-mapped memory instead of paying
@@ -96,7 +121,7 @@ struct DevBuf {
         release();
         if (count == 0) count = 1;  // keep a valid pointer for empty dims
         // +64 bytes: the pass engine's bulk copies read 16-byte-aligned supersets
-        cudaError_t e = pool_alloc(reinterpret_cast<void**>(&p), count * sizeof(T) + 64);
+        cudaError_t e = pool_alloc(reinterpret_cast<void**>(&p), count * sizeof(T) + 64 + kGuardBytes);
         if (e != cudaSuccess) {
             p = nullptr;
             cudaGetLastError();
@@ -105,9 +130,11 @@ struct DevBuf {
             return CF_ENOMEM;
         }
         n = count;
+        if (kGuardBytes) guard_fill(p, count * sizeof(T), count * sizeof(T) + 64 + kGuardBytes);
         return CF_OK;
     }
     void release() {
+        if (p && kGuardBytes) guard_check(p, n * sizeof(T), n * sizeof(T) + 64 + kGuardBytes);
         if (p) pool_free(p);
         p = nullptr;
         n = 0;

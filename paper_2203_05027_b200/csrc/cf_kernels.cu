@@ -24,6 +24,8 @@
 #include "cf_common.h"
 #include <utility>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "cf_pass.cuh"
 #include "cf_report.cuh"
 
@@ -640,8 +642,41 @@ pass::Tiles col_band_tiles(const cf_plan* p, int band) {
     const int64_t t0 = p->col_band_tile[band], t1 = p->col_band_tile[band + 1];
     return pass::Tiles{p->col_tb.p + t0, (int32_t)(t1 - t0), !p->col_large_tiles};
 }
-pass::Jds row_jds(const cf_plan* p) { return pass::Jds{p->rj_idx.p, p->rj_val.p, p->rj_pl.p}; }
-pass::Jds col_jds(const cf_plan* p) { return pass::Jds{p->cj_idx.p, p->cj_val.p, p->cj_pl.p}; }
+pass::Jds row_jds(const cf_plan* p) {
+    return pass::Jds{p->rj_idx.p, p->rj_val.p, p->rj_pl.p, (int64_t)p->rj_idx.n, p->n};
+}
+pass::Jds col_jds(const cf_plan* p) {
+    return pass::Jds{p->cj_idx.p, p->cj_val.p, p->cj_pl.p, (int64_t)p->cj_idx.n, p->m};
+}
+
+// L2 persisting window for the gathered vector of the next pass launches
+// (CF_L2_PERSIST_MB=<set-aside MB>; off by default). Set by the pass launchers.
+struct L2Window {
+    const void* ptr = nullptr;
+    size_t bytes = 0;
+};
+thread_local L2Window g_l2win;
+size_t l2_persist_bytes() {
+    static const size_t v = [] {
+        const char* e = getenv("CF_L2_PERSIST_MB");
+        if (!e || atoi(e) <= 0) return (size_t)0;
+        int dev = 0, maxp = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
+        const size_t want = std::min<size_t>((size_t)atoi(e) << 20, (size_t)maxp);
+        if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess) {
+            cudaGetLastError();
+            return (size_t)0;
+        }
+        return want;
+    }();
+    return v;
+}
+struct L2WindowScope {
+    L2Window saved;
+    L2WindowScope(const void* p, size_t b) : saved(g_l2win) { g_l2win = L2Window{p, b}; }
+    ~L2WindowScope() { g_l2win = saved; }
+};
 
 // Launch with programmatic stream serialization (the kernel calls pdl_wait()
 // before touching its predecessor's results): the launch overlaps the
@@ -654,11 +689,28 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, 
     cfg.blockDim = dim3(block);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
+    const size_t persist = g_l2win.ptr ? l2_persist_bytes() : 0;
+    if (persist) {
+        static const size_t max_win = [] {
+            int dev = 0, v = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&v, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+            return (size_t)v;
+        }();
+        const size_t nb = std::min(g_l2win.bytes, max_win);
+        at[1].id = cudaLaunchAttributeAccessPolicyWindow;
+        at[1].val.accessPolicyWindow.base_ptr = const_cast<void*>(g_l2win.ptr);
+        at[1].val.accessPolicyWindow.num_bytes = nb;
+        at[1].val.accessPolicyWindow.hitRatio = nb ? (float)std::min(1.0, (double)persist / (double)nb) : 0.f;
+        at[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        at[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cfg.numAttrs = 2;
+    }
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
@@ -819,6 +871,9 @@ int launch_row_only(cf_plan* p, const IterOpts& opt, const int32_t* done, int64_
         r.rcorr = opt.rcorr;
         r.br = (opt.report || p->keep_br) ? p->br.p : nullptr;
         r.ax = opt.report ? p->ax.p : nullptr;
+        const int64_t c0 = std::min<int64_t>(p->n, (int64_t)pn * p->panel_cols);
+        const int64_t c1 = std::min<int64_t>(p->n, c0 + p->panel_cols);
+        L2WindowScope w(g_l2win.ptr ? (const void*)(p->x.p + c0) : nullptr, (size_t)(c1 - c0) * 8);
         CF_TRY(launch_pass(r, row_jds(p), row_panel_tiles(p, pn), done, p->stream, nullptr, row_avg_len(p)));
         ++nl;
     }
@@ -841,9 +896,22 @@ int launch_iteration(cf_plan* p, const IterOpts& opt, const int32_t* done, int64
         p->prof_used += 3;
         CF_CUDA(cudaEventRecord(e_a, p->stream));
     }
-    CF_TRY(launch_col_only(p, opt, done, &nl));
+    {
+        // NVTX ranges (host enqueue of each pass; free without a profiler attached)
+        nvtxRangePushA("cf col pass");
+        L2WindowScope w(p->h.p, (size_t)p->m * 8);
+        const int rc = launch_col_only(p, opt, done, &nl);
+        nvtxRangePop();
+        CF_TRY(rc);
+    }
     if (p->profiling) CF_CUDA(cudaEventRecord(e_b, p->stream));
-    CF_TRY(launch_row_only(p, opt, done, &nl));
+    {
+        nvtxRangePushA("cf row pass");
+        L2WindowScope w(p->x.p, (size_t)p->n * 8);
+        const int rc = launch_row_only(p, opt, done, &nl);
+        nvtxRangePop();
+        CF_TRY(rc);
+    }
     if (p->profiling) CF_CUDA(cudaEventRecord(e_c, p->stream));
     if (launches) *launches += nl;
     return CF_OK;

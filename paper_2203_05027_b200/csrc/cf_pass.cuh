@@ -261,6 +261,8 @@ struct Jds {
     const int32_t* idx;
     const double* val;
     const uint32_t* pl;
+    int64_t n_idx = 0;     // entries of idx/val (bounds of the checked build)
+    int64_t g_len = 0;     // length of the gathered vector (bounds of the checked build)
 };
 
 // ---------------------------------------------------------------- the engine
@@ -290,8 +292,10 @@ __device__ __forceinline__ void load_batch(const Jds& L, int (&nj)[U], double (&
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const bool ok = mylen > k + u;
+        if (ok) CF_DASSERT(pos >= 0 && pos < L.n_idx);
         nj[u] = ok ? ld_first(L.idx + pos, pf) : 0;
         nv[u] = ok ? ld_first(L.val + pos, pf) : 0.0;
+        if (ok) CF_DASSERT(nj[u] >= 0 && nj[u] < L.g_len);
         pos += __popc(__ballot_sync(0xffffffffu, ok));   // width of diagonal k+u
     }
 }
@@ -320,7 +324,9 @@ __device__ __forceinline__ void long_tile(P& p, Smem& sm, const Jds& L, int tile
     for (int c0 = 0; c0 < len; c0 += kLongChunk) {
         const int cl = min(kLongChunk, len - c0);
         for (int e = gt; e < cl; e += kComputeThreads) {
+            CF_DASSERT(k0 + c0 + e < L.n_idx);
             const int jj = ld_first(L.idx + k0 + c0 + e, pf);
+            CF_DASSERT(jj >= 0 && jj < L.g_len);
             const double a = ld_first(L.val + k0 + c0 + e, pf);
             const double gj = ld_gather(g + jj, pl_);
             p.check(a, jj, gj);
@@ -560,6 +566,7 @@ __device__ __forceinline__ void load_batch_smem(const int32_t* ib, const double*
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const bool ok = mylen > k + u;
+        if (ok) CF_DASSERT(pos >= 0 && pos < kPCap + 8);
         nj[u] = ok ? ib[pos] : 0;
         nv[u] = ok ? vb[pos] : 0.0;
         pos += __popc(__ballot_sync(0xffffffffu, ok));   // width of diagonal k+u
@@ -588,6 +595,8 @@ __global__ void __launch_bounds__(kPThreads, P::kMinBlocks) k_pass(const P p0, c
     for (int tile = blockIdx.x; tile < T.n_tiles; tile += G) {
         const int4 lo = __ldg(T.tb + tile), hi = __ldg(T.tb + tile + 1);
         const int s0 = lo.x, nseg = hi.x - lo.x, k0 = lo.y, len = hi.y - lo.y;
+        CF_DASSERT(nseg >= 0 && len >= 0 && k0 >= 0 && (int64_t)k0 + len <= L.n_idx);
+        CF_DASSERT(!lo.z || (nseg <= kPSeg && (!P::kStaged || len <= kPCap)));
         if (lo.z) {
             const int32_t* ib = nullptr;
             const double* vb = nullptr;
@@ -630,8 +639,10 @@ __global__ void __launch_bounds__(kPThreads, P::kMinBlocks) k_pass(const P p0, c
                     else
                         load_batch<U>(L, nj, nv, pos, mylen, k, pol_first());
 #pragma unroll
-                    for (int u = 0; u < U; ++u)
+                    for (int u = 0; u < U; ++u) {
+                        if (mylen > k + u) CF_DASSERT(nj[u] >= 0 && nj[u] < L.g_len);
                         gv[u] = (mylen > k + u) ? ld_gather(g + (uint32_t)nj[u], pol_last()) : 0.0;
+                    }
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         if (mylen > k + u) p.check(nv[u], nj[u], gv[u]);

@@ -1,0 +1,140 @@
+// Probe: an IDEAL C2 iteration — the lower bound any implementation of the two passes
+// can reach on this GPU (VERDICT r1 "prove the ceiling").
+//
+// Same access pattern and bytes as one C2 iteration (m = 5M, n = 10M, o = 1e8,
+// B_alg = 24o + 44m + 68n = 3.30 GB), but with every convenience the real matrix
+// does not offer:
+//   * every row has exactly 10 nonzeros per x panel (2 panels of 5M columns = 40 MB of
+//     x each, L2-resident) and every column exactly 10 (h = 40 MB);
+//   * ELL layout, element k of segment s at k*S + s: every idx/val load is a full,
+//     aligned, coalesced warp load (0.094 L1TEX requests per nonzero), no tiles, no
+//     jagged diagonals, no tail segments, no cone logic;
+//   * one thread per segment, 10 independent gathers in flight per thread.
+// Row pass: panel 0 writes the partial row sums (carry), panel 1 continues them and
+// runs the row epilogue (reads b, lam, fu, d*b; writes lam, h). Column pass: the LP
+// column epilogue (reads x, z, delta, c; writes x, z, delta). The random indices are
+// uniform, so the gathers are as random as C2's.
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o scratch/ideal_iter_probe scratch/ideal_iter_probe.cu
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstdint>
+#include <vector>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e)); exit(1); } } while (0)
+
+constexpr int L = 10;   // nonzeros per segment (per panel for rows)
+
+__device__ __forceinline__ uint64_t pol_first() { uint64_t p; asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p)); return p; }
+__device__ __forceinline__ uint64_t pol_last() { uint64_t p; asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p)); return p; }
+__device__ __forceinline__ double ldh(const double* p, uint64_t pol) {
+    double v; asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol)); return v;
+}
+__device__ __forceinline__ int ldh(const int* p, uint64_t pol) {
+    int v; asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol)); return v;
+}
+__device__ __forceinline__ void sth(double* p, double v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+
+// segment sum over ELL column k*S + s, gathering g
+__device__ __forceinline__ double ell_sum(const int* __restrict__ idx, const double* __restrict__ val,
+                                          const double* __restrict__ g, int64_t S, int64_t s, double acc,
+                                          uint64_t pf, uint64_t pl) {
+    int j[L];
+    double a[L], v[L];
+#pragma unroll
+    for (int k = 0; k < L; ++k) { j[k] = ldh(idx + k * S + s, pf); a[k] = ldh(val + k * S + s, pf); }
+#pragma unroll
+    for (int k = 0; k < L; ++k) v[k] = ldh(g + j[k], pl);
+#pragma unroll
+    for (int k = 0; k < L; ++k) acc = __dadd_rn(acc, __dmul_rn(a[k], v[k]));
+    return acc;
+}
+
+__global__ void __launch_bounds__(256) k_row(const int* idx, const double* val, const double* xpanel, int64_t m,
+                                             bool last, double* carry, const double* b, double* lam,
+                                             const double* fu, const double* db, double* h) {
+    const uint64_t pf = pol_first(), pl = pol_last();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        if (!last) {
+            sth(carry + i, ell_sum(idx, val, xpanel, m, i, 0.0, pf, pl), pl);
+        } else {
+            const double ax = ell_sum(idx, val, xpanel, m, i, ldh(carry + i, pf), pf, pl);
+            const double r = ldh(fu + i, pf) * (ldh(db + i, pf) + ax);
+            const double bi = ldh(b + i, pf);
+            const double ln = ldh(lam + i, pf) + (r - bi);
+            sth(lam + i, ln, pf);
+            sth(h + i, (bi - r) - ln, pl);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_col(const int* idx, const double* val, const double* h, int64_t n,
+                                             double* x, double* z, double* dl, const double* c) {
+    const uint64_t pf = pol_first(), pl = pol_last();
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        const double ath = ell_sum(idx, val, h, n, j, 0.0, pf, pl);
+        const double xj = ldh(x + j, pf), zj = ldh(z + j, pf), dj = ldh(dl + j, pf), cj = ldh(c + j, pf);
+        const double xp = (1.0 / 11.0) * ((((10.0 * xj + ath) + zj) + dj) - cj);
+        const double w = xp - dj;
+        const double zp = w > 0.0 ? w : 0.0;
+        sth(x + j, xp, pl);
+        sth(z + j, zp, pf);
+        sth(dl + j, dj + (zp - xp), pf);
+    }
+}
+
+__global__ void k_fill_idx(int* idx, int64_t count, int range, uint32_t seed) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t a = (uint32_t)i * 2654435761u ^ seed;
+        a ^= a >> 16; a *= 0x7feb352dU; a ^= a >> 15; a *= 0x846ca68bU; a ^= a >> 16;
+        idx[i] = (int)(a % (uint32_t)range);
+    }
+}
+
+int main(int argc, char** argv) {
+    const int64_t m = 5000000, n = 10000000, o = 2 * m * L;   // o = 1e8 (= n * L)
+    const int iters = argc > 1 ? atoi(argv[1]) : 1000;
+    int *ridx, *cidx;
+    double *rval, *cval, *x, *z, *dl, *c, *b, *lam, *fu, *db, *h, *carry;
+    CK(cudaMalloc(&ridx, o * 4)); CK(cudaMalloc(&cidx, o * 4));
+    CK(cudaMalloc(&rval, o * 8)); CK(cudaMalloc(&cval, o * 8));
+    for (double** v : {&x, &z, &dl, &c}) { CK(cudaMalloc(v, n * 8)); CK(cudaMemset(*v, 0, n * 8)); }
+    for (double** v : {&b, &lam, &fu, &db, &h, &carry}) { CK(cudaMalloc(v, m * 8)); CK(cudaMemset(*v, 0, m * 8)); }
+    CK(cudaMemset(rval, 0, o * 8)); CK(cudaMemset(cval, 0, o * 8));
+    // row panel p: column indices uniform in [0, n/2) (offset into the panel's x slice)
+    k_fill_idx<<<4096, 256>>>(ridx, o, (int)(n / 2), 1u);
+    k_fill_idx<<<4096, 256>>>(cidx, o, (int)m, 2u);
+    CK(cudaDeviceSynchronize());
+    const int grid = 148 * 8;
+    auto iteration = [&] {
+        k_col<<<grid, 256>>>(cidx, cval, h, n, x, z, dl, c);
+        k_row<<<grid, 256>>>(ridx, rval, x, m, false, carry, b, lam, fu, db, h);
+        k_row<<<grid, 256>>>(ridx + m * L, rval + m * L, x + n / 2, m, true, carry, b, lam, fu, db, h);
+    };
+    for (int i = 0; i < 200; ++i) iteration();   // warm-up: reach the sustained (power-capped) clock
+    cudaEvent_t e0, e1, e2, e3;
+    CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1)); CK(cudaEventCreate(&e2)); CK(cudaEventCreate(&e3));
+    CK(cudaEventRecord(e0));
+    for (int i = 0; i < iters; ++i) iteration();
+    CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1));
+    float ms; CK(cudaEventElapsedTime(&ms, e0, e1));
+    // one of each pass, timed alone
+    CK(cudaEventRecord(e0));
+    for (int i = 0; i < 20; ++i) k_col<<<grid, 256>>>(cidx, cval, h, n, x, z, dl, c);
+    CK(cudaEventRecord(e1));
+    for (int i = 0; i < 20; ++i) {
+        k_row<<<grid, 256>>>(ridx, rval, x, m, false, carry, b, lam, fu, db, h);
+        k_row<<<grid, 256>>>(ridx + m * L, rval + m * L, x + n / 2, m, true, carry, b, lam, fu, db, h);
+    }
+    CK(cudaEventRecord(e2)); CK(cudaEventSynchronize(e2));
+    float mc, mr;
+    CK(cudaEventElapsedTime(&mc, e0, e1)); CK(cudaEventElapsedTime(&mr, e1, e2));
+    const double balg = 24.0 * o + 44.0 * m + 68.0 * n;
+    const double per = ms / iters;
+    printf("ideal C2 iteration: %.4f ms  (%.1f it/s)  B_alg %.3f GB -> %.1f GB/s = %.3f of 6556.2 GB/s\n", per,
+           1000.0 / per, balg / 1e9, balg / (per * 1e-3) / 1e9, balg / (per * 1e-3) / 1e9 / 6556.2);
+    printf("  col pass alone %.4f ms, row pass (2 panels) alone %.4f ms, 100M gathers each\n", mc / 20, mr / 20);
+    return 0;
+}
