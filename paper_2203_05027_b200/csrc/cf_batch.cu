@@ -874,6 +874,15 @@ void balanced_cuts(const std::vector<int32_t>& ptr, const std::vector<int32_t>& 
 }  // namespace
 }  // namespace cf
 
+namespace {
+// cf_cluster_solve declines (cluster_used = 0, CF_OK) and the caller builds a plan;
+// CF_VERBOSE=1 says why
+int decline(const char* why) {
+    if (getenv("CF_VERBOSE")) fprintf(stderr, "cf_cluster_solve: declined: %s\n", why);
+    return CF_OK;
+}
+}  // namespace
+
 extern "C" int cf_cluster_solve(int64_t m, int64_t n, int64_t o, const int64_t* rows, const int64_t* cols,
                                 const double* vals, const double* b, const double* c, int64_t n_blocks,
                                 const int64_t* block_sizes, const cf_config* cfg, double* x_out, double* lam_out,
@@ -971,8 +980,8 @@ extern "C" int cf_cluster_solve(int64_t m, int64_t n, int64_t o, const int64_t* 
         // ~2,800 nonzeros and 1,024 rows or columns per CTA, and at least 4 CTAs once o >= 2,000.
         if (cor <= 2800 && coc <= 2800 && cm <= 1024 && cn <= 1024 && (cand >= 4 || o < 2000)) break;
     }
-    if (C == 0) return CF_OK;   // does not fit a cluster: the caller uses cf_plan_solve
-    if (trace_cap > kMaxClusterTrace) return CF_OK;   // huge max_iters: the plan path streams its trace
+    if (C == 0) return decline("no cluster size fits the shared memory");   // the caller uses cf_plan_solve
+    if (trace_cap > kMaxClusterTrace) return decline("trace too long");   // the plan path streams its trace
     cf_plan* plan = nullptr;
     int rc = cf_plan_create_mode(m, n, o, rows, cols, vals, b, c, n_blocks, block_sizes, 0, nullptr, checks,
                                  /*batch_mode=*/1, &plan);
@@ -995,7 +1004,7 @@ extern "C" int cf_cluster_solve(int64_t m, int64_t n, int64_t o, const int64_t* 
         if (attr_err == cudaSuccess)
             attr_err = cudaFuncSetAttribute(k_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     });
-    if (attr_err != cudaSuccess) return CF_OK;   // cannot configure the kernel here: plan path
+    if (attr_err != cudaSuccess) return decline(cudaGetErrorString(attr_err));   // cannot configure the kernel
     DevBuf<double> d_x, d_lam;
     DevBuf<cf_report> d_final, d_trace;
     DevBuf<int32_t> d_nrep;
@@ -1003,7 +1012,7 @@ extern "C" int cf_cluster_solve(int64_t m, int64_t n, int64_t o, const int64_t* 
     if (d_x.alloc(n) != CF_OK || d_lam.alloc(m) != CF_OK || d_final.alloc(1) != CF_OK ||
         d_trace.alloc(std::max<int64_t>(1, trace_cap)) != CF_OK || d_nrep.alloc(1) != CF_OK) {
         (void)cudaGetLastError();
-        return CF_OK;
+        return decline("out of device memory");
     }
     a.M = (int32_t)m;
     a.N = (int32_t)n;
@@ -1041,9 +1050,12 @@ extern "C" int cf_cluster_solve(int64_t m, int64_t n, int64_t o, const int64_t* 
     // a cluster of C CTAs with this much shared memory may not be schedulable (MPS, an
     // SM-limited context, a busy GPU): treat that like "does not fit"
     int active = 0;
-    if (cudaOccupancyMaxActiveClusters(&active, k_cluster, &lc) != cudaSuccess || active < 1) {
-        (void)cudaGetLastError();
-        return CF_OK;
+    {
+        const cudaError_t oe = cudaOccupancyMaxActiveClusters(&active, k_cluster, &lc);
+        if (oe != cudaSuccess || active < 1) {
+            (void)cudaGetLastError();
+            return decline(oe != cudaSuccess ? cudaGetErrorString(oe) : "no active cluster of this size fits");
+        }
     }
     CF_CUDA(cudaEventRecord(plan->ev0, st));
     {
@@ -1051,7 +1063,7 @@ extern "C" int cf_cluster_solve(int64_t m, int64_t n, int64_t o, const int64_t* 
         if (le == cudaErrorLaunchOutOfResources ||
             le == cudaErrorMemoryAllocation || le == cudaErrorInvalidClusterSize) {
             (void)cudaGetLastError();
-            return CF_OK;
+            return decline(cudaGetErrorString(le));
         }
         CF_CUDA(le);
     }

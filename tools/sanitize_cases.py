@@ -58,8 +58,8 @@ def main(case):
         from paper_2203_05027_b200 import api
 
         p = generate(GenSpec(300, 600, 0.03, "lp", seed=4))
-        res = solve(p, cfg)
-        assert api._LAST_CLUSTER == int(case[len("cluster"):]), api._LAST_CLUSTER
+        res = api._solve_cluster(p, cfg)   # direct: solve() skips the cluster path when CF_LIB_PATH is set
+        assert res is not None and api._LAST_CLUSTER == int(case[len("cluster"):]), api._LAST_CLUSTER
         _check(p, res, cfg)
     elif case == "batch":
         probs = [generate(GenSpec(30, 60, 0.1, "lp", seed=s)) for s in range(64)]
