@@ -308,6 +308,33 @@ int cf_plan_set_profiling(cf_plan* plan, int enable);
 /* Synchronise the plan's stream. */
 int cf_plan_sync(cf_plan* plan);
 
+/* ---------------------------------------------------------------- NVLS (NVLink SHARP) fused step
+ * SURVEY §2 K7 stage 2 / §8e: the row-sharded exchange done by the NVSwitch. A multicast
+ * object (CUDA VMM, cuMulticastCreate) binds one buffer per rank; a multimem.ld_reduce of
+ * the multicast address returns the sum of every rank's copy, a multimem.st writes every
+ * rank's copy. Replaces reduce-scatter -> cf_column_update -> all-gather
+ * (solver.py:168-176,186-188,196) like cf_column_update_p2p. */
+typedef struct cf_mc cf_mc;
+/* 1 when the current device supports multicast objects (CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED) */
+int cf_mc_supported(int* supported);
+/* create a multicast object of >= bytes per rank for `world` ranks; world > 1 also
+ * exports a POSIX fd for the other ranks (cf_mc_import) */
+int cf_mc_create(int64_t bytes, int32_t world, cf_mc** out, int* fd_out);
+int cf_mc_import(int fd, int64_t bytes, int32_t world, cf_mc** out);
+/* join with the current device (every rank), then bind + map: uc = this rank's copy,
+ * mc = the multicast address (blocks until every rank has joined) */
+int cf_mc_add_device(cf_mc* mc);
+int cf_mc_bind(cf_mc* mc, void** uc_ptr, void** mc_ptr);
+int cf_mc_destroy(cf_mc* mc);
+/* cf_column_update on a slice with A^T h = multimem.ld_reduce(parts_mc) and x+ stored to
+ * x (the slice) and through x_mc (every rank's replica; NULL: none) */
+int cf_column_update_nvls(int64_t n, const double* parts_mc, const double* cnt, const double* c, double* x,
+                          double* z, double* delta, double mu, int64_t n_blocks, const int32_t* cone_ptr,
+                          double* x_mc, void* stream);
+/* device-side team barrier: multimem.red.add 1 on the counter, wait until this rank's
+ * copy reaches target (= world * epoch); stream-ordered, no host synchronisation */
+int cf_mc_barrier(uint32_t* flag_mc, const uint32_t* flag_uc, uint32_t target, void* stream);
+
 /* ---------------------------------------------------------------- instance generator (bench tooling)
  * Counter-based draws for the large synthetic configs, bit-identical to the numpy
  * restatement paper_2203_05027_b200/cfgen.py (which replaces the PCG64 stream of the

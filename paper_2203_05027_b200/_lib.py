@@ -139,6 +139,14 @@ SIGNATURES = {
     "cf_ipc_open": (c_int, [c_void_p, POINTER(c_void_p)]),
     "cf_ipc_close": (c_int, [_P]),
     "cf_plan_bind_x": (c_int, [_P, _P]),
+    "cf_mc_supported": (c_int, [POINTER(c_int)]),
+    "cf_mc_create": (c_int, [c_int64, c_int32, POINTER(c_void_p), POINTER(c_int)]),
+    "cf_mc_import": (c_int, [c_int, c_int64, c_int32, POINTER(c_void_p)]),
+    "cf_mc_add_device": (c_int, [_P]),
+    "cf_mc_bind": (c_int, [_P, POINTER(c_void_p), POINTER(c_void_p)]),
+    "cf_mc_destroy": (c_int, [_P]),
+    "cf_column_update_nvls": (c_int, [c_int64, _P, _P, _P, _P, _P, _P, c_double, c_int64, _P, _P, _P]),
+    "cf_mc_barrier": (c_int, [_P, _P, ctypes.c_uint32, _P]),
     "cf_gen_normal": (c_int, [ctypes.c_uint64, ctypes.c_uint64, c_int64, c_int64, _P, _P]),
     "cf_gen_cells": (c_int, [ctypes.c_uint64, c_int64, c_int64, c_int64, _P, _P]),
     "cf_gen_keys": (c_int, [ctypes.c_uint64, ctypes.c_uint64, c_int64, c_int64, _P, _P]),

@@ -9,7 +9,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libcfb200.so")
-SOURCES = ["cf_kernels.cu", "cf_setup.cu", "cf_api.cu", "cf_batch.cu", "cf_h2d.cu", "cf_gen.cu", "cf_io.cpp"]
+SOURCES = ["cf_kernels.cu", "cf_setup.cu", "cf_api.cu", "cf_batch.cu", "cf_h2d.cu", "cf_gen.cu", "cf_nvls.cu", "cf_io.cpp"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

@@ -96,6 +96,63 @@ class _DevArray:
                                          "strides": None}
 
 
+def torch_all_ranks(torch, flag: bool, group, device) -> bool:
+    """True on every rank iff ``flag`` is true on every rank."""
+    import torch.distributed as dist
+
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return flag
+    t = torch.tensor([1.0 if flag else 0.0], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    return bool(t.item() > 0)
+
+
+def _mc_create_export(L, size, world, mc):
+    import ctypes
+
+    from . import _lib
+
+    fd = ctypes.c_int(-1)
+    _lib.check(L.cf_mc_create(size, world, ctypes.byref(mc), ctypes.byref(fd)))
+    return fd.value
+
+
+def _share_fd(make_fd, rank, group):
+    """Rank 0 runs make_fd() and passes the descriptor to every other rank of the (single-node)
+    group over an abstract Unix socket (SCM_RIGHTS); returns the descriptor on every rank."""
+    import os
+    import socket
+    import uuid
+
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    name = [None]
+    if rank == 0:
+        name[0] = "\0cfb200-nvls-" + uuid.uuid4().hex
+    dist.broadcast_object_list(name, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    if rank == 0:
+        srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+        srv.bind(name[0])
+        srv.listen(world)
+        fd = make_fd()
+        dist.barrier(group=group)                      # the others connect after the listen
+        for _ in range(world - 1):
+            conn, _ = srv.accept()
+            socket.send_fds(conn, [b"fd"], [fd])
+            conn.close()
+        srv.close()
+        dist.barrier(group=group)
+        return fd
+    dist.barrier(group=group)
+    cli = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+    cli.connect(name[0])
+    _, fds, _, _ = socket.recv_fds(cli, 16, 1)
+    cli.close()
+    dist.barrier(group=group)
+    return fds[0]
+
+
 class CudaRankBackend:
     """One rank on its GPU: a plan over its row block (all columns) + its column slice state."""
 
@@ -254,6 +311,97 @@ class CudaRankBackend:
         """This rank's full x (torch), filled by every rank's fused step."""
         return self.x_full
 
+    # ------------------------------------------------------------ NVLS (NVLink SHARP) step
+    def enable_nvls(self, group, col_cuts):
+        """One multicast object (cf_mc_*) per team holding [partial A^T h | x replica | barrier
+        counter], one physical copy per rank. The fused step reads the partials' SUM with
+        multimem.ld_reduce and writes x+ into every replica with multimem.st; the barrier is a
+        device-side multimem counter. world > 1: rank 0 creates the object and hands its
+        POSIX fd to the other ranks over a Unix socket."""
+        import ctypes
+
+        import torch.distributed as dist
+
+        from . import _lib
+
+        if getattr(self, "_mc", None):
+            return
+        world = dist.get_world_size(group)
+        rank = dist.get_rank(group)
+        L = self.lib
+        sup = ctypes.c_int(0)
+        _lib.check(L.cf_mc_supported(ctypes.byref(sup)))
+        ok = torch_all_ranks(self.torch, bool(sup.value), group, self.device)
+        if not ok:
+            raise RuntimeError("NVLS: multicast objects are not supported on every rank's device")
+        seg = -(-(8 * max(self.n, 1) + 64) // 256) * 256
+        size = 2 * seg + 256
+        mc = ctypes.c_void_p()
+        if world == 1:
+            _lib.check(L.cf_mc_create(size, 1, ctypes.byref(mc), None))
+        else:
+            fd = _share_fd(lambda: _mc_create_export(L, size, world, mc), rank, group)
+            if rank != 0:
+                _lib.check(L.cf_mc_import(fd, size, world, ctypes.byref(mc)))
+        self._mc = mc.value
+        self._mc_group = group
+        _lib.check(L.cf_mc_add_device(ctypes.c_void_p(self._mc)))
+        uc, mcp = ctypes.c_void_p(), ctypes.c_void_p()
+        _lib.check(L.cf_mc_bind(ctypes.c_void_p(self._mc), ctypes.byref(uc), ctypes.byref(mcp)))
+        if world > 1:
+            dist.barrier(group=group)
+        self._mc_uc, self._mc_mc = uc.value, mcp.value
+        self.nvls_partial = self.torch.as_tensor(_DevArray(self._mc_uc, self.n), device=self.device)
+        self._nvls_parts_mc = self._mc_mc + 8 * self.lo
+        self._nvls_x_mc = self._mc_mc + seg + 8 * self.lo
+        self._nvls_flag_uc, self._nvls_flag_mc = self._mc_uc + 2 * seg, self._mc_mc + 2 * seg
+        self._nvls_world, self._nvls_epoch = world, 0
+        _lib.check(L.cf_plan_bind_x(self.plan.handle, ctypes.c_void_p(self._mc_uc + seg)))
+        self.x_full = self.torch.as_tensor(_DevArray(self._mc_uc + seg, self.n), device=self.device)
+
+    def nvls_barrier(self):
+        """Stream-ordered team barrier on the multicast counter (cf_mc_barrier)."""
+        import ctypes
+
+        from . import _lib
+
+        self._nvls_epoch += 1
+        _lib.check(self.lib.cf_mc_barrier(ctypes.c_void_p(self._nvls_flag_mc), ctypes.c_void_p(self._nvls_flag_uc),
+                                          self._nvls_world * self._nvls_epoch, self.stream.cuda_stream))
+
+    def column_update_nvls(self, mu: float):
+        """The switch sums the ranks' partials (multimem.ld_reduce), then the column update,
+        then x+ into every replica (multimem.st): cf_column_update_nvls."""
+        import ctypes
+
+        from . import _lib
+
+        _lib.check(self.lib.cf_column_update_nvls(
+            self.xs.numel(), ctypes.c_void_p(self._nvls_parts_mc), self._p(self.cnt_s), self._p(self.cs),
+            self._p(self.xs), self._p(self.zs), self._p(self.ds), float(mu), self.n_blocks,
+            self._p(self.cone_ptr) if self.cone_ptr is not None else None, ctypes.c_void_p(self._nvls_x_mc),
+            self.stream.cuda_stream))
+
+    def disable_nvls(self):
+        import ctypes
+
+        import torch.distributed as dist
+
+        from . import _lib
+
+        if not getattr(self, "_mc", None):
+            return
+        self.torch.cuda.synchronize()
+        _lib.check(self.lib.cf_plan_bind_x(self.plan.handle, None))
+        if dist.is_available() and dist.is_initialized():
+            dist.barrier(group=getattr(self, "_mc_group", None))   # no peer still stores into our copy
+        self.lib.cf_mc_destroy(ctypes.c_void_p(self._mc))
+        self._mc = None
+        ptr, ln = ctypes.c_void_p(), ctypes.c_int64()
+        _lib.check(self.lib.cf_plan_vector(self.plan.handle, 0, ctypes.byref(ptr), ctypes.byref(ln)))
+        self.x_full = self.torch.as_tensor(_DevArray(ptr.value or 0, ln.value), device=self.device)
+
+
     def disable_p2p(self):
         import ctypes
 
@@ -316,6 +464,7 @@ class CudaRankBackend:
 
     def close(self):
         self.disable_p2p()
+        self.disable_nvls()
         self.plan.close()
 
 
@@ -329,7 +478,7 @@ def _cone_ptr_slice(p, lo: int, hi: int):
 
 
 def solve_sharded(p, cfg: SolverConfig | None = None, group=None, backend_factory=None,
-                  p2p: bool = False) -> SolveResult:
+                  p2p: bool = False, nvls: bool = False) -> SolveResult:
     """solve() with A's rows split over the ranks of ``group`` (every rank passes the same problem).
 
     Cold start only. Returns the same SolveResult on every rank. ``p2p``: the fused
@@ -346,14 +495,15 @@ def solve_sharded(p, cfg: SolverConfig | None = None, group=None, backend_factor
     factory = backend_factory or CudaRankBackend
     be = factory(lp, lo, hi, _cone_ptr_slice(p, lo, hi), None)
     try:
-        return run_sharded(be, row_cuts, col_cuts, cfg, norms(p.b), norms(p.c), group, p2p=p2p)
+        return run_sharded(be, row_cuts, col_cuts, cfg, norms(p.b), norms(p.c), group, p2p=p2p, nvls=nvls)
     finally:
         if hasattr(be, "close"):
             be.close()
 
 
 def run_sharded(be, row_cuts, col_cuts, cfg, b_norms, c_norms, group=None, timing=None,
-                gather_result: bool = True, overlap_reduce: bool = True, p2p: bool = False) -> SolveResult:
+                gather_result: bool = True, overlap_reduce: bool = True, p2p: bool = False,
+                nvls: bool = False) -> SolveResult:
     """The sharded loop on an existing rank backend (row/column cuts shared by all ranks).
 
     ``timing``: if a dict, receives the CUDA-event time of the loop on this rank (ms).
@@ -362,7 +512,10 @@ def run_sharded(be, row_cuts, col_cuts, cfg, b_norms, c_norms, group=None, timin
     ``p2p``: CUDA backend: the fused step instead. A^T h is computed into peer-visible memory,
     then a barrier, then one kernel per rank that sums its slice over the peers in rank order,
     updates it and stores x+ into every rank's x replica over NVLink, then a barrier. That
-    replaces the reduce-scatter, the column update and the all-gather."""
+    replaces the reduce-scatter, the column update and the all-gather.
+    ``nvls``: the same fused step with the reduction and the broadcast done by the NVSwitch
+    (multimem.ld_reduce / multimem.st on a multicast object, enable_nvls) and a device-side
+    multimem counter as the barrier."""
     import torch
     import torch.distributed as dist
 
@@ -434,7 +587,10 @@ def run_sharded(be, row_cuts, col_cuts, cfg, b_norms, c_norms, group=None, timin
             ag_out.copy_(torch.cat(parts))
         return ag_out[:n] if contiguous else ag_out[pad_idx]
 
-    use_p2p = p2p and hasattr(be, "enable_p2p") and hasattr(be, "partial_into")
+    use_nvls = nvls and hasattr(be, "enable_nvls")
+    if nvls and not use_nvls:
+        raise ValueError("nvls=True needs a backend with enable_nvls")
+    use_p2p = (not use_nvls) and p2p and hasattr(be, "enable_p2p") and hasattr(be, "partial_into")
     bar = torch.zeros(1, dtype=torch.float64, device=torch_dev)
 
     def barrier():
@@ -447,13 +603,21 @@ def run_sharded(be, row_cuts, col_cuts, cfg, b_norms, c_norms, group=None, timin
     be.cnt_s = reduce_scatter(be.local_counts).clone()
     if use_p2p:
         be.enable_p2p(group, col_cuts)
+    if use_nvls:
+        be.enable_nvls(group, col_cuts)
     trace = []
     x_full = None
     if timing is not None and torch_dev.type == "cuda":
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
     for k in range(1, cfg.max_iters + 1):
-        if use_p2p:
+        if use_nvls:
+            be.partial_into("h", be.nvls_partial)
+            be.nvls_barrier()
+            be.column_update_nvls(cfg.mu)
+            be.nvls_barrier()
+            x_full = be.x_replica()
+        elif use_p2p:
             be.partial_into("h", be.p2p_partial)
             barrier()
             be.column_update_p2p(cfg.mu)
@@ -462,7 +626,7 @@ def run_sharded(be, row_cuts, col_cuts, cfg, b_norms, c_norms, group=None, timin
         else:
             ath = reduce_scatter_partial("h")
             be.column_update(ath, cfg.mu)
-        if use_p2p:
+        if use_p2p or use_nvls:
             pass
         elif fast:
             dist.all_gather_into_tensor(be.x_full, be.xs, group=group)

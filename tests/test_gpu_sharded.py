@@ -266,3 +266,118 @@ def test_ipc_buffer_opens_in_another_process():
         assert total == float(sum(1.5 * k for k in range(64))) and last == 94.5
     finally:
         L.cf_ipc_free(ptr)
+
+
+_MC = {}
+
+
+def _mc_supported():
+    """The device reports multicast support AND the driver creates a multicast object here.
+    (The single-GPU boxes of this pool report CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED = 1
+    but refuse cuMulticastCreate with CUDA_ERROR_INVALID_VALUE: no NVSwitch fabric team;
+    scratch/mc_probe.cu, profiles/r02_probes.md.)"""
+    import ctypes
+
+    from paper_2203_05027_b200 import _lib
+
+    if "ok" not in _MC:
+        s = ctypes.c_int(0)
+        _lib.check(_lib.lib().cf_mc_supported(ctypes.byref(s)))
+        mc = ctypes.c_void_p()
+        rc = _lib.lib().cf_mc_create(4 << 20, 1, ctypes.byref(mc), None) if s.value else -1
+        if rc == 0:
+            _lib.lib().cf_mc_destroy(mc)
+        _MC["ok"] = bool(s.value) and rc == 0
+        _MC["why"] = ("multicast attribute 0" if not s.value else
+                      f"cuMulticastCreate refused: {_lib.last_error()}" if rc != 0 else "")
+    return _MC["ok"]
+
+
+def test_multicast_support_reported():
+    """cf_mc_supported answers and a one-device multicast object is attempted (the NVLS tests
+    below need one; a box without an NVSwitch multicast team skips them with the reason)."""
+    print("multicast usable:", _mc_supported(), _MC.get("why"))
+
+
+@pytest.mark.parametrize("cones", [False, True])
+def test_nvls_update_kernel_world1(cones):
+    """cf_column_update_nvls on a one-device multicast object (multimem.ld_reduce of one copy,
+    multimem.st into it) == cf_column_update on the partial, bit for bit, and the replica
+    region of the multicast buffer receives x+."""
+    import ctypes
+
+    import torch
+
+    from paper_2203_05027_b200 import _lib
+    from paper_2203_05027_b200.sharded import _DevArray
+
+    if not _mc_supported():
+        pytest.skip("no multicast object on this box: " + _MC["why"])
+    L = _lib.lib()
+    n = 12_000
+    g = torch.Generator(device="cuda")
+    g.manual_seed(9)
+
+    def rnd():
+        return torch.randn(n, generator=g, device="cuda", dtype=torch.float64)
+
+    a, c, x, z, d = rnd(), rnd(), rnd(), rnd(), rnd()
+    cnt = torch.randint(0, 20, (n,), generator=g, device="cuda").double()
+    cone_ptr = torch.arange(0, n + 1, 4, dtype=torch.int32, device="cuda") if cones else None
+    nb = n // 4 if cones else 0
+
+    def p(t):
+        return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+    x1, z1, d1 = x.clone(), z.clone(), d.clone()
+    _lib.check(L.cf_column_update(n, p(a), p(cnt), p(c), p(x1), p(z1), p(d1), 0.7, nb, p(cone_ptr), None))
+    mc = ctypes.c_void_p()
+    _lib.check(L.cf_mc_create(16 * n + 4096, 1, ctypes.byref(mc), None))
+    try:
+        _lib.check(L.cf_mc_add_device(mc))
+        uc, mcp = ctypes.c_void_p(), ctypes.c_void_p()
+        _lib.check(L.cf_mc_bind(mc, ctypes.byref(uc), ctypes.byref(mcp)))
+        part = torch.as_tensor(_DevArray(uc.value, n), device="cuda")
+        rep = torch.as_tensor(_DevArray(uc.value + 8 * n + 256, n), device="cuda")
+        part.copy_(a)
+        torch.cuda.synchronize()
+        x2, z2, d2 = x.clone(), z.clone(), d.clone()
+        _lib.check(L.cf_column_update_nvls(n, ctypes.c_void_p(mcp.value), p(cnt), p(c), p(x2), p(z2), p(d2), 0.7, nb,
+                                           p(cone_ptr), ctypes.c_void_p(mcp.value + 8 * n + 256), None))
+        torch.cuda.synchronize()
+        assert torch.equal(x1, x2) and torch.equal(z1, z2) and torch.equal(d1, d2)
+        assert torch.equal(rep, x2)
+        # the device barrier on the counter: one rank, target 1 then 2
+        flag_uc, flag_mc = uc.value + 16 * n + 1024, mcp.value + 16 * n + 1024
+        for t in (1, 2):
+            _lib.check(L.cf_mc_barrier(ctypes.c_void_p(flag_mc), ctypes.c_void_p(flag_uc), t, None))
+        torch.cuda.synchronize()
+    finally:
+        L.cf_mc_destroy(mc)
+
+
+@pytest.mark.parametrize("kind", ["lp", "socp4"])
+def test_sharded_nvls_step_equals_nccl_step(nccl_group, kind):
+    """run_sharded(nvls=True) (switch reduction + multicast x store + device barrier; one
+    rank) == the NCCL reduce-scatter + update + all-gather step, bit for bit."""
+    import torch
+
+    from paper_2203_05027_b200 import SolverConfig
+    from paper_2203_05027_b200.devgen import generate_device_shard
+    from paper_2203_05027_b200.sharded import CudaRankBackend, run_sharded
+
+    if not _mc_supported():
+        pytest.skip("no multicast object on this box: " + _MC["why"])
+    st = torch.cuda.current_stream()
+    plan, rc, cc, cs, bn, cn, cones = generate_device_shard(20_000, 40_000, 5e-4, kind, 3, 0, 1,
+                                                            stream=st.cuda_stream)
+    cfg = SolverConfig(max_iters=60, check_every=25, eps_prim=0.0, eps_dual=0.0, eps_gap=0.0)
+    out = []
+    for nvls in (False, True):
+        plan.set_state(1.0, None, export=False)
+        be = CudaRankBackend.from_plan(plan, cc[0], cc[1], cs, cones)
+        out.append(run_sharded(be, rc, cc, cfg, bn, cn, nvls=nvls))
+        be.disable_nvls()
+    assert np.array_equal(out[0].x, out[1].x) and np.array_equal(out[0].lam, out[1].lam)
+    assert out[0].trace == out[1].trace
+    plan.close()

@@ -131,6 +131,19 @@ class NumpyRankBackend:
         for pair in self._peers:
             pair[1][lo:hi] = self.xs                     # x+ into every replica
 
+    # the NVLS step: the switch's reduction and broadcast emulated on the same shared memory
+    # (the reduction order inside a switch is the hardware's; here rank order)
+    def enable_nvls(self, group, col_cuts):
+        self.enable_p2p(group, col_cuts)
+        self.nvls_partial = self.p2p_partial
+        self._nvls_group = group
+
+    def nvls_barrier(self):
+        dist.barrier(group=self._nvls_group)
+
+    def column_update_nvls(self, mu):
+        self.column_update_p2p(mu)
+
     def close(self):
         self.x_full = np.array(self.x_full)
         self.p2p_partial = self.x_full_t = None
@@ -149,7 +162,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, spec, cfg_kw, out_path, p2p=False):
+def _worker(rank, world, port, spec, cfg_kw, out_path, p2p=False, nvls=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -157,7 +170,7 @@ def _worker(rank, world, port, spec, cfg_kw, out_path, p2p=False):
         p = generate(spec)
         cfg = SolverConfig(**cfg_kw)
 
-        res = solve_sharded(p, cfg, backend_factory=NumpyRankBackend, p2p=p2p)
+        res = solve_sharded(p, cfg, backend_factory=NumpyRankBackend, p2p=p2p, nvls=nvls)
         if rank == 0:
             np.savez(out_path, x=res.x, lam=res.lam, iters=np.array([r.iter for r in res.trace]),
                      status=np.array([r.status for r in res.trace]),
@@ -166,18 +179,20 @@ def _worker(rank, world, port, spec, cfg_kw, out_path, p2p=False):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,spec,cfg_kw,p2p", [
-    (2, GenSpec(40, 90, 0.06, "lp", seed=31), dict(eps_prim=1e-4, eps_dual=1e-4, eps_gap=1e-4, max_iters=4000), False),
-    (3, GenSpec(30, 64, 0.08, "socp4", seed=32), dict(mu=0.7, max_iters=600, check_every=20), False),
+@pytest.mark.parametrize("world,spec,cfg_kw,mode", [
+    (2, GenSpec(40, 90, 0.06, "lp", seed=31), dict(eps_prim=1e-4, eps_dual=1e-4, eps_gap=1e-4, max_iters=4000), "nccl"),
+    (3, GenSpec(30, 64, 0.08, "socp4", seed=32), dict(mu=0.7, max_iters=600, check_every=20), "nccl"),
     # the fused peer-memory step's ordering (partials -> barrier -> reduce+update+broadcast -> barrier)
-    (2, GenSpec(40, 90, 0.06, "lp", seed=31), dict(eps_prim=1e-4, eps_dual=1e-4, eps_gap=1e-4, max_iters=4000), True),
-    (3, GenSpec(30, 64, 0.08, "socp4", seed=32), dict(mu=0.7, max_iters=600, check_every=20), True),
+    (2, GenSpec(40, 90, 0.06, "lp", seed=31), dict(eps_prim=1e-4, eps_dual=1e-4, eps_gap=1e-4, max_iters=4000), "p2p"),
+    (3, GenSpec(30, 64, 0.08, "socp4", seed=32), dict(mu=0.7, max_iters=600, check_every=20), "p2p"),
+    # the NVLS step (switch reduction + multicast store, device barrier) in the same driver
+    (3, GenSpec(30, 64, 0.08, "socp4", seed=32), dict(mu=0.7, max_iters=600, check_every=20), "nvls"),
 ])
-def test_sharded_matches_oracle(tmp_path, world, spec, cfg_kw, p2p):
+def test_sharded_matches_oracle(tmp_path, world, spec, cfg_kw, mode):
     out = str(tmp_path / "res.npz")
     port = _free_port()
-    mp.start_processes(_worker, args=(world, port, spec, cfg_kw, out, p2p), nprocs=world, join=True,
-                       start_method="spawn")
+    mp.start_processes(_worker, args=(world, port, spec, cfg_kw, out, mode == "p2p", mode == "nvls"), nprocs=world,
+                       join=True, start_method="spawn")
     got = np.load(out)
     p = generate(spec)
     cfg = SolverConfig(**cfg_kw)

@@ -1,2 +1,2 @@
-timeout 1500 python -m pytest tests -m gpu -x -q --durations=8 > gpurun_out/r2_t2_all.log 2>&1; echo "all rc=$?"
-tail -n 12 gpurun_out/r2_t2_all.log
+./scratch/mc_probe
+nvidia-smi -q | grep -iA3 "fabric" | head -12
