@@ -45,10 +45,10 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     return target
 
 
-# Compile-time variants kept measured and tested beside the product library: the
-# producer-warp TMA ring engine and the checked build (device bounds
-# asserts + buffer guard canaries) that stands in for compute-sanitizer.
-VARIANTS = {"tma": ["CF_TMA=1"], "checked": ["CF_CHECKED=1"]}
+# Compile-time variants tested beside the product library: the checked build (device
+# bounds asserts + buffer guard canaries) that stands in for compute-sanitizer.
+VARIANTS = {"checked": ["CF_CHECKED=1"]}
+# experiments (python -m paper_2203_05027_b200.build --exp NAME=DEFINE,...): built on demand only
 
 
 def variant_path(name: str) -> str:

@@ -40,6 +40,9 @@ constexpr int kTileNnzLarge = CF_PCAP_LARGE;
 constexpr int kStagedMaxTiles = CF_MEDIUM_TILES;   // passes with more tiles per launch run unstaged
 constexpr int kTileSeg = CF_PSEG;  // rows / columns per tile (= pass::kPSeg)
 constexpr int kTileDiag = 256;    // longest segment inside a multi-segment tile (= pass::kMaxDiag)
+// jagged-diagonal slack per tile: 8 warp blocks each aligned to 32 elements, + the tile's
+// own alignment (tile t's JDS copy starts at align32(k0_t + kTilePad * t))
+constexpr int kTilePad = 288;
 constexpr int kSmallCone = kTileSeg;  // cones up to this size are projected inside the column tile
 constexpr int kReportFieldsRow = 5;
 constexpr int kReportFieldsCol = 8;

@@ -142,78 +142,83 @@ inline int bits_for(uint64_t maxval) {
     return b;
 }
 
-// Warp-local jagged-diagonal layout of one tile (see cf_pass.cuh). Warp w
-// handles the block of segments [32w, 32w+32): ranks them by length
-// (descending, stable), writes pl[rank] = local segment | length << 5 |
-// start_w << 14 (one u32 per segment position) and scatters the k-th nonzero of rank r to
-// k0 + start_w + sum_{j<k} width_j + r, where width_j = number of the block's
-// segments longer than j and start_w = nonzeros of the blocks before w. The
-// pass recomputes those offsets from the lengths with warp ballots. A long
-// tile (normal flag 0) is copied as is.
+// Jagged-diagonal layout of one tile (see cf_pass.cuh). The tile's segments are ranked
+// by length over the whole tile (descending, ties in segment order); warp block w is
+// ranks [32w, 32w+32). pl[s0 + rank] = local segment | length << 8 | start_w << 17,
+// and the k-th nonzero of rank r goes to base + start_w + sum_{j<k} width_j + (r mod 32),
+// width_j = ranks of the block longer than j, start_w = the blocks before w each rounded
+// up to 32 elements (so every full diagonal is aligned). base = tb.w, a multiple of 32.
+// The pass recomputes the offsets from the lengths with warp ballots. A long tile
+// (normal flag 0) is copied as is (canonical order) to base.
 __global__ void __launch_bounds__(kTileSeg) k_build_jds(const int32_t* ptr, const int32_t* isrc,
                                                         const double* vsrc, const int4* tb, int32_t* idst,
                                                         double* vdst, uint32_t* pl) {
     constexpr int kW = kTileSeg / 32;
     __shared__ int lens[kTileSeg];
-    __shared__ int bsum[kW], bmax[kW];
+    __shared__ int perm[kTileSeg];
+    __shared__ int rlen[kTileSeg];
+    __shared__ int bsum[kW];
     __shared__ int boff[kW + 1];
     __shared__ int jo[kW][kTileDiag + 2];
     const int t = blockIdx.x;
     const int4 lo = tb[t], hi = tb[t + 1];
-    const int s0 = lo.x, nseg = hi.x - lo.x, k0 = lo.y, k1 = hi.y, normal = lo.z;
+    const int s0 = lo.x, nseg = hi.x - lo.x, k0 = lo.y, k1 = hi.y, normal = lo.z, base = lo.w;
     if (!normal) {
-        for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
-            idst[k] = isrc[k];
-            vdst[k] = vsrc[k];
+        for (int k = threadIdx.x; k < k1 - k0; k += blockDim.x) {
+            idst[base + k] = isrc[k0 + k];
+            vdst[base + k] = vsrc[k0 + k];
         }
         if (threadIdx.x == 0) pl[s0] = 0;
         return;
     }
-    const int w = threadIdx.x >> 5, r = threadIdx.x & 31;
     const int q = threadIdx.x;
     const bool valid = q < nseg;
     const int len = valid ? ptr[s0 + q + 1] - ptr[s0 + q] : -1;
     lens[q] = len;
-    // rank inside the warp block: longer first, ties in segment order
-    int rank = 0;
-    for (int r2 = 0; r2 < 32; ++r2) {
-        const int l2 = __shfl_sync(0xffffffffu, len, r2);
-        rank += (l2 > len) || (l2 == len && r2 < r);
+    __syncthreads();
+    if (valid) {
+        // rank over the tile: longer first, ties in segment order
+        int rank = 0;
+        for (int q2 = 0; q2 < nseg; ++q2) {
+            const int l2 = lens[q2];
+            rank += (l2 > len) || (l2 == len && q2 < q);
+        }
+        perm[rank] = q;
+        rlen[rank] = len;
     }
-    int sum = valid ? len : 0, mx = valid ? len : 0;
-    for (int off = 16; off > 0; off >>= 1) {
-        sum += __shfl_xor_sync(0xffffffffu, sum, off);
-        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-    }
-    if (r == 0) {
-        bsum[w] = sum;
-        bmax[w] = mx;
-    }
+    __syncthreads();
+    // thread r now stands for rank r
+    const int r = threadIdx.x, w = r >> 5, l = r & 31;
+    const bool rv = r < nseg;
+    const int myl = rv ? rlen[r] : 0;
+    int sum = myl;
+    for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+    if (l == 0) bsum[w] = sum;
     __syncthreads();
     if (threadIdx.x == 0) {
         boff[0] = 0;
-        for (int b = 0; b < kW; ++b) boff[b + 1] = boff[b] + (b * 32 < nseg ? bsum[b] : 0);
+        for (int bk = 0; bk < kW; ++bk) boff[bk + 1] = boff[bk] + (bk * 32 < nseg ? (bsum[bk] + 31) / 32 * 32 : 0);
     }
     __syncthreads();
-    if (valid) pl[s0 + w * 32 + rank] = (uint32_t)r | ((uint32_t)len << 5) | ((uint32_t)boff[w] << 14);
+    if (rv) pl[s0 + r] = (uint32_t)perm[r] | ((uint32_t)myl << 8) | ((uint32_t)boff[w] << 17);
     if (w * 32 < nseg) {
-        const int mlen = bmax[w];
-        // width of diagonal k = number of segments of the block longer than k
-        for (int k = r; k < mlen; k += 32) {
+        const int mlen = rlen[w * 32];   // the block's longest
+        // width of diagonal k = ranks of the block longer than k
+        for (int k = l; k < mlen; k += 32) {
             int wd = 0;
-            for (int r2 = 0; r2 < 32; ++r2) wd += lens[w * 32 + r2] > k;
+            for (int r2 = 0; r2 < 32; ++r2) wd += (w * 32 + r2 < nseg) && rlen[w * 32 + r2] > k;
             jo[w][k + 1] = wd;
         }
         __syncwarp();
-        if (r == 0) {
+        if (l == 0) {
             jo[w][0] = boff[w];
             for (int k = 0; k < mlen; ++k) jo[w][k + 1] += jo[w][k];
         }
         __syncwarp();
-        if (valid) {
-            const int src0 = ptr[s0 + q];
-            for (int kk = 0; kk < len; ++kk) {
-                const int dst = k0 + jo[w][kk] + rank;
+        if (rv) {
+            const int src0 = ptr[s0 + perm[r]];
+            for (int kk = 0; kk < myl; ++kk) {
+                const int dst = base + jo[w][kk] + l;
                 idst[dst] = isrc[src0 + kk];
                 vdst[dst] = vsrc[src0 + kk];
             }
@@ -221,7 +226,6 @@ __global__ void __launch_bounds__(kTileSeg) k_build_jds(const int32_t* ptr, cons
     }
 }
 
-// Greedy tile starts over segments [s_begin, s_end) of a compressed layout:
 // a tile takes consecutive segments while it stays within kTileSeg segments
 // and kTileNnz nonzeros and holds no segment longer than kTileDiag; such a long
 // segment gets a (long) tile of its own. `longs` lists the long segments in
@@ -293,13 +297,29 @@ void tile_table(const int32_t* ptr, const std::vector<int64_t>& starts, int64_t 
     tb.push_back(make_int4((int)s_end, ptr[s_end], 0, 0));
 }
 
-int build_jds(cf_plan* p, const int32_t* ptr, const int32_t* isrc, const double* vsrc, const std::vector<int4>& tb,
+int build_jds(cf_plan* p, const int32_t* ptr, const int32_t* isrc, const double* vsrc, const std::vector<int4>& tb_in,
               int64_t nseg_total, DevBuf<int4>& dtb, DevBuf<int32_t>& idst, DevBuf<double>& vdst,
               DevBuf<uint32_t>& pl) {
+    // JDS base of every tile: align32(k0 + kTilePad * t) leaves room for the per-block
+    // alignment slack of every tile before it (cf_pass.cuh kTilePad)
+    std::vector<int4> tb(tb_in);
+    for (size_t t = 0; t < tb.size(); ++t) {
+        const int64_t b = ((int64_t)tb[t].y + (int64_t)kTilePad * (int64_t)t + 31) / 32 * 32;
+        if (b > INT32_MAX - 64) {
+            set_error("build_jds: padded nonzero positions exceed int32");
+            return CF_EINVAL;
+        }
+        tb[t].w = (int)b;
+    }
+    const int64_t jds_len = (int64_t)tb.back().w + 32;
     CF_TRY(dtb.alloc(tb.size()));
     CF_CUDA(cudaMemcpyAsync(dtb.p, tb.data(), tb.size() * sizeof(int4), cudaMemcpyHostToDevice, p->stream));
-    CF_TRY(idst.alloc(p->o));
-    CF_TRY(vdst.alloc(p->o));
+    CF_TRY(idst.alloc(jds_len));
+    CF_TRY(vdst.alloc(jds_len));
+    // padding slots are never read by a lane; zero them so staged copies see defined bytes
+    CF_CUDA(cudaMemsetAsync(idst.p, 0, (size_t)jds_len * 4, p->stream));
+    CF_CUDA(cudaMemsetAsync(vdst.p, 0, (size_t)jds_len * 8, p->stream));
+    CF_CUDA(cudaStreamSynchronize(p->stream));   // tb (a host copy) is released at return
     CF_TRY(pl.alloc(nseg_total));
     const int64_t ntiles = (int64_t)tb.size() - 1;
     if (ntiles > 0) {

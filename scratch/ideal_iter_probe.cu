@@ -37,18 +37,26 @@ __device__ __forceinline__ void sth(double* p, double v, uint64_t pol) {
     asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
 }
 
-// segment sum over ELL column k*S + s, gathering g
+#ifndef BATCH
+#define BATCH L    // idx/val loads (then gathers) in flight per batch: L = all at once
+#endif
+// segment sum over ELL column k*S + s, gathering g, in batches of BATCH dependent rounds
 __device__ __forceinline__ double ell_sum(const int* __restrict__ idx, const double* __restrict__ val,
                                           const double* __restrict__ g, int64_t S, int64_t s, double acc,
                                           uint64_t pf, uint64_t pl) {
-    int j[L];
-    double a[L], v[L];
 #pragma unroll
-    for (int k = 0; k < L; ++k) { j[k] = ldh(idx + k * S + s, pf); a[k] = ldh(val + k * S + s, pf); }
+    for (int k0 = 0; k0 < L; k0 += BATCH) {
+        int j[BATCH];
+        double a[BATCH], v[BATCH];
 #pragma unroll
-    for (int k = 0; k < L; ++k) v[k] = ldh(g + j[k], pl);
+        for (int k = 0; k < BATCH; ++k) {
+            if (k0 + k < L) { j[k] = ldh(idx + (k0 + k) * S + s, pf); a[k] = ldh(val + (k0 + k) * S + s, pf); }
+        }
 #pragma unroll
-    for (int k = 0; k < L; ++k) acc = __dadd_rn(acc, __dmul_rn(a[k], v[k]));
+        for (int k = 0; k < BATCH; ++k) if (k0 + k < L) v[k] = ldh(g + j[k], pl);
+#pragma unroll
+        for (int k = 0; k < BATCH; ++k) if (k0 + k < L) acc = __dadd_rn(acc, __dmul_rn(a[k], v[k]));
+    }
     return acc;
 }
 
