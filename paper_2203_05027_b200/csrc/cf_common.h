@@ -42,7 +42,9 @@ constexpr int kTileSeg = CF_PSEG;  // rows / columns per tile (= pass::kPSeg)
 constexpr int kTileDiag = 256;    // longest segment inside a multi-segment tile (= pass::kMaxDiag)
 // jagged-diagonal slack per tile: 8 warp blocks each aligned to 32 elements, + the tile's
 // own alignment (tile t's JDS copy starts at align32(k0_t + kTilePad * t))
-constexpr int kTilePad = 288;
+constexpr int kTilePad = (kTileSeg / 32) * 32 + 32;
+// pl = tile-local segment | length << kPlPermBits | block start << (kPlPermBits + 9)
+constexpr int kPlPermBits = kTileSeg <= 256 ? 8 : 9;
 constexpr int kSmallCone = kTileSeg;  // cones up to this size are projected inside the column tile
 constexpr int kReportFieldsRow = 5;
 constexpr int kReportFieldsCol = 8;

@@ -75,7 +75,7 @@ constexpr int kMinBlocks = CF_MINB;
 static_assert(kTilePad >= kComputeWarps * 31 + 31, "tile padding must cover the block alignment");
 constexpr int kLongChunk = kComputeWarps * 128;   // long tiles: products buffered per chunk (in the vals buffer)
 constexpr int kFvTab = 256;
-constexpr int kPlPermBits = 8, kPlLenBits = 9;   // pl = local segment | length << 8 | block start << 17
+constexpr int kPlLenBits = 9;   // pl = local segment | length << kPlPermBits | block start << (kPlPermBits + 9)
 static_assert(kPSeg <= (1 << kPlPermBits), "tile-local segment must fit pl");
 static_assert(kMaxDiag < (1 << kPlLenBits), "segment length must fit pl");
 

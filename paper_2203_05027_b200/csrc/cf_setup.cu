@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(kTileSeg) k_build_jds(const int32_t* ptr, cons
         for (int bk = 0; bk < kW; ++bk) boff[bk + 1] = boff[bk] + (bk * 32 < nseg ? (bsum[bk] + 31) / 32 * 32 : 0);
     }
     __syncthreads();
-    if (rv) pl[s0 + r] = (uint32_t)perm[r] | ((uint32_t)myl << 8) | ((uint32_t)boff[w] << 17);
+    if (rv) pl[s0 + r] = (uint32_t)perm[r] | ((uint32_t)myl << kPlPermBits) | ((uint32_t)boff[w] << (kPlPermBits + 9));
     if (w * 32 < nseg) {
         const int mlen = rlen[w * 32];   // the block's longest
         // width of diagonal k = ranks of the block longer than k
