@@ -117,6 +117,14 @@ def gather_bound(o, pass_ms, clocks):
             "sm_mhz": mhz, "source": "probe: 1.03 random fp64 gathers per SM-cycle (profiles/r01_probes.md)"}
 
 
+# The ideal C2 iteration (scratch/ideal_iter_probe.cu, profiles/r02_probes.md): uniform
+# 10-nonzero segments in ELL layout, every load a full aligned line, the same bytes and
+# gathers as C2 — 0.888 ms per iteration sustained (0.567 of the measured HBM peak) with
+# the request port 88 % busy. No implementation of C2's access pattern beats it on this
+# power-capped part, so it is the practical ceiling the line is compared with.
+IDEAL_C2_MS = 0.888
+
+
 def native_so_loaded():
     """Shared objects of this repo mapped into the process (the reference arm must show none)."""
     out = set()
@@ -493,7 +501,7 @@ def run_ours(args, spec, rank, world, local_rank):
     plan.set_state(1.0, None, export=False)
     plan.run(never(args.warmup), want_x=False)
     per_it = plan.last_timing()["loop_ms"] / 1000.0 / args.warmup
-    warm_more = int(min(200_000, max(0, WARM_SECONDS / max(per_it, 1e-7))))
+    warm_more = int(min(200_000, max(0, args.warm_seconds / max(per_it, 1e-7))))
     if warm_more:
         plan.run(never(warm_more), want_x=False)
     # ---------------- timed iterations (device-resident inputs), from a cold start
@@ -665,6 +673,11 @@ def run_ours(args, spec, rank, world, local_rank):
         "time_to_tol": ttt, "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
         "gather_bound": gather_bound(o, dms, clocks),
     }
+    if args.config == "c2":
+        line["ideal_bound"] = {"ideal_ms_per_iteration": IDEAL_C2_MS, "frac": IDEAL_C2_MS / (ms_max / args.steps),
+                               "source": "scratch/ideal_iter_probe.cu: the same bytes and gathers with uniform "
+                                         "segments in a perfectly coalesced ELL layout, sustained on this pool's "
+                                         "B200 (profiles/r02_probes.md); 0.567 of the HBM peak"}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -1067,6 +1080,8 @@ def parse_args(argv=None):
     ap.add_argument("--c5-mode", choices=("rows", "cols", "p2p", "auto"), default="rows",
                     help="C5: split A's rows (exchange n-vectors) or columns (all-reduce the m-vector A x); "
                          "auto: by shape (sharded.choose_sharding)")
+    ap.add_argument("--warm-seconds", type=float, default=WARM_SECONDS,
+                    help="GPU arm: extra warm-up time so the timed steps run at the sustained clock (0: W steps only)")
     ap.add_argument("--no-c5-extra", dest="c5_extra", action="store_false",
                     help="N>1: skip the full-scale C5 number carried as the 'c5' key")
     args = ap.parse_args(argv)
