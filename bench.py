@@ -760,7 +760,7 @@ def run_strong(args, spec, rank, world, local_rank, group=None, factories=None, 
         m, n, o = int(problem.A.num_rows), int(problem.A.num_cols), int(problem.A.nnz)
         fp = None
         bn, cn = norms(problem.b), norms(problem.c)
-    mode = choose_sharding(m, n, world)
+    mode = choose_sharding(m, n, world) if args.layout == "auto" else args.layout
 
     def backend():
         if on_gpu:
@@ -1080,6 +1080,10 @@ def parse_args(argv=None):
     ap.add_argument("--c5-mode", choices=("rows", "cols", "p2p", "auto"), default="rows",
                     help="C5: split A's rows (exchange n-vectors) or columns (all-reduce the m-vector A x); "
                          "auto: by shape (sharded.choose_sharding)")
+    ap.add_argument("--strong", action="store_true",
+                    help="run the N>1 strong-scaling path even at N=1 (an NCCL group of one; tests the code path)")
+    ap.add_argument("--layout", choices=("auto", "rows", "cols"), default="auto",
+                    help="N>1 path: sharding layout (auto: sharded.choose_sharding by shape)")
     ap.add_argument("--warm-seconds", type=float, default=WARM_SECONDS,
                     help="GPU arm: extra warm-up time so the timed steps run at the sustained clock (0: W steps only)")
     ap.add_argument("--no-c5-extra", dest="c5_extra", action="store_false",
@@ -1098,22 +1102,28 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return run_reference(args, spec, rank)
-    if world > 1:
+    distributed = world > 1 or (args.strong and not spec.get("sharded") and "batch" not in spec)
+    if distributed:
         import torch
         import torch.distributed as tdist
 
         torch.cuda.set_device(local_rank)
-        tdist.init_process_group("nccl")
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            tdist.init_process_group("nccl", rank=0, world_size=1)
+        else:
+            tdist.init_process_group("nccl")
     try:
         if "batch" in spec:
             return run_batch(args, spec, rank, world)
         if spec.get("sharded"):
             return run_sharded_bench(args, spec, rank, world, local_rank)
-        if world > 1:
+        if distributed:
             return run_strong(args, spec, rank, world, local_rank)
         return run_ours(args, spec, rank, world, local_rank)
     finally:
-        if world > 1:
+        if distributed:
             import torch.distributed as tdist
 
             tdist.destroy_process_group()
