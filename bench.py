@@ -375,9 +375,10 @@ def reference_solve(a, eps):
     return tr[-1]["iter"], secs, rep, "port"
 
 
-def run_reference_batch(args, spec):
-    """C4 reference arm: the reference's own run_bench (bench.py:96-106, a process pool over
-    solve()) on every host core, over a bounded prefix of the batch."""
+def reference_batch_baseline(args, spec):
+    """C4 CPU baseline: the reference's own run_bench (bench.py:96-106, a process pool over
+    solve()) on every host core, over a bounded prefix of the batch (the oracle port in the
+    same scheme without baseline/_ref). Returns a cpu_baseline dict in problem-iterations/s."""
     workers = os.cpu_count() or 1
     P = min(spec["batch"], 16 * workers)
     cfg_kw = dict(eps_prim=args.eps, eps_dual=args.eps, eps_gap=args.eps)
@@ -403,6 +404,13 @@ def run_reference_batch(args, spec):
 
         probs = [generate(GenSpec(spec["m"], spec["n"], spec["density"], spec["cone_kind"], seed=s)) for s in range(P)]
         cpu = cpu_batch_pool(probs, SolverConfig(**cfg_kw), args.eps, args.cpu_budget)
+    return cpu
+
+
+def run_reference_batch(args, spec):
+    """C4 reference arm: reference_batch_baseline on every host core."""
+    workers = os.cpu_count() or 1
+    cpu = reference_batch_baseline(args, spec)
     value = cpu["value"]
     line = {
         "metric": METRIC, "value": value, "unit": "problem-iterations/s", "n_gpus": args.gpus, "steps": 1,
@@ -1042,7 +1050,7 @@ def run_batch(args, spec, rank, world):
         statuses[r.report.status] = statuses.get(r.report.status, 0) + 1
     cpu = None
     if not args.skip_cpu:
-        cpu = cpu_batch_pool(probs, cfg, args.eps, args.cpu_budget)
+        cpu = reference_batch_baseline(args, spec)
     line = {
         "metric": METRIC, "value": value, "unit": "problem-iterations/s", "n_gpus": world, "steps": 1,
         "warmup": args.warmup, "ms_per_step": tim["kernel_ms"], "higher_is_better": True, "scaling": "weak",
