@@ -687,9 +687,16 @@ def run_sharded(be, row_cuts, col_cuts, cfg, b_norms, c_norms, group=None, timin
 # rank); the column part (A_s^T lam over the slice) is all-reduced.
 
 def local_columns(p, c0: int, c1: int):
-    """The rank's columns [c0, c1) renumbered from 0, all rows, with the slice's cones."""
+    """The rank's columns [c0, c1) renumbered from 0, all rows, with the slice's cones.
+
+    Entries already sorted by column (canonical order, as generate.py stores them) are a
+    contiguous range found by binary search; any other order takes a mask pass."""
     cols = np.asarray(p.A.cols, dtype=np.int64)
-    sel = (cols >= c0) & (cols < c1)
+    if cols.size and bool(np.all(cols[1:] >= cols[:-1])):
+        k0, k1 = int(np.searchsorted(cols, c0, "left")), int(np.searchsorted(cols, c1, "left"))
+        sel = slice(k0, k1)
+    else:
+        sel = (cols >= c0) & (cols < c1)
     a = TripletMatrix(p.A.num_rows, c1 - c0, np.asarray(p.A.rows)[sel], cols[sel] - c0, np.asarray(p.A.vals)[sel])
     sizes = cone_sizes_array(p.cones)
     starts = np.concatenate(([0], np.cumsum(sizes)))
@@ -871,7 +878,7 @@ def solve_col_sharded(p, cfg: SolverConfig | None = None, group=None, backend_fa
     cfg = cfg or SolverConfig()
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    _, col_cuts = partition(p, world)
+    col_cuts = column_cuts(cone_sizes_array(p.cones), int(p.A.num_cols), world)   # no row counts needed
     lp = local_columns(p, col_cuts[rank], col_cuts[rank + 1])
     be = (backend_factory or CudaColBackend)(lp)
     try:
