@@ -846,7 +846,12 @@ def run_strong(args, spec, rank, world, local_rank, group=None, factories=None, 
                        "and the x/lam gather)"}
     c5 = None
     if on_gpu and args.c5_extra and args.c5_scale > 0:
-        c5 = run_sharded_bench(args, CONFIGS["c5"], rank, world, local_rank, emit=False)
+        # an extra: a failure here (e.g. memory on a small part) must not void the C2 line
+        try:
+            c5 = run_sharded_bench(args, CONFIGS["c5"], rank, world, local_rank, emit=False)
+        except Exception as exc:   # noqa: BLE001
+            c5 = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+            torch.cuda.synchronize()
     if rank == 0:
         row_b, col_b = algorithmic_bytes(m, n, o)
         peak, src = hbm_peak()
