@@ -40,8 +40,8 @@ constexpr int kTileNnzLarge = CF_PCAP_LARGE;
 constexpr int kStagedMaxTiles = CF_MEDIUM_TILES;   // passes with more tiles per launch run unstaged
 constexpr int kTileSeg = CF_PSEG;  // rows / columns per tile (= pass::kPSeg)
 constexpr int kTileDiag = 256;    // longest segment inside a multi-segment tile (= pass::kMaxDiag)
-// jagged-diagonal slack per tile: 8 warp blocks each aligned to 32 elements, + the tile's
-// own alignment (tile t's JDS copy starts at align32(k0_t + kTilePad * t))
+// jagged-diagonal slack per tile-ranked tile: 8 warp blocks each aligned to 32 elements, +
+// the tile's own alignment (cf_setup.cu build_jds)
 constexpr int kTilePad = (kTileSeg / 32) * 32 + 32;
 // pl = tile-local segment | length << kPlPermBits | block start << (kPlPermBits + 9)
 constexpr int kPlPermBits = kTileSeg <= 256 ? 8 : 9;
@@ -193,6 +193,9 @@ struct cf_plan {
     int64_t panel_cols = 0;
     std::vector<int64_t> row_panel_tile;   // first row tile of each panel (n_panels+1)
     std::vector<int32_t> col_tile_start;   // first segment of each column tile (host copy, col_tiles+1)
+    // prefix counts of tile-ranked (aligned, unstageable) tiles: a launch over tiles [t0, t1)
+    // may stage them iff the count over the range is 0
+    std::vector<int32_t> row_unpacked, col_unpacked;
     // column-pass row bands: with h larger than ~48 MB the column pass runs band by band
     // (segment = band*n + col, each band's slice of h L2-resident), carrying the partial
     // column sums in atcarry; only the last band runs the epilogue

@@ -634,13 +634,20 @@ inline int grid_for(int64_t work, int threads) {
     return (int)g;
 }
 
+// every tile of [t0, t1) is block-ranked and packed, so it fits a TileStage
+// (unpacked[t] = tile-ranked tiles among the first t; size = tiles + 1)
+int32_t stageable(const std::vector<int32_t>& unpacked, int64_t t0, int64_t t1) {
+    if (t0 < 0 || t1 <= t0 || t1 >= (int64_t)unpacked.size() + 1) return 0;
+    return unpacked[t1] - unpacked[t0] == 0 ? 1 : 0;
+}
+
 pass::Tiles row_panel_tiles(const cf_plan* p, int panel) {
     const int64_t t0 = p->row_panel_tile[panel], t1 = p->row_panel_tile[panel + 1];
-    return pass::Tiles{p->row_tb.p + t0, (int32_t)(t1 - t0), !p->row_large_tiles};
+    return pass::Tiles{p->row_tb.p + t0, (int32_t)(t1 - t0), stageable(p->row_unpacked, t0, t1)};
 }
 pass::Tiles col_band_tiles(const cf_plan* p, int band) {
     const int64_t t0 = p->col_band_tile[band], t1 = p->col_band_tile[band + 1];
-    return pass::Tiles{p->col_tb.p + t0, (int32_t)(t1 - t0), !p->col_large_tiles};
+    return pass::Tiles{p->col_tb.p + t0, (int32_t)(t1 - t0), stageable(p->col_unpacked, t0, t1)};
 }
 pass::Jds row_jds(const cf_plan* p) {
     return pass::Jds{p->rj_idx.p, p->rj_val.p, p->rj_pl.p, (int64_t)p->rj_idx.n, p->n};
@@ -714,6 +721,18 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, 
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+#ifndef CF_MEDIUM_MINB
+#define CF_MEDIUM_MINB 4
+#endif
+#ifndef CF_CARVEOUT
+#define CF_CARVEOUT 1      // size the carve-out of the unstaged variants for kMinBlocks CTAs too
+#endif
+#ifndef CF_STAGED_CTAS
+#define CF_STAGED_CTAS 3   // staged CTAs per SM the shared-memory carve-out is sized for (0: driver default)
+#endif
+#ifndef CF_STAGED_CAP
+#define CF_STAGED_CAP 0   // >0: at most this many staged CTAs per SM (their shared memory starves the gathers' L1)
+#endif
 // resident CTAs of k_pass<P> on the device (computed once, thread-safe: plans are
 // created and run from several host threads by solve_batch / run_bench)
 template <class P>
@@ -722,6 +741,16 @@ int pass_capacity() {
         int per_sm = 0, sms = 0, dev = 0;
         bool ok = cudaFuncSetAttribute(pass::k_pass<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)pass::smem_bytes<P>()) == cudaSuccess;
+        // The L1 left beside the shared-memory carve-out is what keeps the gathers in flight, so
+        // size the carve-out for the CTAs per SM the variant is meant to run (staged tiles hold
+        // ~54 KB each: 3 per SM, 1e6 nonzeros 25 -> 20 us per iteration; the others kMinBlocks)
+        const int ctas = P::kStaged ? CF_STAGED_CTAS : (CF_CARVEOUT ? P::kMinBlocks : 0);
+        if (ok && ctas > 0) {
+            const double need = (double)ctas * (double)(pass::smem_bytes<P>() + 1024);
+            const int pct = std::min(100, (int)std::ceil(100.0 * need / (228.0 * 1024.0)));
+            ok = cudaFuncSetAttribute(pass::k_pass<P>, cudaFuncAttributePreferredSharedMemoryCarveout, pct) ==
+                 cudaSuccess;
+        }
         ok = ok && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pass::k_pass<P>, pass::kPThreads,
                                                                  pass::smem_bytes<P>()) == cudaSuccess;
         ok = ok && cudaGetDevice(&dev) == cudaSuccess;
@@ -760,7 +789,7 @@ struct Wide : P {
 template <class P>
 struct Medium : P {
     static constexpr int kUnroll = P::kMediumUnroll;
-    static constexpr int kMinBlocks = 4;
+    static constexpr int kMinBlocks = CF_MEDIUM_MINB;
     static constexpr bool kStaged = CF_STAGED_SMALL;
 };
 // large passes over long segments (>= 16 nonzeros on average): 4 diagonals in flight,
@@ -777,8 +806,9 @@ constexpr int kMediumTiles = kStagedMaxTiles;
 template <class Q>
 int launch_variant(const Q& pol, const pass::Jds& L, const pass::Tiles& T, const int32_t* done, cudaStream_t st,
                    int* grid_out) {
-    const int grid = persistent_grid<Q>(T.n_tiles);
+    int grid = persistent_grid<Q>(T.n_tiles);
     if (grid <= 0) return CF_ECUDA;
+    if (CF_STAGED_CAP > 0 && Q::kStaged) grid = std::min(grid, CF_STAGED_CAP * 148);
     if (grid_out) *grid_out = grid;
     CF_CUDA(launch_pdl(pass::k_pass<Q>, (unsigned)grid, (unsigned)pass::kPThreads, pass::smem_bytes<Q>(), st, pol, L,
                        T, done));
@@ -998,7 +1028,7 @@ int launch_spmv_cols_range(cf_plan* p, const double* y, double* x, int64_t col_l
     ColSpmv c{};
     c.g_ = y;
     c.y = x;
-    return launch_pass(c, col_jds(p), pass::Tiles{p->col_tb.p + t0, (int32_t)(t1 - t0), !p->col_large_tiles}, nullptr,
+    return launch_pass(c, col_jds(p), pass::Tiles{p->col_tb.p + t0, (int32_t)(t1 - t0), stageable(p->col_unpacked, t0, t1)}, nullptr,
                        p->stream);
 }
 

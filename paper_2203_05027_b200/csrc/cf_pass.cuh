@@ -79,33 +79,48 @@ constexpr int kPlLenBits = 9;   // pl = local segment | length << kPlPermBits | 
 static_assert(kPSeg <= (1 << kPlPermBits), "tile-local segment must fit pl");
 static_assert(kMaxDiag < (1 << kPlLenBits), "segment length must fit pl");
 
-struct alignas(16) Smem {   // 16-byte multiple: a TileStage follows it (cp.async 16-byte copies)
+// Laid out so each flow allocates only a prefix: staged tiles without cones stop after vals,
+// the deferred flow after the third sum buffer and its mbarriers, the cone group epilogue
+// takes everything. Less shared memory leaves more L1 for the gathers in flight.
+struct alignas(16) Smem {   // 16-byte multiple: a TileStage follows the allocated prefix
     double fvtab[kFvTab];               // 1/(1+cnt) for small column counts (uv.py:82)
-    double wacc[3][kPSeg];              // rank -> natural transpose of the sums (3 tiles in flight)
-    int32_t wcnt[3][kPSeg];
-    alignas(8) uint64_t full[3];        // tile sums of a buffer written by every warp (deferred epilogue)
+    double wacc[2][kPSeg];              // rank -> natural transpose of the sums (buffers 0, 1)
+    int32_t wcnt[2][kPSeg];
     double red[kGroups][32];
     double vals[kComputeWarps][4][32];  // epilogue vectors of a warp block (cp.async); long tiles: products
-    alignas(16) double cscr[kGroups][4][kPSeg];   // cone epilogue only: x+, w, delta, delta+ (last member)
+    double wacc2[kPSeg];                // deferred flow only: the third sum buffer
+    int32_t wcnt2[kPSeg];
+    alignas(8) uint64_t full[3];        // deferred flow only: tile sums of a buffer handed in by every warp
+    alignas(16) double cscr[kGroups][4][kPSeg];   // cone group epilogue only: x+, w, delta, delta+
 };
-static_assert(sizeof(Smem) % 16 == 0 && offsetof(Smem, cscr) % 16 == 0, "TileStage alignment");
+static_assert(offsetof(Smem, wacc2) % 16 == 0 && offsetof(Smem, cscr) % 16 == 0, "TileStage alignment");
 static_assert(sizeof(((Smem*)0)->vals) >= kLongChunk * sizeof(double), "long-tile buffer");
+__device__ __forceinline__ double* wacc_buf(Smem& sm, int b) { return b < 2 ? sm.wacc[b] : sm.wacc2; }
+__device__ __forceinline__ int32_t* wcnt_buf(Smem& sm, int b) { return b < 2 ? sm.wcnt[b] : sm.wcnt2; }
 
 constexpr size_t kSmemBytes = sizeof(Smem);
-// policies without a cone epilogue do not allocate the cone scratch
-constexpr size_t kSmemBytesNoCones = offsetof(Smem, cscr);
+// prefixes: staged tiles without cones stop after vals; the deferred flow after the mbarriers;
+// the cone group epilogue takes the whole struct
+constexpr size_t kSmemBytesStaged = offsetof(Smem, wacc2);
+constexpr size_t kSmemBytesDeferred = (offsetof(Smem, full) + sizeof(((Smem*)0)->full) + 15) / 16 * 16;
 
 // Staged tiles (the latency-bound Wide/Medium dispatch): the whole tile's idx/val
 // span (with its alignment slack) is copied to shared memory with 16-byte cp.async
 // at tile start, so a lane pays one DRAM round trip per tile instead of one per batch
-// of diagonals. Placed after the full Smem.
-struct alignas(16) TileStage {
-    int32_t idx[kPCap + kTilePad + 40];
-    double val[kPCap + kTilePad + 40];
+// of diagonals. Placed after the barrier flow's prefix of Smem.
+struct alignas(16) TileStage {   // staged tiles are block-ranked and packed: no alignment slack
+    int32_t idx[kPCap + 40];
+    double val[kPCap + 40];
 };
+// offset of the TileStage (staged policies): after the prefix the flow uses
+template <class P>
+__host__ __device__ constexpr size_t stage_offset() {
+    return P::kGroupEpilogue ? kSmemBytes : kSmemBytesStaged;
+}
 template <class P>
 constexpr size_t smem_bytes() {
-    return P::kStaged ? kSmemBytes + sizeof(TileStage) : (P::kGroupEpilogue ? kSmemBytes : kSmemBytesNoCones);
+    return P::kStaged ? stage_offset<P>() + sizeof(TileStage)
+                      : (P::kGroupEpilogue ? kSmemBytes : kSmemBytesDeferred);
 }
 
 // x / mu; exact multiply when mu is a power of two (then x * (1/mu) == x / mu bit for bit)
@@ -451,8 +466,8 @@ __global__ void __launch_bounds__(kPThreads, P::kMinBlocks) k_pass(const P p0, c
             }
             __syncwarp();
             if (lane < pv_nb)
-                p.segment(sm, pv_tile, pv_s0, gw * 32 + lane, sm.wcnt[b][gw * 32 + lane], sm.wacc[b][gw * 32 + lane],
-                          vv);
+                p.segment(sm, pv_tile, pv_s0, gw * 32 + lane, wcnt_buf(sm, b)[gw * 32 + lane],
+                          wacc_buf(sm, b)[gw * 32 + lane], vv);
             __syncwarp();
         }
         pv_tile = -1;
@@ -486,7 +501,7 @@ __global__ void __launch_bounds__(kPThreads, P::kMinBlocks) k_pass(const P p0, c
                 lane < nbw ? (uint32_t)ld_first(reinterpret_cast<const int32_t*>(L.pl) + s0 + bw * 32 + lane, pol_first())
                            : 0u;
             const int b = seq % 3;
-            if (nbw > 0) block_sums(p, L, nullptr, nullptr, s0, kj, bw, lane, nbw, pr, sm.wacc[b], sm.wcnt[b]);
+            if (nbw > 0) block_sums(p, L, nullptr, nullptr, s0, kj, bw, lane, nbw, pr, wacc_buf(sm, b), wcnt_buf(sm, b));
             drain();                                  // the previous tile's epilogue
             if (P::kVals > 0 && nb > 0) {
                 if (lane < nb) p.load_async(s0 + gw * 32 + lane, slot);   // this tile's epilogue vectors
@@ -502,12 +517,12 @@ __global__ void __launch_bounds__(kPThreads, P::kMinBlocks) k_pass(const P p0, c
             const int32_t* ib = nullptr;
             const double* vb = nullptr;
             if constexpr (P::kStaged) {
-                TileStage& ts = *reinterpret_cast<TileStage*>(smem_raw + kSmemBytes);
+                TileStage& ts = *reinterpret_cast<TileStage*>(smem_raw + stage_offset<P>());
                 __syncthreads();   // the previous tile's readers are done with the stage
-                const int span = hi.w - kj;   // the tile's JDS span, alignment slack included
-                CF_DASSERT(span >= 0 && span <= kPCap + kTilePad + 32);
-                stage_span(ts.idx, L.idx + kj, span, pol_first());
-                stage_span(ts.val, L.val + kj, span, pol_first());
+                // a staged tile is block-ranked and packed: its len elements start at kj
+                CF_DASSERT(lo.z == 2 && len <= kPCap);
+                stage_span(ts.idx, L.idx + kj, len, pol_first());
+                stage_span(ts.val, L.val + kj, len, pol_first());
                 cp_async_commit();
                 ib = ts.idx + (((uintptr_t)(L.idx + kj) & 15u) >> 2);
                 vb = ts.val + (((uintptr_t)(L.val + kj) & 15u) >> 3);
@@ -530,7 +545,12 @@ __global__ void __launch_bounds__(kPThreads, P::kMinBlocks) k_pass(const P p0, c
 #pragma unroll
                 for (int f = 0; f < P::kVals; ++f) vv.v[f] = slot[32 * f];
             }
-            __syncthreads();   // every rank's sum of this tile is in wacc[buf] (wacc[buf ^ 1] is next)
+            // every rank's sum of this tile is in wacc[buf] (wacc[buf ^ 1] is next); a tile ranked
+            // inside its warp blocks (normal flag 2) hands its sums only to its own warp
+            if (lo.z == 2)
+                __syncwarp();
+            else
+                __syncthreads();
             if (nb > 0) {
                 __syncwarp();
                 if (lane < nb)

@@ -177,9 +177,12 @@ __global__ void __launch_bounds__(kTileSeg) k_build_jds(const int32_t* ptr, cons
     lens[q] = len;
     __syncthreads();
     if (valid) {
-        // rank over the tile: longer first, ties in segment order
-        int rank = 0;
-        for (int q2 = 0; q2 < nseg; ++q2) {
+        // rank over the tile (normal = 1) or inside the warp block (normal = 2: the tile runs
+        // with a CTA barrier, which a tile-wide ranking would unbalance): longer first, ties in
+        // segment order
+        const int lo_q = normal == 2 ? (q & ~31) : 0, hi_q = normal == 2 ? min(nseg, lo_q + 32) : nseg;
+        int rank = lo_q;
+        for (int q2 = lo_q; q2 < hi_q; ++q2) {
             const int l2 = lens[q2];
             rank += (l2 > len) || (l2 == len && q2 < q);
         }
@@ -197,7 +200,10 @@ __global__ void __launch_bounds__(kTileSeg) k_build_jds(const int32_t* ptr, cons
     __syncthreads();
     if (threadIdx.x == 0) {
         boff[0] = 0;
-        for (int bk = 0; bk < kW; ++bk) boff[bk + 1] = boff[bk] + (bk * 32 < nseg ? (bsum[bk] + 31) / 32 * 32 : 0);
+        // tile-ranked tiles align every block to 32 elements (full diagonals are aligned
+        // lines); block-ranked tiles (staged launches) stay packed so a tile fits a TileStage
+        for (int bk = 0; bk < kW; ++bk)
+            boff[bk + 1] = boff[bk] + (bk * 32 < nseg ? (normal == 1 ? (bsum[bk] + 31) / 32 * 32 : bsum[bk]) : 0);
     }
     __syncthreads();
     if (rv) pl[s0 + r] = (uint32_t)perm[r] | ((uint32_t)myl << kPlPermBits) | ((uint32_t)boff[w] << (kPlPermBits + 9));
@@ -300,11 +306,14 @@ void tile_table(const int32_t* ptr, const std::vector<int64_t>& starts, int64_t 
 int build_jds(cf_plan* p, const int32_t* ptr, const int32_t* isrc, const double* vsrc, const std::vector<int4>& tb_in,
               int64_t nseg_total, DevBuf<int4>& dtb, DevBuf<int32_t>& idst, DevBuf<double>& vdst,
               DevBuf<uint32_t>& pl) {
-    // JDS base of every tile: align32(k0 + kTilePad * t) leaves room for the per-block
-    // alignment slack of every tile before it (cf_pass.cuh kTilePad)
+    // JDS base of every tile: align32(k0 + kTilePad * (tile-ranked tiles before it) + 31 t)
+    // leaves room for the per-block alignment slack of the tile-ranked tiles before it
+    // (cf_common.h kTilePad); packed (block-ranked) tiles only need their own alignment
     std::vector<int4> tb(tb_in);
+    int64_t aligned = 0;   // tile-ranked (aligned-block) tiles before t: only they need the slack
     for (size_t t = 0; t < tb.size(); ++t) {
-        const int64_t b = ((int64_t)tb[t].y + (int64_t)kTilePad * (int64_t)t + 31) / 32 * 32;
+        const int64_t b = ((int64_t)tb[t].y + (int64_t)kTilePad * aligned + 31 * (int64_t)t + 31) / 32 * 32;
+        if (tb[t].z == 1) ++aligned;
         if (b > INT32_MAX - 64) {
             set_error("build_jds: padded nonzero positions exceed int32");
             return CF_EINVAL;
@@ -477,6 +486,32 @@ int build_tiles(cf_plan* p, const int64_t* sizes, int64_t nb) {
         for (int64_t q = 1; q < nb && uniform; ++q) uniform = sizes[q] == s;
         if (uniform) p->warp_cone = (int32_t)s;
     }
+    // Tiles that run with a CTA barrier (staged launches of the small passes, the cone group
+    // epilogue) keep the ranking inside each warp block (normal flag 2): ranking over the tile
+    // would give one warp the longest block and make the others wait for it at the barrier
+    // (1e6 nonzeros: 19.7 -> 25.4 us per iteration). The rest rank over the tile (flag 1).
+    auto block_rank = [](std::vector<int4>& tb, int64_t t0, int64_t t1) {
+        for (int64_t t = t0; t < t1; ++t)
+            if (tb[t].z) tb[t].z = 2;
+    };
+    if (!p->row_large_tiles)
+        for (int pn = 0; pn < p->n_panels; ++pn)
+            if (p->row_panel_tile[pn + 1] - p->row_panel_tile[pn] <= kStagedMaxTiles)
+                block_rank(rtb, p->row_panel_tile[pn], p->row_panel_tile[pn + 1]);
+    if (!p->all_unit && p->warp_cone == 0) {
+        block_rank(ctb, 0, (int64_t)ctb.size() - 1);
+    } else if (!p->col_large_tiles) {
+        for (int b = 0; b < B; ++b)
+            if (p->col_band_tile[b + 1] - p->col_band_tile[b] <= kStagedMaxTiles)
+                block_rank(ctb, p->col_band_tile[b], p->col_band_tile[b + 1]);
+    }
+    // stageable launch ranges: only block-ranked (packed) tiles fit a TileStage
+    auto packed_prefix = [](const std::vector<int4>& tb, std::vector<int32_t>& pre) {
+        pre.assign(tb.size(), 0);
+        for (size_t t = 0; t + 1 < tb.size(); ++t) pre[t + 1] = pre[t] + (tb[t].z == 1 ? 1 : 0);
+    };
+    packed_prefix(rtb, p->row_unpacked);
+    packed_prefix(ctb, p->col_unpacked);
     CF_TRY(build_jds(p, p->rowptr.p, p->colidx.p, p->valr.p, rtb, nsr, p->row_tb, p->rj_idx, p->rj_val, p->rj_pl));
     if (B > 1) {
         CF_TRY(build_jds(p, p->bcolptr.p, p->browidx.p, p->bvalc.p, ctb, nsc, p->col_tb, p->cj_idx, p->cj_val,
