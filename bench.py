@@ -28,8 +28,8 @@ Also on the GPU line:
   gather_bound the dominant pass against the measured random-gather ceiling
 
 N>1 (torchrun): the SAME C2 instance strong-scaled over the ranks through the sharded
-engine (sharded.choose_sharding picks columns for m < n: one NCCL all-reduce of A x
-per iteration), ``scaling: "strong"``; the full-scale 1e9-nonzero C5 row/column-
+engine (sharded.choose_sharding picks columns for m < n: NCCL reduce-scatter of A x,
+each rank updates its block of rows, all-gather of h), ``scaling: "strong"``; the full-scale 1e9-nonzero C5 row/column-
 sharded number rides along as ``c5``.
 
 --impl reference: the unmodified reference (baseline/_ref/conefree: validate,
@@ -863,9 +863,9 @@ def run_strong(args, spec, rank, world, local_rank, group=None, factories=None, 
             "config": {"workload": spec["workload"], "m": m, "n": n, "o": o, "mu": 1.0, "check_every": 25,
                        "instance_fingerprint": fp,
                        "parallelism": f"{mode}-sharded x{world} (sharded.choose_sharding: "
-                                      + ("NCCL all-reduce of A x per iteration" if mode == "cols" else
+                                      + ("NCCL reduce-scatter of A x, per-rank row block update, all-gather of h" if mode == "cols" else
                                          "per-slice NCCL reduce of A^T h + all-gather of x") + ")"},
-            "gpu_launches": args.steps * (3 if mode == "cols" else 4) + (args.steps // 25) * 5,
+            "gpu_launches": args.steps * 4 + (args.steps // 25) * 5,
             "iteration_roofline": {"bytes_per_iteration_total": row_b + col_b,
                                    "achieved_per_gpu_GBs": (row_b + col_b) / world / per_it / 1e9,
                                    "frac_per_gpu": (row_b + col_b) / world / per_it / 1e9 / peak,
@@ -992,7 +992,7 @@ def run_col_sharded_bench(args, spec, rank, world, m, n, scale, stream, own_grou
     if own_group:
         dist.destroy_process_group()
     return _c5_line(args, spec, rank, world, m, n, scale, int(o_t.item()), ms, steps, emit,
-                    f"column-sharded x{world} (NCCL all-reduce of A x)", steps * 4 + (steps // 25) * 5)
+                    f"column-sharded x{world} (NCCL reduce-scatter of A x, all-gather of h)", steps * 4 + (steps // 25) * 5)
 
 
 def _oracle_iters(p, cfg, budget_s):

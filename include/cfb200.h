@@ -268,6 +268,15 @@ int cf_plan_row_update(cf_plan* plan, double mu, int report);
 /* row part of compute_report over the plan's rows: out = {sum (Ax-b)^2, max|Ax-b|,
  * max|Ax|, sum b*lam, nonfinite(lam)} (host array of 5) */
 int cf_plan_row_parts(cf_plan* plan, double* out5);
+/* column sharding with the row update sharded too: y_update + lam/gamma updates of rows
+ * [r0, r1) only, from that slice of the full A x (reduce-scattered, ax_dev = r1 - r0
+ * doubles); writes lam, h (and b - r when report) at those rows of the plan */
+int cf_plan_row_update_range(cf_plan* plan, double mu, int report, int64_t r0, int64_t r1, const double* ax_dev);
+/* cf_plan_row_parts over rows [r0, r1) from that slice of A x (host array of 5) */
+int cf_plan_row_parts_range(cf_plan* plan, int64_t r0, int64_t r1, const double* ax_dev, double* out5);
+/* Run the plan on an external h buffer (>= m doubles + 64 bytes; e.g. the NCCL all-gather
+ * target of the sharded row update); the current h is copied over. NULL: back to the own. */
+int cf_plan_bind_h(cf_plan* plan, double* h_ext);
 /* x_update + z_update + delta update (solver.py:168-176,186-188,196) on a column slice
  * from the reduced A^T h: all device arrays of n; cone_ptr (device, n_blocks+1,
  * slice-local offsets) or NULL for the orthant; vterm (optional) replaces cnt*x + ath. */

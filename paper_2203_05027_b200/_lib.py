@@ -139,6 +139,9 @@ SIGNATURES = {
     "cf_ipc_open": (c_int, [c_void_p, POINTER(c_void_p)]),
     "cf_ipc_close": (c_int, [_P]),
     "cf_plan_bind_x": (c_int, [_P, _P]),
+    "cf_plan_row_update_range": (c_int, [_P, c_double, c_int, c_int64, c_int64, _P]),
+    "cf_plan_row_parts_range": (c_int, [_P, c_int64, c_int64, _P, _P]),
+    "cf_plan_bind_h": (c_int, [_P, _P]),
     "cf_mc_supported": (c_int, [POINTER(c_int)]),
     "cf_mc_create": (c_int, [c_int64, c_int32, POINTER(c_void_p), POINTER(c_int)]),
     "cf_mc_import": (c_int, [c_int, c_int64, c_int32, POINTER(c_void_p)]),

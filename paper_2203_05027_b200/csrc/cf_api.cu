@@ -141,6 +141,7 @@ int cf_plan_destroy(cf_plan* p) {
     for (cudaEvent_t e : p->prof_events) cudaEventDestroy(e);
     cudaStream_t st = p->own_stream ? p->stream : nullptr;
     if (p->x_own) p->x.p = p->x_own;   // an external x (cf_plan_bind_x) belongs to the caller
+    if (p->h_own) p->h.p = p->h_own;   // likewise an external h (cf_plan_bind_h)
     delete p;  // DevBuf destructors free device memory
     if (st) cudaStreamDestroy(st);
     return CF_OK;
@@ -520,6 +521,51 @@ int cf_plan_row_update(cf_plan* p, double mu, int report) {
     CF_TRY(launch_row_update(p->m, p->ax.p, p->b.p, p->fu.p, p->db.p, p->lam.p, p->h.p,
                              (report || p->keep_br) ? p->br.p : nullptr, mu, p->stream));
     p->br_valid = report || p->keep_br;
+    return CF_OK;
+}
+
+int cf_plan_row_update_range(cf_plan* p, double mu, int report, int64_t r0, int64_t r1, const double* ax_dev) {
+    CF_TRY(check_plan(p, "cf_plan_row_update_range"));
+    CF_TRY(check_mu(mu, "cf_plan_row_update_range"));
+    if (r0 < 0 || r1 < r0 || r1 > p->m || (r1 > r0 && !ax_dev)) {
+        set_error("cf_plan_row_update_range: rows outside the plan or NULL A x");
+        return CF_EINVAL;
+    }
+    if (r1 == r0) return CF_OK;
+    const bool keep = report || p->keep_br;
+    CF_TRY(launch_row_update(r1 - r0, ax_dev, p->b.p + r0, p->fu.p + r0, p->db.p + r0, p->lam.p + r0, p->h.p + r0,
+                             keep ? p->br.p + r0 : nullptr, mu, p->stream));
+    p->br_valid = keep;
+    return CF_OK;
+}
+
+int cf_plan_row_parts_range(cf_plan* p, int64_t r0, int64_t r1, const double* ax_dev, double* out5) {
+    CF_TRY(check_plan(p, "cf_plan_row_parts_range"));
+    if (r0 < 0 || r1 < r0 || r1 > p->m || !out5 || (r1 > r0 && !ax_dev)) {
+        set_error("cf_plan_row_parts_range: bad arguments");
+        return CF_EINVAL;
+    }
+    DevBuf<double> d;
+    CF_TRY(d.alloc(5));
+    CF_TRY(launch_row_parts_range(p, r0, r1, ax_dev, d.p));
+    CF_CUDA(cudaMemcpyAsync(out5, d.p, 5 * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+    CF_CUDA(cudaStreamSynchronize(p->stream));
+    return CF_OK;
+}
+
+int cf_plan_bind_h(cf_plan* p, double* h_ext) {
+    CF_TRY(check_plan(p, "cf_plan_bind_h"));
+    const size_t bytes = (size_t)std::max<int64_t>(p->m, 1) * sizeof(double);
+    if (h_ext) {
+        if (!p->h_own) p->h_own = p->h.p;
+        if (h_ext != p->h.p) CF_CUDA(cudaMemcpyAsync(h_ext, p->h.p, bytes, cudaMemcpyDeviceToDevice, p->stream));
+        p->h.p = h_ext;
+    } else if (p->h_own) {
+        CF_CUDA(cudaMemcpyAsync(p->h_own, p->h.p, bytes, cudaMemcpyDeviceToDevice, p->stream));
+        p->h.p = p->h_own;
+        p->h_own = nullptr;
+    }
+    CF_CUDA(cudaStreamSynchronize(p->stream));
     return CF_OK;
 }
 

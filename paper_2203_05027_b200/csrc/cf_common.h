@@ -224,6 +224,7 @@ struct cf_plan {
     cf::DevBuf<cf_report> report_slot;         // device report ring
     cf::DevBuf<int32_t> done;                  // device early-exit flag
     double* x_own = nullptr;                   // cf_plan_bind_x: the plan's own x while x.p is external
+    double* h_own = nullptr;                   // cf_plan_bind_h: the plan's own h while h.p is external
     cf::DevBuf<int32_t> nf_flag;               // report: non-finite implicit y/gamma
     cf_report* host_reports = nullptr;         // pinned ring
     std::vector<cf_report> trace_all;          // every report of the last cf_plan_solve (grows per report)
@@ -262,6 +263,8 @@ int launch_col_only(cf_plan* p, const IterOpts& opt, const int32_t* done = nullp
 int launch_row_norms(cf_plan* p, double* dout, double* amax);
 int launch_set_row_diag(cf_plan* p, const double* din, const double* amax_in);
 // RowIter's row epilogue from a full A x (column-sharded driver)
+// row part of compute_report over rows [r0, r1) from the given A x slice (column sharding)
+int launch_row_parts_range(cf_plan* p, int64_t r0, int64_t r1, const double* ax, double* out5_dev);
 int launch_row_update(int64_t m, const double* ax, const double* b, const double* fu, const double* db, double* lam,
                       double* h, double* br, double mu, cudaStream_t st);
 // the row pass of one iteration (all column panels)

@@ -1340,6 +1340,26 @@ int launch_row_parts(cf_plan* p, double* out5_dev) {
     return CF_OK;
 }
 
+int launch_row_parts_range(cf_plan* p, int64_t r0, int64_t r1, const double* ax, double* out5_dev) {
+    if (r1 <= r0) {
+        CF_CUDA(cudaMemsetAsync(out5_dev, 0, 5 * sizeof(double), p->stream));
+        return CF_OK;
+    }
+    RowReportArgs a{};
+    a.ax = ax;
+    a.b = p->b.p + r0;
+    a.lam = p->lam.p + r0;
+    a.br = p->br_valid ? p->br.p + r0 : nullptr;
+    a.amax = p->amax.p + r0;
+    a.part = p->part_row.p;
+    a.m = (int32_t)(r1 - r0);
+    k_row_report<<<p->row_report_ctas, kThreads, 0, p->stream>>>(a);
+    CF_LAUNCHED();
+    k_row_parts_final<<<1, 1024, 0, p->stream>>>(p->part_row.p, p->row_report_ctas, out5_dev);
+    CF_LAUNCHED();
+    return CF_OK;
+}
+
 int launch_counts(cf_plan* p, double* cnt) {
     if (p->n == 0) return CF_OK;
     k_counts<<<grid_for(p->n, 256), 256, 0, p->stream>>>(p->colptr.p, p->n, cnt);

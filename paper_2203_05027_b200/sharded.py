@@ -796,6 +796,44 @@ class CudaColBackend:
     def lam_full(self):
         return self.lam
 
+    # ---- the sharded row update (run_col_sharded shard_rows)
+    def ax_into(self, out):
+        """A_s x_s into out[:m] (out: the padded reduce-scatter input)."""
+        from . import _lib
+
+        if self.n:
+            _lib.check(self.lib.cf_apply_A_async(self.plan.handle, self._p(self.x), self._p(out)))
+        else:
+            out[:self.m].zero_()
+
+    def bind_h(self, h):
+        """Run the column pass on h (the all-gather target), or back on the plan's own (None)."""
+        import ctypes
+
+        from . import _lib
+
+        _lib.check(self.lib.cf_plan_bind_h(self.plan.handle, None if h is None else ctypes.c_void_p(h.data_ptr())))
+
+    def row_update_range(self, mu, report, r0, r1, ax_slice):
+        from . import _lib
+
+        _lib.check(self.lib.cf_plan_row_update_range(self.plan.handle, float(mu), 1 if report else 0, int(r0), int(r1),
+                                                     self._p(ax_slice)))
+
+    def row_parts_range(self, r0, r1, ax_slice):
+        from . import _lib
+
+        out = np.zeros(5)
+        _lib.check(self.lib.cf_plan_row_parts_range(self.plan.handle, int(r0), int(r1), self._p(ax_slice),
+                                                    ctypes_ptr(out)))
+        return out
+
+    def lam_range(self, r0, r1):
+        return self.lam[r0:r1]
+
+    def set_lam(self, lam_full):
+        self.lam.copy_(lam_full)
+
     def close(self):
         self.plan.close()
 
@@ -807,41 +845,96 @@ def ctypes_ptr(a):
 
 
 def run_col_sharded(be, col_cuts, cfg, b_norms, c_norms, group=None, timing=None,
-                    gather_result: bool = True) -> SolveResult:
-    """The column-sharded loop on an existing rank backend (column cuts shared by all ranks)."""
+                    gather_result: bool = True, shard_rows: bool | None = None) -> SolveResult:
+    """The column-sharded loop on an existing rank backend (column cuts shared by all ranks).
+
+    ``shard_rows`` (default: when the backend supports it): instead of all-reducing A x and
+    updating every row on every rank, reduce-scatter A x, update this rank's block of
+    rows only, and all-gather h (the column passes gather it) — the same NVLink volume as
+    the all-reduce, 1/N of the row update's HBM traffic per rank. lam is all-gathered on
+    report iterations (A^T lam) and at the end."""
     import torch
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
+    nccl = dist.get_backend(group) == "nccl"
+    if shard_rows is None:
+        shard_rows = hasattr(be, "row_update_range")
     # fu = 1/(1 + d) and the implicit-y finiteness check need WHOLE rows: sum the slices' d
     # (uv.py:81; the association of the sum differs from one GPU's only by rounding)
     d, am = be.row_norms()
     dist.all_reduce(d, op=dist.ReduceOp.SUM, group=group)
     dist.all_reduce(am, op=dist.ReduceOp.MAX, group=group)
     be.set_row_norms(d, am)
+    m = int(d.numel())
+    S = -(-m // world) if m else 0
+    r0, r1 = min(m, rank * S), min(m, (rank + 1) * S)
+    if shard_rows:
+        ax_pad = torch.zeros(world * S, dtype=torch.float64, device=be.device)
+        h_pad = torch.zeros(world * S + 8, dtype=torch.float64, device=be.device)   # + slack (engine reads)
+        be.bind_h(h_pad)
+        ax_mine = ax_pad[rank * S:(rank + 1) * S]
+        h_mine = h_pad[rank * S:(rank + 1) * S]
+        lam_pad = torch.zeros(world * S, dtype=torch.float64, device=be.device)
+
+        def gather_lam():
+            lam_pad[rank * S:rank * S + (r1 - r0)] = be.lam_range(r0, r1)
+            if nccl:
+                dist.all_gather_into_tensor(lam_pad, lam_pad[rank * S:(rank + 1) * S].clone(), group=group)
+            else:
+                parts = [torch.empty(S, dtype=torch.float64) for _ in range(world)]
+                dist.all_gather(parts, lam_pad[rank * S:(rank + 1) * S].clone(), group=group)
+                lam_pad.copy_(torch.cat(parts))
+            be.set_lam(lam_pad[:m])
     trace = []
     if timing is not None and be.device.type == "cuda":
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
     for k in range(1, cfg.max_iters + 1):
         be.col_step(cfg.mu)
-        ax = be.partial_Ax()
-        dist.all_reduce(ax, op=dist.ReduceOp.SUM, group=group)
         report = (k % cfg.check_every == 0) or (k == cfg.max_iters)
-        be.row_update(cfg.mu, report)
+        if shard_rows:
+            be.ax_into(ax_pad)
+            if nccl:   # in place: this rank's block of the sum lands at its own offset
+                dist.reduce_scatter_tensor(ax_mine, ax_pad, op=dist.ReduceOp.SUM, group=group)
+            else:
+                dist.all_reduce(ax_pad, op=dist.ReduceOp.SUM, group=group)
+            ax_slice = ax_mine[:r1 - r0]
+            be.row_update_range(cfg.mu, report, r0, r1, ax_slice)   # writes h_pad[r0:r1]
+            if nccl:
+                dist.all_gather_into_tensor(h_pad[:world * S], h_mine, group=group)
+            else:
+                parts = [torch.empty(S, dtype=torch.float64) for _ in range(world)]
+                dist.all_gather(parts, h_mine.clone(), group=group)
+                h_pad[:world * S].copy_(torch.cat(parts))
+        else:
+            ax = be.partial_Ax()
+            dist.all_reduce(ax, op=dist.ReduceOp.SUM, group=group)
+            be.row_update(cfg.mu, report)
         if not report:
             continue
-        rp = be.row_parts()          # full rows: the same on every rank
+        if shard_rows:
+            rpl = torch.as_tensor(be.row_parts_range(r0, r1, ax_slice), dtype=torch.float64, device=be.device)
+            gather_lam()   # A^T lam below needs every row's lam
+        else:
+            rpl = None
+            rp = be.row_parts()          # full rows: the same on every rank
         cp = torch.as_tensor(be.col_parts(), dtype=torch.float64, device=be.device)
-        sums = torch.stack([cp[0], cp[2], cp[5]])
-        maxs = torch.stack([cp[1], cp[3], cp[4], cp[6], cp[7]])
+        if shard_rows:   # row parts: {sum prim^2, max|prim|, max|Ax|, sum b.lam, nonfinite} over the blocks
+            sums = torch.stack([cp[0], cp[2], cp[5], rpl[0], rpl[3]])
+            maxs = torch.stack([cp[1], cp[3], cp[4], cp[6], cp[7], rpl[1], rpl[2], rpl[4]])
+        else:
+            sums = torch.stack([cp[0], cp[2], cp[5]])
+            maxs = torch.stack([cp[1], cp[3], cp[4], cp[6], cp[7]])
         nan = torch.isnan(maxs).to(torch.float64)
         dist.all_reduce(sums, op=dist.ReduceOp.SUM, group=group)
         dist.all_reduce(maxs, op=dist.ReduceOp.MAX, group=group)
         dist.all_reduce(nan, op=dist.ReduceOp.MAX, group=group)
         maxs = torch.where(nan > 0, torch.full_like(maxs, float("nan")), maxs)
         s, mx = sums.tolist(), maxs.tolist()
+        if shard_rows:
+            rp = [s[3], mx[5], mx[6], s[4], mx[7]]
         f = [rp[0], rp[1], rp[2], rp[3], rp[4], s[0], mx[0], s[1], mx[1], mx[2], s[2], mx[3], mx[4]]
         rep = assemble_report(k, f)
         status = _decide(rep, cfg, b_norms, c_norms)
@@ -855,6 +948,9 @@ def run_col_sharded(be, col_cuts, cfg, b_norms, c_norms, group=None, timing=None
         e1.synchronize()
         timing["loop_ms"] = e0.elapsed_time(e1)
         timing["iters"] = trace[-1].iter
+    if shard_rows:
+        gather_lam()
+        be.bind_h(None)
     if not gather_result:
         return SolveResult(x=None, lam=None, report=trace[-1], trace=tuple(trace))
     S = max(col_cuts[r + 1] - col_cuts[r] for r in range(world))
@@ -869,7 +965,8 @@ def run_col_sharded(be, col_cuts, cfg, b_norms, c_norms, group=None, timing=None
                        report=trace[-1], trace=tuple(trace))
 
 
-def solve_col_sharded(p, cfg: SolverConfig | None = None, group=None, backend_factory=None) -> SolveResult:
+def solve_col_sharded(p, cfg: SolverConfig | None = None, group=None, backend_factory=None,
+                      shard_rows: bool | None = None) -> SolveResult:
     """solve() with A's columns split over the ranks of ``group`` (every rank passes the same problem).
 
     Cold start only. Returns the same SolveResult on every rank."""
@@ -882,7 +979,7 @@ def solve_col_sharded(p, cfg: SolverConfig | None = None, group=None, backend_fa
     lp = local_columns(p, col_cuts[rank], col_cuts[rank + 1])
     be = (backend_factory or CudaColBackend)(lp)
     try:
-        return run_col_sharded(be, col_cuts, cfg, norms(p.b), norms(p.c), group=group)
+        return run_col_sharded(be, col_cuts, cfg, norms(p.b), norms(p.c), group=group, shard_rows=shard_rows)
     finally:
         if hasattr(be, "close"):
             be.close()

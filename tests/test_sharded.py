@@ -241,7 +241,8 @@ class NumpyColBackend:
         self.fu, self.db = 1.0 / (1.0 + d), d * self.b
 
     def col_step(self, mu):
-        ath = np.bincount(self.cols, weights=self.vals * self.h[self.rows], minlength=self.n)
+        h = self.h_t.numpy()[:self.m] if getattr(self, "h_t", None) is not None else self.h
+        ath = np.bincount(self.cols, weights=self.vals * h[self.rows], minlength=self.n)
         fv = 1.0 / (1.0 + self.cnt)
         dm = self.d / mu
         xp = fv * ((((self.cnt * self.x) + ath) + self.z + dm) - self.c / mu)
@@ -282,8 +283,36 @@ class NumpyColBackend:
     def lam_full(self):
         return torch.tensor(self.lam)
 
+    # the sharded row update (run_col_sharded shard_rows): cf_apply_A_async into the padded
+    # reduce-scatter input, cf_plan_row_update_range / _row_parts_range, cf_plan_bind_h
+    def ax_into(self, out):
+        out[:self.m] = torch.tensor(np.bincount(self.rows, weights=self.vals * self.x[self.cols], minlength=self.m))
 
-def _col_worker(rank, world, port, spec, cfg_kw, out_path):
+    def bind_h(self, h):
+        self.h_t = h
+
+    def row_update_range(self, mu, report, r0, r1, ax_slice):
+        ax = ax_slice.numpy()
+        r = self.fu[r0:r1] * (self.db[r0:r1] + ax)
+        self.lam[r0:r1] = self.lam[r0:r1] + mu * (r - self.b[r0:r1])
+        self.h_t.numpy()[r0:r1] = (self.b[r0:r1] - r) - self.lam[r0:r1] / mu
+
+    def row_parts_range(self, r0, r1, ax_slice):
+        if r1 <= r0:
+            return np.zeros(5)
+        ax = ax_slice.numpy()
+        pr = ax - self.b[r0:r1]
+        return np.array([np.sum(pr * pr), np.max(np.abs(pr)), np.max(np.abs(ax)),
+                         np.sum(self.b[r0:r1] * self.lam[r0:r1]), float(not np.isfinite(self.lam[r0:r1]).all())])
+
+    def lam_range(self, r0, r1):
+        return torch.tensor(self.lam[r0:r1])
+
+    def set_lam(self, lam_full):
+        self.lam = lam_full.numpy().copy()
+
+
+def _col_worker(rank, world, port, spec, cfg_kw, out_path, shard_rows=None):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -291,7 +320,7 @@ def _col_worker(rank, world, port, spec, cfg_kw, out_path):
         from paper_2203_05027_b200.sharded import solve_col_sharded
 
         p = generate(spec)
-        res = solve_col_sharded(p, SolverConfig(**cfg_kw), backend_factory=NumpyColBackend)
+        res = solve_col_sharded(p, SolverConfig(**cfg_kw), backend_factory=NumpyColBackend, shard_rows=shard_rows)
         if rank == 0:
             np.savez(out_path, x=res.x, lam=res.lam, iters=np.array([r.iter for r in res.trace]),
                      status=np.array([r.status for r in res.trace]),
@@ -300,15 +329,17 @@ def _col_worker(rank, world, port, spec, cfg_kw, out_path):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,spec,cfg_kw", [
-    (2, GenSpec(40, 90, 0.06, "lp", seed=41), dict(eps_prim=1e-4, eps_dual=1e-4, eps_gap=1e-4, max_iters=4000)),
-    (3, GenSpec(30, 64, 0.08, "socp4", seed=42), dict(mu=0.7, max_iters=600, check_every=20)),
+@pytest.mark.parametrize("world,spec,cfg_kw,shard_rows", [
+    (2, GenSpec(40, 90, 0.06, "lp", seed=41), dict(eps_prim=1e-4, eps_dual=1e-4, eps_gap=1e-4, max_iters=4000), True),
+    (3, GenSpec(31, 64, 0.08, "socp4", seed=42), dict(mu=0.7, max_iters=600, check_every=20), True),   # padded blocks
+    (3, GenSpec(30, 64, 0.08, "socp4", seed=42), dict(mu=0.7, max_iters=600, check_every=20), False),
 ])
-def test_column_sharded_matches_oracle(tmp_path, world, spec, cfg_kw):
-    """Column sharding (one all-reduce of A x per iteration) reaches the oracle's iterates."""
+def test_column_sharded_matches_oracle(tmp_path, world, spec, cfg_kw, shard_rows):
+    """Column sharding reaches the oracle's iterates: reduce-scatter of A x + each rank's block
+    of rows + all-gather of h (shard_rows), or one all-reduce of A x + every row on every rank."""
     out = str(tmp_path / "res.npz")
     port = _free_port()
-    mp.start_processes(_col_worker, args=(world, port, spec, cfg_kw, out), nprocs=world, join=True,
+    mp.start_processes(_col_worker, args=(world, port, spec, cfg_kw, out, shard_rows), nprocs=world, join=True,
                        start_method="spawn")
     got = np.load(out)
     p = generate(spec)

@@ -1,9 +1,18 @@
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/r2_t7_all.log 2>&1; echo "all rc=$?"
-tail -n 1 gpurun_out/r2_t7_all.log
-bash tools/lib_sweep.sh old base nocarve old base nocarve
-CFG=c3 bash tools/lib_sweep.sh old base nocarve
-CFG=c3m bash tools/lib_sweep.sh old base nocarve
-for l in old base; do
-  if [ $l = base ]; then P=""; else P=paper_2203_05027_b200/libcfb200_$l.so; fi
-  echo "== $l"; CF_LIB_PATH=$P timeout 600 python tools/prof_sizes.py 2>&1 | tail -7
-done
+timeout 900 python -X faulthandler -c "
+import sys, runpy, traceback
+sys.argv=['bench.py','--strong','--layout','cols','--steps','50','--warmup','3','--no-c5-extra','--skip-e2e']
+import bench
+args=bench.parse_args(sys.argv[1:])
+import os
+os.environ.setdefault('MASTER_ADDR','127.0.0.1'); os.environ.setdefault('MASTER_PORT','29533')
+import torch, torch.distributed as dist
+torch.cuda.set_device(0)
+dist.init_process_group('nccl', rank=0, world_size=1)
+try:
+    r = bench.run_strong(args, bench.CONFIGS['c2'], 0, 1, 0)
+    print('returned', r, file=sys.stderr)
+except BaseException as e:
+    traceback.print_exc()
+    print('EXC', repr(e), file=sys.stderr)
+" > gpurun_out/r02_dbg.out 2> gpurun_out/r02_dbg.err; echo "rc=$?"
+grep -v "Warning\|return func" gpurun_out/r02_dbg.err | tail -n 30; head -c 300 gpurun_out/r02_dbg.out
