@@ -33,7 +33,7 @@ def needs_build() -> bool:
 
 def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
     """defines/out: experiment variants (e.g. CF_GATHER_WARPS=12) built beside the product library."""
-    target = out or OUT
+    target = os.path.abspath(out) if out else OUT
     if not force and out is None and not defines and not needs_build():
         return OUT
     tmp = target + ".tmp"

@@ -58,6 +58,12 @@ namespace pass {
 #ifndef CF_DEFERRED
 #define CF_DEFERRED 1              // deferred-epilogue pipeline (mbarriers) instead of one CTA barrier per tile
 #endif
+#ifndef CF_FULL_DIAG
+#define CF_FULL_DIAG 1             // full-width diagonals without predicates (block_sums)
+#endif
+#ifndef CF_FULL_UNROLL
+#define CF_FULL_UNROLL 0           // diagonals per batch on the full-width part (0: the policy's kUnroll)
+#endif
 #ifndef CF_BULK_PREFETCH
 #define CF_BULK_PREFETCH 0         // L2-prefetch the idx/val/pl of the tile this many rounds ahead (measured slower)
 #endif
@@ -392,7 +398,45 @@ __device__ __forceinline__ void block_sums(P& p, const Jds& L, const int32_t* ib
     // my segment's carry (no shuffle: the load's latency hides behind the gathers)
     double acc = (p.carry_in() && has) ? p.carry(s0 + q) : 0.0;
     const double* __restrict__ g = p.gvec();
-    for (int k = 0; k < mlen; k += U) {
+    int k = 0;
+#if CF_FULL_DIAG
+    // Full diagonals: the ranks are sorted by length, so while k is below the block's
+    // shortest length (rank 31; 0 for a partial block) every diagonal is 32 wide and
+    // lane l's element k sits at pos + 32 k: constant offsets, no predicates, no ballots.
+    constexpr int UF = CF_FULL_UNROLL > 0 ? CF_FULL_UNROLL : U;
+    const int mmin = __shfl_sync(0xffffffffu, mylen, 31);
+    if (mmin >= UF) {
+        const uint64_t pf = pol_first(), plast = pol_last();
+        for (; k + UF <= mmin; k += UF) {
+            int nj[UF];
+            double nv[UF], gv[UF];
+#pragma unroll
+            for (int u = 0; u < UF; ++u) {
+                if constexpr (P::kStaged) {
+                    CF_DASSERT(pos + 32 * u < kPCap + 8);
+                    nj[u] = ib[pos + 32 * u];
+                    nv[u] = vb[pos + 32 * u];
+                } else {
+                    CF_DASSERT(pos + 32 * u < L.n_idx);
+                    nj[u] = ld_first(L.idx + (pos + 32 * u), pf);
+                    nv[u] = ld_first(L.val + (pos + 32 * u), pf);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < UF; ++u) {
+                CF_DASSERT(nj[u] >= 0 && nj[u] < L.g_len);
+                gv[u] = ld_gather(g + (uint32_t)nj[u], plast);
+            }
+#pragma unroll
+            for (int u = 0; u < UF; ++u) {
+                p.check(nv[u], nj[u], gv[u]);
+                acc = __dadd_rn(acc, __dmul_rn(nv[u], gv[u]));
+            }
+            pos += 32 * UF;
+        }
+    }
+#endif
+    for (; k < mlen; k += U) {
         int nj[U];
         double nv[U], gv[U];
         if constexpr (P::kStaged)
