@@ -123,6 +123,7 @@ def gather_bound(o, pass_ms, clocks):
 # the request port 88 % busy. No implementation of C2's access pattern beats it on this
 # power-capped part, so it is the practical ceiling the line is compared with.
 IDEAL_C2_MS = 0.888
+IDEAL_C2_MHZ = 1965.0   # its sustained SM clock (below the 1 kW cap: 860-910 W)
 
 
 def native_so_loaded():
@@ -682,10 +683,17 @@ def run_ours(args, spec, rank, world, local_rank):
         "gather_bound": gather_bound(o, dms, clocks),
     }
     if args.config == "c2":
-        line["ideal_bound"] = {"ideal_ms_per_iteration": IDEAL_C2_MS, "frac": IDEAL_C2_MS / (ms_max / args.steps),
+        mhz = (clocks or {}).get("sm_mhz") or IDEAL_C2_MHZ
+        per_it = ms_max / args.steps
+        line["ideal_bound"] = {"ideal_ms_per_iteration": IDEAL_C2_MS, "frac": IDEAL_C2_MS / per_it,
+                               "ideal_mhz": IDEAL_C2_MHZ,
+                               # the probe runs below the power cap at the top clock; this line's
+                               # engine runs at the cap: the same comparison at this line's clock
+                               "frac_at_this_clock": IDEAL_C2_MS * IDEAL_C2_MHZ / mhz / per_it,
                                "source": "scratch/ideal_iter_probe.cu: the same bytes and gathers with uniform "
                                          "segments in a perfectly coalesced ELL layout, sustained on this pool's "
-                                         "B200 (profiles/r02_probes.md); 0.567 of the HBM peak"}
+                                         "B200 at 1,965 MHz and 860-910 W (profiles/r02_probes.md); 0.567 of the "
+                                         "HBM peak"}
     print(json.dumps(line), flush=True)
     return 0
 

@@ -64,6 +64,12 @@ namespace pass {
 #ifndef CF_FULL_UNROLL
 #define CF_FULL_UNROLL 0           // diagonals per batch on the full-width part (0: the policy's kUnroll)
 #endif
+#ifndef CF_PRED_TAIL
+#define CF_PRED_TAIL 1             // predicated loads/gathers/adds on the narrow diagonals (block_sums)
+#endif
+#ifndef CF_TAIL_UNROLL
+#define CF_TAIL_UNROLL 0           // diagonals per batch on the narrow part (0: the policy's kUnroll)
+#endif
 #ifndef CF_BULK_PREFETCH
 #define CF_BULK_PREFETCH 0         // L2-prefetch the idx/val/pl of the tile this many rounds ahead (measured slower)
 #endif
@@ -210,6 +216,33 @@ __device__ __forceinline__ double ld_first(const double* p, uint64_t pol) {
 __device__ __forceinline__ int32_t ld_first(const int32_t* p, uint64_t pol) {
     int32_t v;
     asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+// predicated forms returning 0 where !ok: one zeroing move plus a predicated load into
+// the same register (a C++ `ok ? ld : 0` becomes a load into a temporary and a select)
+__device__ __forceinline__ int32_t ld_first_if(const int32_t* p, uint64_t pol, bool ok) {
+    int32_t v;
+    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %3, 0;\n mov.b32 %0, 0;\n"
+                 " @q ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;\n}"
+                 : "=&r"(v) : "l"(p), "l"(pol), "r"((unsigned)ok));
+    return v;
+}
+__device__ __forceinline__ double ld_first_if(const double* p, uint64_t pol, bool ok) {
+    double v;
+    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %3, 0;\n mov.b64 %0, 0;\n"
+                 " @q ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;\n}"
+                 : "=&d"(v) : "l"(p), "l"(pol), "r"((unsigned)ok));
+    return v;
+}
+__device__ __forceinline__ double ld_gather_if(const double* p, uint64_t pol, bool ok) {
+    double v;
+    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %3, 0;\n mov.b64 %0, 0;\n"
+#if CF_GATHER_NOALLOC
+                 " @q ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;\n}"
+#else
+                 " @q ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;\n}"
+#endif
+                 : "=&d"(v) : "l"(p), "l"(pol), "r"((unsigned)ok));
     return v;
 }
 __device__ __forceinline__ void st_hint(double* p, double v, uint64_t pol) {
@@ -436,6 +469,41 @@ __device__ __forceinline__ void block_sums(P& p, const Jds& L, const int32_t* ib
         }
     }
 #endif
+#if CF_PRED_TAIL
+    // the rest (diagonals narrower than 32, or all of a partial block): per-lane
+    // predicated loads, gathers and adds; the ranks are sorted, so the lanes of
+    // diagonal k+u are a prefix and its width is the ballot's popcount
+    constexpr int UT = CF_TAIL_UNROLL > 0 ? CF_TAIL_UNROLL : U;
+    for (; k < mlen; k += UT) {
+        int nj[UT];
+        double nv[UT], gv[UT];
+#pragma unroll
+        for (int u = 0; u < UT; ++u) {
+            const bool ok = mylen > k + u;
+            if constexpr (P::kStaged) {
+                if (ok) CF_DASSERT(pos >= 0 && pos < kPCap + 8);
+                nj[u] = ok ? ib[pos] : 0;
+                nv[u] = ok ? vb[pos] : 0.0;
+            } else {
+                if (ok) CF_DASSERT(pos >= 0 && pos < L.n_idx);
+                nj[u] = ld_first_if(L.idx + pos, pol_first(), ok);
+                nv[u] = ld_first_if(L.val + pos, pol_first(), ok);
+            }
+            pos += __popc(__ballot_sync(0xffffffffu, ok));   // width of diagonal k+u
+        }
+#pragma unroll
+        for (int u = 0; u < UT; ++u) {
+            const bool ok = mylen > k + u;
+            if (ok) CF_DASSERT(nj[u] >= 0 && nj[u] < L.g_len);
+            gv[u] = ld_gather_if(g + (uint32_t)nj[u], pol_last(), ok);
+        }
+#pragma unroll
+        for (int u = 0; u < UT; ++u) {
+            if (mylen > k + u) p.check(nv[u], nj[u], gv[u]);
+            acc = __dadd_rn(acc, __dmul_rn(nv[u], gv[u]));   // +0.0 * +0.0 past my segment: acc unchanged
+        }
+    }
+#else
     for (; k < mlen; k += U) {
         int nj[U];
         double nv[U], gv[U];
@@ -456,6 +524,7 @@ __device__ __forceinline__ void block_sums(P& p, const Jds& L, const int32_t* ib
             acc = __dadd_rn(acc, __dmul_rn(nv[u], gv[u]));
         }
     }
+#endif
     if (has) {
         wacc[q] = acc;
         wcnt[q] = mylen;
