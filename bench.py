@@ -817,8 +817,13 @@ def run_strong(args, spec, rank, world, local_rank, group=None, factories=None, 
 
     zero = dict(check_every=25, eps_prim=0.0, eps_dual=0.0, eps_gap=0.0)
     loop(SolverConfig(max_iters=args.warmup, **zero), {})               # warm-up (fresh state after)
+    sampler = ClockSampler(local_rank).start() if (on_gpu and rank == 0) else None
     tim = {}
+    w0 = time.time()
     res = loop(SolverConfig(max_iters=args.steps, **zero), tim)
+    if sampler:
+        sampler.mark(w0, time.time())
+        sampler.stop()
     assert res.report.iter == args.steps and res.report.status == "max_iters", res.report
     ms = max_over_ranks(tim["loop_ms"])
     value = args.steps / (ms / 1000.0)
@@ -880,7 +885,13 @@ def run_strong(args, spec, rank, world, local_rank, group=None, factories=None, 
                                    "nvlink_bytes_per_rank_per_iteration": exchange_bytes(m, n, world, mode),
                                    "peak": peak, "peak_source": src},
             "time_to_tol": ttt, "e2e": e2e, "c5": c5,
+            "clocks": sampler.summary() if sampler else None,
         }
+        # per GPU over the whole sharded iteration (its passes and the exchange), device time
+        # max over ranks: the rank's share of the algorithmic bytes / the iteration time
+        ach = (row_b + col_b) / world / per_it / 1e9
+        line["roofline"] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                            "traffic": None, "kernel": f"whole {mode}-sharded iteration per GPU", "peak_source": src}
         print(json.dumps(line), flush=True)
     return 0
 
