@@ -338,7 +338,8 @@ _BATCH_SMEM_LIMIT = 227 * 1024
 
 
 def _batch_smem(m: int, n: int, o: int, k: int) -> int:
-    return 8 * (2 * o + 7 * m + 7 * n + 32) + 4 * (2 * o + m + 1 + n + 1 + k + 1) + 16
+    # + the length-ranked row and column orders (CF_BATCH_RANK)
+    return 8 * (2 * o + 7 * m + 7 * n + 32) + 4 * (2 * o + m + 1 + n + 1 + k + 1 + m + n) + 16
 
 
 def solve_batch(problems, cfg: SolverConfig | None = None, trace: bool = True, timing: dict | None = None,

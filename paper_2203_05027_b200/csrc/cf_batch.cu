@@ -160,6 +160,9 @@ __device__ __forceinline__ void project_block_b(const double* w, int q, double* 
     }
 }
 
+#ifndef CF_BATCH_RANK
+#define CF_BATCH_RANK 1  // LP problems relabelled by row/column length (less divergence in the dot loops)
+#endif
 #ifndef CF_BATCH_SEG
 #define CF_BATCH_SEG 0   // 0: seg_dot (unrolled by 4); N: seg_dot_pf<N>
 #endif
@@ -198,6 +201,10 @@ __global__ void __launch_bounds__(kBT, CF_BATCH_MINB) k_batch(const BatchArgs a)
     int32_t* rowptr = rowidx + CO;
     int32_t* colptr = rowptr + CM + 1;
     int32_t* cptr = colptr + CN + 1;   // cone offsets (local), cap_k + 1
+#if CF_BATCH_RANK
+    int32_t* cperm = cptr + a.cap_k + 1;   // columns by length, longest first (cap_n)
+    int32_t* rperm = cperm + CN;           // rows by length, longest first (cap_m)
+#endif
     __shared__ int32_t s_prob, s_status;
     const int t = threadIdx.x;
 
@@ -214,29 +221,110 @@ __global__ void __launch_bounds__(kBT, CF_BATCH_MINB) k_batch(const BatchArgs a)
         const double mu = cfg.mu;
         const MuDivB div = make_mudiv_b(mu);
         // ---- load the problem (canonical CSC, CSR, vectors) and a cold start (solver.py:309)
-        for (int i = t; i <= m; i += kBT) rowptr[i] = (int32_t)(a.rowptr[r0 + i] - kr0);
-        for (int j = t; j <= n; j += kBT) colptr[j] = (int32_t)(a.colptr[c0 + j] - kc0);
         CF_DASSERT(m >= 0 && n >= 0 && o >= 0 && m <= a.cap_m && n <= a.cap_n && o <= a.cap_o);
-        for (int k = t; k < o; k += kBT) {
-            colidx[k] = (int32_t)(a.colidx[kr0 + k] - c0);
-            valr[k] = a.valr[kr0 + k];
-            rowidx[k] = (int32_t)(a.rowidx[kc0 + k] - r0);
-            valc[k] = a.valc[kc0 + k];
-            CF_DASSERT(colidx[k] >= 0 && colidx[k] < n && rowidx[k] >= 0 && rowidx[k] < m);
+#if CF_BATCH_RANK
+        // LP problems are relabelled: rows and columns in order of decreasing length (ties by
+        // index), so the lanes of a warp run dot loops of similar lengths (a warp costs its
+        // longest lane) and the epilogues stay contiguous in shared memory. Only labels
+        // change: every row and column keeps its entries in canonical order, so each sum is
+        // the same sequence of operations and the iterates are unchanged (the report's
+        // cross-thread sums associate differently: rounding only). Cone problems keep
+        // their natural order (a cone is a contiguous column range).
+        const bool ranked = !a.cones;
+        if (ranked) {
+            int32_t* crank = reinterpret_cast<int32_t*>(wv);   // scratch during the load (cap_n)
+            int32_t* rrank = reinterpret_cast<int32_t*>(ax);   // (cap_m)
+            for (int j = t; j < n; j += kBT) {
+                const int64_t lj = a.colptr[c0 + j + 1] - a.colptr[c0 + j];
+                int r = 0;
+                for (int q = 0; q < n; ++q) {
+                    const int64_t lq = a.colptr[c0 + q + 1] - a.colptr[c0 + q];
+                    r += (lq > lj) || (lq == lj && q < j);
+                }
+                crank[j] = r;
+                cperm[r] = j;
+            }
+            for (int i = t; i < m; i += kBT) {
+                const int64_t li = a.rowptr[r0 + i + 1] - a.rowptr[r0 + i];
+                int r = 0;
+                for (int q = 0; q < m; ++q) {
+                    const int64_t lq = a.rowptr[r0 + q + 1] - a.rowptr[r0 + q];
+                    r += (lq > li) || (lq == li && q < i);
+                }
+                rrank[i] = r;
+                rperm[r] = i;
+            }
+            __syncthreads();
+            if (t == 0) {   // pointers in rank order
+                colptr[0] = 0;
+                for (int r = 0; r < n; ++r)
+                    colptr[r + 1] = colptr[r] + (int32_t)(a.colptr[c0 + cperm[r] + 1] - a.colptr[c0 + cperm[r]]);
+            } else if (t == 32) {
+                rowptr[0] = 0;
+                for (int r = 0; r < m; ++r)
+                    rowptr[r + 1] = rowptr[r] + (int32_t)(a.rowptr[r0 + rperm[r] + 1] - a.rowptr[r0 + rperm[r]]);
+            }
+            __syncthreads();
+            for (int r = t; r < n; r += kBT) {   // column r = natural column cperm[r], entries in order
+                const int64_t g0 = a.colptr[c0 + cperm[r]];
+                const int d0 = colptr[r], len = colptr[r + 1] - d0;
+                for (int e = 0; e < len; ++e) {
+                    rowidx[d0 + e] = rrank[a.rowidx[g0 + e] - r0];
+                    valc[d0 + e] = a.valc[g0 + e];
+                }
+            }
+            for (int r = t; r < m; r += kBT) {   // row r = natural row rperm[r]
+                const int64_t g0 = a.rowptr[r0 + rperm[r]];
+                const int d0 = rowptr[r], len = rowptr[r + 1] - d0;
+                for (int e = 0; e < len; ++e) {
+                    colidx[d0 + e] = crank[a.colidx[g0 + e] - c0];
+                    valr[d0 + e] = a.valr[g0 + e];
+                }
+            }
+            for (int r = t; r < m; r += kBT) {
+                const int i = rperm[r];
+                b[r] = a.b[r0 + i];
+                fu[r] = a.fu[r0 + i];
+                db[r] = a.db[r0 + i];
+            }
+            for (int r = t; r < n; r += kBT) {
+                const int j = cperm[r];
+                const double cj = a.c[c0 + j];
+                c[r] = cj;
+                cmu[r] = div(cj);
+                fvs[r] = 1.0 / (1.0 + (double)(a.colptr[c0 + j + 1] - a.colptr[c0 + j]));
+            }
+            __syncthreads();   // crank / rrank (in wv / ax) are read above
+        } else
+#endif
+        {
+            for (int i = t; i <= m; i += kBT) rowptr[i] = (int32_t)(a.rowptr[r0 + i] - kr0);
+            for (int j = t; j <= n; j += kBT) colptr[j] = (int32_t)(a.colptr[c0 + j] - kc0);
+            for (int k = t; k < o; k += kBT) {
+                colidx[k] = (int32_t)(a.colidx[kr0 + k] - c0);
+                valr[k] = a.valr[kr0 + k];
+                rowidx[k] = (int32_t)(a.rowidx[kc0 + k] - r0);
+                valc[k] = a.valc[kc0 + k];
+            }
+            for (int i = t; i < m; i += kBT) {
+                b[i] = a.b[r0 + i];
+                fu[i] = a.fu[r0 + i];
+                db[i] = a.db[r0 + i];
+            }
+            for (int j = t; j < n; j += kBT) {
+                const double cj = a.c[c0 + j];
+                c[j] = cj;
+                cmu[j] = div(cj);
+                fvs[j] = 1.0 / (1.0 + (double)(a.colptr[c0 + j + 1] - a.colptr[c0 + j]));
+            }
         }
+        for (int k = t; k < o; k += kBT) CF_DASSERT(colidx[k] >= 0 && colidx[k] < n && rowidx[k] >= 0 && rowidx[k] < m);
         for (int i = t; i < m; i += kBT) {
-            b[i] = a.b[r0 + i];
-            fu[i] = a.fu[r0 + i];
-            db[i] = a.db[r0 + i];
             lam[i] = 0.0;
             h[i] = 0.0;
             br[i] = 0.0;
         }
         for (int j = t; j < n; j += kBT) {
-            const double cj = a.c[c0 + j];
-            c[j] = cj;
-            cmu[j] = div(cj);
-            fvs[j] = 1.0 / (1.0 + (double)(a.colptr[c0 + j + 1] - a.colptr[c0 + j]));
             x[j] = 0.0;
             z[j] = 0.0;
             dl[j] = 0.0;
@@ -359,8 +447,16 @@ __global__ void __launch_bounds__(kBT, CF_BATCH_MINB) k_batch(const BatchArgs a)
             if (s_status != CF_STATUS_RUNNING) break;
         }
         // ---- SolveResult (solver.py:329-334)
-        for (int j = t; j < n; j += kBT) a.x_out[c0 + j] = x[j];
-        for (int i = t; i < m; i += kBT) a.lam_out[r0 + i] = lam[i];
+#if CF_BATCH_RANK
+        if (ranked) {
+            for (int r = t; r < n; r += kBT) a.x_out[c0 + cperm[r]] = x[r];
+            for (int r = t; r < m; r += kBT) a.lam_out[r0 + rperm[r]] = lam[r];
+        } else
+#endif
+        {
+            for (int j = t; j < n; j += kBT) a.x_out[c0 + j] = x[j];
+            for (int i = t; i < m; i += kBT) a.lam_out[r0 + i] = lam[i];
+        }
         if (t == 0) {
             a.final_report[pid] = last;
             a.n_reports[pid] = nrep;
@@ -371,7 +467,7 @@ __global__ void __launch_bounds__(kBT, CF_BATCH_MINB) k_batch(const BatchArgs a)
 
 size_t batch_smem(int cm, int cn, int co, int ck) {
     return sizeof(double) * (size_t)(2 * co + 7 * cm + 7 * cn + 32) +
-           sizeof(int32_t) * (size_t)(2 * co + cm + 1 + cn + 1 + ck + 1) + 16;
+           sizeof(int32_t) * ((size_t)2 * co + cm + 1 + cn + 1 + ck + 1 + (CF_BATCH_RANK ? (size_t)cn + cm : 0)) + 16;
 }
 
 }  // namespace
