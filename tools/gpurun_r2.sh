@@ -1,7 +1,6 @@
-for lib in base s4 s2 m5 t128 base s4 s2 m5 t128; do
-  if [ "$lib" = base ]; then path=""; else path="paper_2203_05027_b200/libcfb200_$lib.so"; fi
-  CF_LIB_PATH=$path timeout 300 python bench.py --config c4 --skip-cpu 2>/dev/null | python -c "
-import json,sys
-d=json.loads(sys.stdin.read().strip().splitlines()[-1])
-print('$lib', '%.1f M problem-it/s' % (d['value']/1e6))"
-done
+# launch list of the bench command (cold-cache serialised times: the share of the step is what counts)
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r02b_launches.csv python bench.py --steps 20 --warmup 5 --warm-seconds 0 --skip-e2e --skip-ttt --skip-cpu > gpurun_out/r02b_launch_bench.log 2>&1
+echo launch rc=$?
+# one full capture of the passes (row panel 1, row panel 2, column pass) of the bench iteration
+timeout 1200 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"RowIter|ColIter" -c 3 -o gpurun_out/r02b_c2_full -f python tools/prof_iter.py --config c2 --iters 2 > gpurun_out/r02b_full.log 2>&1
+echo full rc=$?
