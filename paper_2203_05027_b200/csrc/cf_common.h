@@ -169,6 +169,7 @@ struct cf_plan {
 
     // problem vectors and cached diagonals (fu_diag uv.py:81; d*b for the row pass)
     cf::DevBuf<double> b, c, fu, db, amax;
+    cf::DevBuf<double> dn;   // row norms d_i (the row pass recomputes fu and d b from d and b)
 
     // cones (cones.py:39-59) and column tiling
     bool all_unit = true;

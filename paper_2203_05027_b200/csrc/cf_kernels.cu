@@ -117,8 +117,9 @@ struct RowIter : Layout {
     bool has_carry;        // panel > 0: the sum continues from carry[i]
     double* carry_buf;     // partial A x between panels (= the plan's ax buffer)
     const double* b;
-    const double* fu;
-    const double* db;
+    const double* dn;      // d_i = sum_k a_ik^2: fu = 1/(1+d) and d b are recomputed (the same
+                           // IEEE operations as k_row_diag's, so the same bits; one vector
+                           // streamed instead of two)
     double* lam;
     double* h;
     double* br;            // optional: b - r
@@ -126,7 +127,7 @@ struct RowIter : Layout {
     const double* rcorr;   // optional: warm-start U eps / mu
     double mu;
     pass::MuDiv div;
-    static constexpr int kVals = 4;   // b, lam, fu, d*b (last panel only)
+    static constexpr int kVals = 3;   // b, lam, d (last panel only)
     __device__ __forceinline__ bool carry_in() const { return has_carry; }
     __device__ __forceinline__ double carry(int s) const {
         return pass::ld_first(carry_buf + (s - seg_off), pass::pol_first());
@@ -137,8 +138,7 @@ struct RowIter : Layout {
         const int64_t i = s - seg_off;
         pass::cp_async8(slot, b + i, pf);
         pass::cp_async8(slot + 32, lam + i, pf);
-        pass::cp_async8(slot + 64, fu + i, pf);
-        pass::cp_async8(slot + 96, db + i, pf);
+        pass::cp_async8(slot + 64, dn + i, pf);
     }
     __device__ __forceinline__ void segment(Smem&, int, int s0, int q, int, double axi, const Vals& v) {
         const int64_t i = s0 + q - seg_off;
@@ -146,7 +146,8 @@ struct RowIter : Layout {
             carry_buf[i] = axi;
             return;
         }
-        const double bi = v.v[0], li = v.v[1], fui = v.v[2], dbi = v.v[3];
+        const double bi = v.v[0], li = v.v[1], di = v.v[2];
+        const double fui = 1.0 / (1.0 + di), dbi = di * bi;   // k_row_diag (uv.py:81)
         double si = dbi + axi;                  // (U t)_i with t = a b + x
         if (rcorr) si = si - rcorr[i];
         const double r = fui * si;              // r = U y+ = fu (U t)
@@ -584,7 +585,7 @@ __global__ void k_warm_rows(const int32_t* rowptr, const double* valr, const int
 // also amax_i = max_k |a_k| of row i: a_k*v is finite for every k of row i iff amax_i*v is
 // (the report's exact row-level test of the implicit y and gamma, solver.py:208-211)
 __global__ void k_row_diag(const int32_t* rowptr, const double* valr, const double* b, double* fu, double* db,
-                           double* amax, int64_t m, int32_t panels) {
+                           double* amax, double* dn, int64_t m, int32_t panels) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
         double d = 0.0, am = 0.0;
         for (int32_t pn = 0; pn < panels; ++pn) {
@@ -597,6 +598,7 @@ __global__ void k_row_diag(const int32_t* rowptr, const double* valr, const doub
         fu[i] = 1.0 / (1.0 + d);
         db[i] = d * b[i];
         amax[i] = am;
+        dn[i] = d;
     }
 }
 
@@ -618,12 +620,13 @@ __global__ void k_row_norms(const int32_t* rowptr, const double* valr, double* d
 }
 // fu = 1/(1+d) (uv.py:81), d*b and amax from given (e.g. all-reduced) row norms
 __global__ void k_set_row_diag(const double* din, const double* amax_in, const double* b, double* fu, double* db,
-                               double* amax, int64_t m) {
+                               double* amax, double* dn, int64_t m) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
         const double d = din[i];
         fu[i] = 1.0 / (1.0 + d);
         db[i] = d * b[i];
         amax[i] = amax_in[i];
+        dn[i] = d;
     }
 }
 
@@ -892,8 +895,7 @@ int launch_row_only(cf_plan* p, const IterOpts& opt, const int32_t* done, int64_
         r.has_carry = pn > 0;
         r.carry_buf = p->ax.p;
         r.b = p->b.p;
-        r.fu = p->fu.p;
-        r.db = p->db.p;
+        r.dn = p->dn.p;
         r.lam = p->lam.p;
         r.h = p->h.p;
         r.mu = opt.mu;
@@ -1132,7 +1134,7 @@ int launch_warm_start(cf_plan* p, double mu) {
 int launch_row_diag(cf_plan* p) {
     if (p->m == 0) return CF_OK;
     k_row_diag<<<grid_for(p->m, 128), 128, 0, p->stream>>>(p->rowptr.p, p->valr.p, p->b.p, p->fu.p, p->db.p,
-                                                          p->amax.p, p->m, p->n_panels);
+                                                          p->amax.p, p->dn.p, p->m, p->n_panels);
     CF_LAUNCHED();
     return CF_OK;
 }
@@ -1147,7 +1149,7 @@ int launch_row_norms(cf_plan* p, double* dout, double* amax) {
 int launch_set_row_diag(cf_plan* p, const double* din, const double* amax_in) {
     if (p->m == 0) return CF_OK;
     k_set_row_diag<<<grid_for(p->m, 128), 128, 0, p->stream>>>(din, amax_in, p->b.p, p->fu.p, p->db.p, p->amax.p,
-                                                                p->m);
+                                                                p->dn.p, p->m);
     CF_LAUNCHED();
     return CF_OK;
 }

@@ -745,6 +745,7 @@ int build(cf_plan* p, const int64_t* rows, const int64_t* cols, const double* va
     CF_TRY(p->fu.alloc(m));
     CF_TRY(p->db.alloc(m));
     CF_TRY(p->amax.alloc(m));
+    CF_TRY(p->dn.alloc(m));
     CF_TRY(launch_row_diag(p));
 
     // ---- cones (cones.py:39-59) and tiles
