@@ -100,6 +100,7 @@ struct Layout {
     __device__ __forceinline__ const double* gvec() const { return g_; }
     static constexpr int kVals = 0;
     __device__ __forceinline__ void load_async(int, double*) const {}
+    __device__ __forceinline__ void load_direct(int, Vals&) const {}
     __device__ __forceinline__ bool carry_in() const { return false; }
     __device__ __forceinline__ double carry(int) const { return 0.0; }
     __device__ __forceinline__ void check(double, int, double) {}
@@ -139,6 +140,14 @@ struct RowIter : Layout {
         pass::cp_async8(slot, b + i, pf);
         pass::cp_async8(slot + 32, lam + i, pf);
         pass::cp_async8(slot + 64, dn + i, pf);
+    }
+    __device__ __forceinline__ void load_direct(int s, Vals& v) const {
+        if (!last) return;
+        const uint64_t pf = pass::pol_first();
+        const int64_t i = s - seg_off;
+        v.v[0] = pass::ld_first(b + i, pf);
+        v.v[1] = pass::ld_first(lam + i, pf);
+        v.v[2] = pass::ld_first(dn + i, pf);
     }
     __device__ __forceinline__ void segment(Smem&, int, int s0, int q, int, double axi, const Vals& v) {
         const int64_t i = s0 + q - seg_off;
@@ -211,6 +220,15 @@ struct ColVecs : Layout {
         pass::cp_async8(slot + 32, z_in + j, pf);
         pass::cp_async8(slot + 64, d_in + j, pf);
         pass::cp_async8(slot + 96, c + j, pf);
+    }
+    __device__ __forceinline__ void load_direct(int s, Vals& v) const {
+        if (!last) return;
+        const uint64_t pf = pass::pol_first();
+        const int64_t j = s - seg_off;
+        v.v[0] = pass::ld_first(x_in + j, pf);
+        v.v[1] = pass::ld_first(z_in + j, pf);
+        v.v[2] = pass::ld_first(d_in + j, pf);
+        v.v[3] = pass::ld_first(c + j, pf);
     }
     // a band before the last only hands its partial sum on
     __device__ __forceinline__ bool carry_out(int64_t j, double acc) const {

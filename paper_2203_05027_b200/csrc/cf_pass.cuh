@@ -70,6 +70,9 @@ namespace pass {
 #ifndef CF_TAIL_UNROLL
 #define CF_TAIL_UNROLL 0           // diagonals per batch on the narrow part (0: the policy's kUnroll)
 #endif
+#ifndef CF_EPI_DIRECT
+#define CF_EPI_DIRECT 1            // deferred flow: epilogue vectors loaded straight into registers at the epilogue (+1 %; 0: cp.async at hand-in)
+#endif
 #ifndef CF_BULK_PREFETCH
 #define CF_BULK_PREFETCH 0         // L2-prefetch the idx/val/pl of the tile this many rounds ahead (measured slower)
 #endif
@@ -572,11 +575,15 @@ __global__ void __launch_bounds__(kPThreads, P::kMinBlocks) k_pass(const P p0, c
         mbar_wait(&sm.full[b], (uint32_t)(((seq - 1) / 3) & 1));
         if (pv_nb > 0) {
             Vals vv{};
+#if CF_EPI_DIRECT
+            if (P::kVals > 0 && lane < pv_nb) p.load_direct(pv_s0 + gw * 32 + lane, vv);
+#else
             if (P::kVals > 0) {
                 cp_async_wait_all();
 #pragma unroll
                 for (int f = 0; f < P::kVals; ++f) vv.v[f] = slot[32 * f];
             }
+#endif
             __syncwarp();
             if (lane < pv_nb)
                 p.segment(sm, pv_tile, pv_s0, gw * 32 + lane, wcnt_buf(sm, b)[gw * 32 + lane],
@@ -616,7 +623,7 @@ __global__ void __launch_bounds__(kPThreads, P::kMinBlocks) k_pass(const P p0, c
             const int b = seq % 3;
             if (nbw > 0) block_sums(p, L, nullptr, nullptr, s0, kj, bw, lane, nbw, pr, wacc_buf(sm, b), wcnt_buf(sm, b));
             drain();                                  // the previous tile's epilogue
-            if (P::kVals > 0 && nb > 0) {
+            if (!CF_EPI_DIRECT && P::kVals > 0 && nb > 0) {
                 if (lane < nb) p.load_async(s0 + gw * 32 + lane, slot);   // this tile's epilogue vectors
                 cp_async_commit();
             }

@@ -3,6 +3,7 @@ row passes only, each for a few seconds with nvidia-smi sampled meanwhile.
 
     python tools/power_split.py [seconds]
 """
+import ctypes
 import os
 import statistics
 import subprocess
@@ -63,9 +64,20 @@ def main():
             _lib.check(lib.cf_plan_row_step(h, 1.0, 0))
         return 200
 
+    import torch as _t
+
+    hv = _t.zeros(inst.m, dtype=_t.float64, device="cuda")
+    xv = _t.zeros(inst.n, dtype=_t.float64, device="cuda")
+
+    def spmv_t():   # A^T h alone: the column pass's sums without its epilogue
+        for _ in range(200):
+            _lib.check(lib.cf_apply_At_async(h, ctypes.c_void_p(hv.data_ptr()), ctypes.c_void_p(xv.data_ptr())))
+        return 200
+
     full()
     torch.cuda.synchronize()
-    for name, fn in (("iteration", full), ("column pass", col), ("row pass", row), ("iteration", full)):
+    for name, fn in (("iteration", full), ("column pass", col), ("A^T h only", spmv_t), ("row pass", row),
+                     ("iteration", full)):
         ms, clk, pw, pmax = sample(fn, secs)
         print(f"{name:12s} {ms:.4f} ms  sm clock median {clk:.0f} MHz  power median {pw:.0f} W (max {pmax:.0f})",
               flush=True)
