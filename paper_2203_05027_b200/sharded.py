@@ -888,69 +888,72 @@ def run_col_sharded(be, col_cuts, cfg, b_norms, c_norms, group=None, timing=None
                 lam_pad.copy_(torch.cat(parts))
             be.set_lam(lam_pad[:m])
     trace = []
-    if timing is not None and be.device.type == "cuda":
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-    for k in range(1, cfg.max_iters + 1):
-        be.col_step(cfg.mu)
-        report = (k % cfg.check_every == 0) or (k == cfg.max_iters)
-        if shard_rows:
-            be.ax_into(ax_pad)
-            if nccl:   # in place: this rank's block of the sum lands at its own offset
-                dist.reduce_scatter_tensor(ax_mine, ax_pad, op=dist.ReduceOp.SUM, group=group)
+    try:   # h stays bound to h_pad only inside the loop (an exception must not leave the plan on it)
+        if timing is not None and be.device.type == "cuda":
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+        for k in range(1, cfg.max_iters + 1):
+            be.col_step(cfg.mu)
+            report = (k % cfg.check_every == 0) or (k == cfg.max_iters)
+            if shard_rows:
+                be.ax_into(ax_pad)
+                if nccl:   # in place: this rank's block of the sum lands at its own offset
+                    dist.reduce_scatter_tensor(ax_mine, ax_pad, op=dist.ReduceOp.SUM, group=group)
+                else:
+                    dist.all_reduce(ax_pad, op=dist.ReduceOp.SUM, group=group)
+                ax_slice = ax_mine[:r1 - r0]
+                be.row_update_range(cfg.mu, report, r0, r1, ax_slice)   # writes h_pad[r0:r1]
+                if nccl:
+                    dist.all_gather_into_tensor(h_pad[:world * S], h_mine, group=group)
+                else:
+                    parts = [torch.empty(S, dtype=torch.float64) for _ in range(world)]
+                    dist.all_gather(parts, h_mine.clone(), group=group)
+                    h_pad[:world * S].copy_(torch.cat(parts))
             else:
-                dist.all_reduce(ax_pad, op=dist.ReduceOp.SUM, group=group)
-            ax_slice = ax_mine[:r1 - r0]
-            be.row_update_range(cfg.mu, report, r0, r1, ax_slice)   # writes h_pad[r0:r1]
-            if nccl:
-                dist.all_gather_into_tensor(h_pad[:world * S], h_mine, group=group)
+                ax = be.partial_Ax()
+                dist.all_reduce(ax, op=dist.ReduceOp.SUM, group=group)
+                be.row_update(cfg.mu, report)
+            if not report:
+                continue
+            if shard_rows:
+                rpl = torch.as_tensor(be.row_parts_range(r0, r1, ax_slice), dtype=torch.float64, device=be.device)
+                gather_lam()   # A^T lam below needs every row's lam
             else:
-                parts = [torch.empty(S, dtype=torch.float64) for _ in range(world)]
-                dist.all_gather(parts, h_mine.clone(), group=group)
-                h_pad[:world * S].copy_(torch.cat(parts))
-        else:
-            ax = be.partial_Ax()
-            dist.all_reduce(ax, op=dist.ReduceOp.SUM, group=group)
-            be.row_update(cfg.mu, report)
-        if not report:
-            continue
+                rpl = None
+                rp = be.row_parts()          # full rows: the same on every rank
+            cp = torch.as_tensor(be.col_parts(), dtype=torch.float64, device=be.device)
+            if shard_rows:   # row parts: {sum prim^2, max|prim|, max|Ax|, sum b.lam, nonfinite} over the blocks
+                sums = torch.stack([cp[0], cp[2], cp[5], rpl[0], rpl[3]])
+                maxs = torch.stack([cp[1], cp[3], cp[4], cp[6], cp[7], rpl[1], rpl[2], rpl[4]])
+            else:
+                sums = torch.stack([cp[0], cp[2], cp[5]])
+                maxs = torch.stack([cp[1], cp[3], cp[4], cp[6], cp[7]])
+            nan = torch.isnan(maxs).to(torch.float64)
+            dist.all_reduce(sums, op=dist.ReduceOp.SUM, group=group)
+            dist.all_reduce(maxs, op=dist.ReduceOp.MAX, group=group)
+            dist.all_reduce(nan, op=dist.ReduceOp.MAX, group=group)
+            maxs = torch.where(nan > 0, torch.full_like(maxs, float("nan")), maxs)
+            s, mx = sums.tolist(), maxs.tolist()
+            if shard_rows:
+                rp = [s[3], mx[5], mx[6], s[4], mx[7]]
+            f = [rp[0], rp[1], rp[2], rp[3], rp[4], s[0], mx[0], s[1], mx[1], mx[2], s[2], mx[3], mx[4]]
+            rep = assemble_report(k, f)
+            status = _decide(rep, cfg, b_norms, c_norms)
+            if status == "running" and k == cfg.max_iters:
+                status = "max_iters"
+            trace.append(replace(rep, status=status))
+            if status != "running":
+                break
+        if timing is not None and be.device.type == "cuda":
+            e1.record()
+            e1.synchronize()
+            timing["loop_ms"] = e0.elapsed_time(e1)
+            timing["iters"] = trace[-1].iter
         if shard_rows:
-            rpl = torch.as_tensor(be.row_parts_range(r0, r1, ax_slice), dtype=torch.float64, device=be.device)
-            gather_lam()   # A^T lam below needs every row's lam
-        else:
-            rpl = None
-            rp = be.row_parts()          # full rows: the same on every rank
-        cp = torch.as_tensor(be.col_parts(), dtype=torch.float64, device=be.device)
-        if shard_rows:   # row parts: {sum prim^2, max|prim|, max|Ax|, sum b.lam, nonfinite} over the blocks
-            sums = torch.stack([cp[0], cp[2], cp[5], rpl[0], rpl[3]])
-            maxs = torch.stack([cp[1], cp[3], cp[4], cp[6], cp[7], rpl[1], rpl[2], rpl[4]])
-        else:
-            sums = torch.stack([cp[0], cp[2], cp[5]])
-            maxs = torch.stack([cp[1], cp[3], cp[4], cp[6], cp[7]])
-        nan = torch.isnan(maxs).to(torch.float64)
-        dist.all_reduce(sums, op=dist.ReduceOp.SUM, group=group)
-        dist.all_reduce(maxs, op=dist.ReduceOp.MAX, group=group)
-        dist.all_reduce(nan, op=dist.ReduceOp.MAX, group=group)
-        maxs = torch.where(nan > 0, torch.full_like(maxs, float("nan")), maxs)
-        s, mx = sums.tolist(), maxs.tolist()
+            gather_lam()
+    finally:
         if shard_rows:
-            rp = [s[3], mx[5], mx[6], s[4], mx[7]]
-        f = [rp[0], rp[1], rp[2], rp[3], rp[4], s[0], mx[0], s[1], mx[1], mx[2], s[2], mx[3], mx[4]]
-        rep = assemble_report(k, f)
-        status = _decide(rep, cfg, b_norms, c_norms)
-        if status == "running" and k == cfg.max_iters:
-            status = "max_iters"
-        trace.append(replace(rep, status=status))
-        if status != "running":
-            break
-    if timing is not None and be.device.type == "cuda":
-        e1.record()
-        e1.synchronize()
-        timing["loop_ms"] = e0.elapsed_time(e1)
-        timing["iters"] = trace[-1].iter
-    if shard_rows:
-        gather_lam()
-        be.bind_h(None)
+            be.bind_h(None)
     if not gather_result:
         return SolveResult(x=None, lam=None, report=trace[-1], trace=tuple(trace))
     S = max(col_cuts[r + 1] - col_cuts[r] for r in range(world))
