@@ -41,7 +41,7 @@ namespace cf {
 namespace pass {
 
 #ifndef CF_UNROLL
-#define CF_UNROLL 3
+#define CF_UNROLL 4
 #endif
 #ifndef CF_MINB
 #define CF_MINB 5                  // resident CTAs per SM the registers are sized for (6 spills with the deferred pipeline)
