@@ -255,7 +255,7 @@ _CLUSTER_TRACE_MAX = 1 << 16   # cf_batch.cu kMaxClusterTrace
 _LAST_CLUSTER = 0   # cluster size of the last cf_cluster_solve call (0: did not fit), for tests
 
 _PLAN_KNOBS = ("CF_PANEL_MB", "CF_BAND_MB", "CF_FORCE_LARGE_TILES", "CF_NO_LARGE_TILES", "CF_GROUP_CONES",
-               "CF_LIB_PATH")
+               "CF_NO_COL_RUNS", "CF_LIB_PATH")
 
 
 def _cluster_candidate(p) -> bool:

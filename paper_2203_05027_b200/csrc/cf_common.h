@@ -203,6 +203,14 @@ struct cf_plan {
     int32_t n_bands = 1;
     int64_t band_rows = 0;
     std::vector<int64_t> col_band_tile;    // first column tile of each band (n_bands+1)
+    // mixed cone sizes in runs (e.g. K4 blocks then an orthant): the column pass launches
+    // each run of tiles with its own epilogue (1: orthant, 2..32: warp cones of that size,
+    // 0: the shared-memory group epilogue); empty = one launch per band
+    struct ColRun {
+        int64_t t0, t1;
+        int32_t cls;
+    };
+    std::vector<ColRun> col_runs;
     cf::DevBuf<double> atcarry;            // partial A^T h / A^T lam between bands (n)
     // banded CSC, only while the column JDS is built (released afterwards)
     cf::DevBuf<int32_t> bcolptr, browidx;

@@ -967,10 +967,39 @@ int launch_iteration(cf_plan* p, const IterOpts& opt, const int32_t* done, int64
     return CF_OK;
 }
 
+// one launch per run of tiles with one cone size (cf_plan::col_runs; a single band)
+int launch_col_runs(cf_plan* p, const IterOpts& opt, const int32_t* done, int64_t* nl) {
+    for (const auto& r : p->col_runs) {
+        const pass::Tiles T{p->col_tb.p + r.t0, (int32_t)(r.t1 - r.t0), stageable(p->col_unpacked, r.t0, r.t1)};
+        auto run = [&](auto c) {
+            c.seg_off = 0;
+            c.last = true;
+            c.has_carry = false;
+            return launch_pass(c, col_jds(p), T, done, p->stream, nullptr, col_avg_len(p));
+        };
+        if (r.cls == 1) {
+            CF_TRY(run(col_iter<kLP>(p, opt)));
+        } else if (r.cls > 1) {
+            auto c = col_iter<kWarpCones>(p, opt);
+            c.cs = r.cls;
+            CF_TRY(run(c));
+        } else {
+            auto c = col_iter<kGroupCones>(p, opt);
+            c.tile_cone += r.t0;   // the kernel indexes them by tile within the launch
+            c.tile_big += r.t0;
+            CF_TRY(run(c));
+        }
+        ++*nl;
+    }
+    return CF_OK;
+}
+
 int launch_col_only(cf_plan* p, const IterOpts& opt, const int32_t* done, int64_t* launches) {
     int64_t nl = 0;
     if (p->n > 0) {
-        if (p->all_unit) {
+        if (!p->col_runs.empty()) {
+            CF_TRY(launch_col_runs(p, opt, done, &nl));
+        } else if (p->all_unit) {
             CF_TRY(launch_col_bands(p, col_iter<kLP>(p, opt), done, &nl));
         } else if (p->warp_cone) {
             CF_TRY(launch_col_bands(p, col_iter<kWarpCones>(p, opt), done, &nl));

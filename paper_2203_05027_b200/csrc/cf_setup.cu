@@ -498,7 +498,35 @@ int build_tiles(cf_plan* p, const int64_t* sizes, int64_t nb) {
         for (int pn = 0; pn < p->n_panels; ++pn)
             if (p->row_panel_tile[pn + 1] - p->row_panel_tile[pn] <= kStagedMaxTiles)
                 block_rank(rtb, p->row_panel_tile[pn], p->row_panel_tile[pn + 1]);
-    if (!p->all_unit && p->warp_cone == 0) {
+    // Cones of mixed sizes that come in runs (the robust-LS shape: K4 blocks, then an
+    // orthant): a large pass launches each run of tiles whose cones all have one size with
+    // the fused per-column (size 1) or warp-shuffle (2..32) epilogue, tile-ranked, and only
+    // the tiles that mix sizes with the group epilogue (block-ranked, CTA barrier).
+    p->col_runs.clear();
+    if (!p->all_unit && p->warp_cone == 0 && p->n_big == 0 && B == 1 && nb > 0 && !getenv("CF_GROUP_CONES") &&
+        !getenv("CF_NO_COL_RUNS") && p->col_tiles > kStagedMaxTiles && (int64_t)tcone.size() == p->col_tiles + 1) {
+        std::vector<cf_plan::ColRun> runs;
+        for (int64_t t = 0; t < p->col_tiles; ++t) {
+            const int64_t q0 = tcone[t], q1 = tcone[t + 1];
+            const int64_t s = sizes[q0];
+            bool uniform = q1 > q0;
+            for (int64_t q = q0 + 1; q < q1 && uniform; ++q) uniform = sizes[q] == s;
+            const int32_t cls = !uniform ? 0 : (s == 1 ? 1 : ((s <= 32 && (s & (s - 1)) == 0) ? (int32_t)s : 0));
+            if (!runs.empty() && runs.back().cls == cls)
+                runs.back().t1 = t + 1;
+            else
+                runs.push_back({t, t + 1, cls});
+        }
+        int64_t fused = 0;
+        for (const auto& r : runs)
+            if (r.cls) fused += r.t1 - r.t0;
+        // worth it when most tiles leave the barrier flow, in a few launches
+        if (runs.size() <= 8 && 2 * fused >= p->col_tiles) p->col_runs = runs;
+    }
+    if (!p->col_runs.empty()) {
+        for (const auto& r : p->col_runs)
+            if (r.cls == 0) block_rank(ctb, r.t0, r.t1);
+    } else if (!p->all_unit && p->warp_cone == 0) {
         block_rank(ctb, 0, (int64_t)ctb.size() - 1);
     } else if (!p->col_large_tiles) {
         for (int b = 0; b < B; ++b)

@@ -56,3 +56,37 @@ def test_rls_solve_matches_oracle():
     res = solve(p, cfg)
     assert res.report.iter == otr[-1]["iter"] and res.report.status == otr[-1]["status"] == "solved"
     assert rel_err(res.x, ox) <= 1e-8 and rel_err(res.lam, olam) <= 1e-8
+
+
+@pytest.mark.gpu
+def test_rls_column_runs_bit_identical(monkeypatch):
+    """A pass large enough to launch per run of one cone size (K4 tiles with the warp-shuffle
+    epilogue, orthant tiles fused, the one mixed tile with the group epilogue) gives the same
+    bits as the group epilogue on every tile (CF_NO_COL_RUNS=1), and matches the oracle."""
+    import oracle
+    from paper_2203_05027_b200.api import build_plan
+
+    p = _instance(120_000, seed=5)
+    f = oracle.build_factors(p.A)
+    st = oracle.OracleState.zeros(f)
+    st = oracle.iterate(f, p.cones.sizes_array(), st, 1.0, p.b, p.c, 3)
+
+    def run(env):
+        if env:
+            monkeypatch.setenv("CF_NO_COL_RUNS", "1")
+        else:
+            monkeypatch.delenv("CF_NO_COL_RUNS", raising=False)
+        with build_plan(p) as plan:
+            plan.set_state(1.0, None)
+            plan.iterate(1.0, 3)
+            s3 = plan.get_state()
+            plan.iterate(1.0, 27)
+            t = plan.last_timing()
+            return s3, plan.get_state(), t["launches"]
+
+    r3, r30, runs_launches = run(False)
+    g3, g30, group_launches = run(True)
+    assert runs_launches > group_launches      # the run dispatch was taken
+    for key in ("x", "y", "z", "lam", "gamma", "delta"):
+        np.testing.assert_array_equal(r30[key], g30[key])
+        assert rel_err(r3[key], getattr(st, key)) <= 1e-9, key
