@@ -90,3 +90,58 @@ def test_rls_column_runs_bit_identical(monkeypatch):
     for key in ("x", "y", "z", "lam", "gamma", "delta"):
         np.testing.assert_array_equal(r30[key], g30[key])
         assert rel_err(r3[key], getattr(st, key)) <= 1e-9, key
+
+
+def _cone_problem(sizes, m, per_col=8, seed=0):
+    """Random sparse problem (distinct cells, ~per_col entries per column) with the given cones."""
+    rng = np.random.default_rng(seed)
+    sizes = np.asarray(sizes, dtype=np.int64)
+    n = int(sizes.sum())
+    cols = np.repeat(np.arange(n, dtype=np.int64), per_col)
+    rows = rng.integers(0, m, size=cols.size, dtype=np.int64)
+    key = np.unique(cols * m + rows)
+    cols, rows = key // m, key % m
+    vals = rng.standard_normal(rows.size)
+    vals[vals == 0.0] = 1.0
+    return ProblemInstance(TripletMatrix(m, n, rows, cols, vals), rng.standard_normal(m), rng.standard_normal(n),
+                           ConeSpec(sizes))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("layout", ["runs", "interleaved"])
+def test_column_runs_other_sizes(monkeypatch, layout):
+    """Runs of K2, K8 and orthant cones (warp epilogues of sizes 2 and 8, fused orthant), and an
+    interleaved K4/K1 pattern (too many runs: the group epilogue on every tile): bit-identical
+    to CF_NO_COL_RUNS and to the oracle's first iterations."""
+    import oracle
+    from paper_2203_05027_b200.api import build_plan
+
+    if layout == "runs":
+        sizes = [2] * 100_000 + [8] * 25_000 + [1] * 120_000 + [8] * 20_000
+    else:
+        sizes = [4, 1, 1] * 80_000
+    p = _cone_problem(sizes, m=200_000, seed=7 if layout == "runs" else 8)
+    f = oracle.build_factors(p.A)
+    st = oracle.iterate(f, p.cones.sizes_array(), oracle.OracleState.zeros(f), 1.0, p.b, p.c, 3)
+
+    def run(no_runs):
+        if no_runs:
+            monkeypatch.setenv("CF_NO_COL_RUNS", "1")
+        else:
+            monkeypatch.delenv("CF_NO_COL_RUNS", raising=False)
+        with build_plan(p) as plan:
+            plan.set_state(1.0, None)
+            plan.iterate(1.0, 3)
+            s3 = plan.get_state()
+            plan.iterate(1.0, 17)
+            return s3, plan.get_state(), plan.last_timing()["launches"]
+
+    r3, r20, nl_runs = run(False)
+    _, g20, nl_group = run(True)
+    if layout == "runs":
+        assert nl_runs > nl_group
+    else:
+        assert nl_runs == nl_group             # too many runs: one launch per pass
+    for key in ("x", "y", "z", "lam", "gamma", "delta"):
+        np.testing.assert_array_equal(r20[key], g20[key])
+        assert rel_err(r3[key], getattr(st, key)) <= 1e-9, key

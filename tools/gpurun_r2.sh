@@ -1,14 +1,1 @@
-timeout 2400 python -m pytest tests -m gpu -q -x 2>&1 | tail -3 > gpurun_out/r02_final_gpu_tests.log
-python -c "import __graft_entry__ as g; g.smoke()" >> gpurun_out/r02_final_gpu_tests.log 2>&1; echo "smoke rc=$?" >> gpurun_out/r02_final_gpu_tests.log
-run() { name=$1; shift; timeout 1200 python bench.py "$@" > gpurun_out/final_$name.json 2> gpurun_out/final_$name.err; echo "$name rc=$?"; }
-run c2
-run ref_c2 --impl reference
-run c3 --config c3
-run ref_c3 --impl reference --config c3
-run c3m --config c3m
-run c4 --config c4
-run ref_c4 --impl reference --config c4
-run c1 --config c1
-run ref_c1 --impl reference --config c1
-run c5_full --config c5
-run strong_cols --strong --layout cols
+timeout 900 python -m pytest tests/test_rls.py -q -x -v 2>&1 | grep -E "PASS|FAIL|Error|error|passed|failed" | head -20
