@@ -652,9 +652,9 @@ int cf_plan_bind_x(cf_plan* p, double* x_ext) {
 
 int cf_column_parts(int64_t n, const double* atl, const double* c, const double* x, const double* z,
                     const double* delta, double* out8, void* stream) {
-    DevBuf<double> d;
-    CF_TRY(d.alloc(8));
-    CF_TRY(launch_col_parts(n, atl, c, x, z, delta, d.p, (cudaStream_t)stream));
+    DevBuf<double> d;   // the 8 results, then the per-CTA partials
+    CF_TRY(d.alloc(8 + 8 * (size_t)col_parts_ctas(n)));
+    CF_TRY(launch_col_parts(n, atl, c, x, z, delta, d.p, d.p + 8, (cudaStream_t)stream));
     CF_CUDA(cudaMemcpyAsync(out8, d.p, 8 * sizeof(double), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
     CF_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
     return CF_OK;

@@ -302,8 +302,9 @@ int launch_col_update(int64_t n, const double* ath, const double* cnt, const dou
 int launch_col_update_p2p(int64_t n, const double* const* parts, int world, const double* cnt, const double* c,
                           double* x, double* z, double* delta, double mu, int64_t n_blocks, const int32_t* cone_ptr,
                           double* const* x_dst, int n_dst, cudaStream_t st);
+int col_parts_ctas(int64_t n);   // CTAs of launch_col_parts (its work buffer: 8 doubles each)
 int launch_col_parts(int64_t n, const double* atl, const double* c, const double* x, const double* z,
-                     const double* delta, double* out8_dev, cudaStream_t st);
+                     const double* delta, double* out8_dev, double* work, cudaStream_t st);
 int launch_row_parts(cf_plan* p, double* out5_dev);
 int launch_counts(cf_plan* p, double* cnt);
 // profiling: reset before a loop, fold the recorded per-pass event times after its final sync

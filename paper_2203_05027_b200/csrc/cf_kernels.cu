@@ -1262,11 +1262,14 @@ __global__ void k_cone_update(int64_t n_blocks, const int32_t* cone_ptr, const d
         for (int u = 0; u < size; ++u) delta[off + u] = delta[off + u] + mu * (z[off + u] - x[off + u]);
     }
 }
+// column parts of compute_report over a column slice: per-CTA partials (part[f * G + cta]),
+// then k_col_parts_final reduces them in CTA order (deterministic)
 __global__ void k_col_parts(int64_t n, const double* atl, const double* c, const double* x, const double* z,
                             const double* delta, double* part) {
     __shared__ double sh[32];
+    const int G = gridDim.x;
     double d2 = 0.0, dmx = 0.0, s2 = 0.0, smx = 0.0, amx = 0.0, cx = 0.0, cg = 0.0, nf = 0.0;
-    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)G * blockDim.x) {
         const double dual = atl[j] + c[j];
         const double stat = dual - delta[j];
         d2 = d2 + dual * dual;
@@ -1282,7 +1285,15 @@ __global__ void k_col_parts(int64_t n, const double* atl, const double* c, const
     const bool is_sum[8] = {true, false, true, false, false, true, false, false};
     for (int f = 0; f < 8; ++f) {
         const double v = is_sum[f] ? block_reduce(vals[f], sh, SumOp()) : block_reduce(vals[f], sh, MaxOp());
-        if (threadIdx.x == 0) part[f] = v;
+        if (threadIdx.x == 0) part[f * G + blockIdx.x] = v;
+    }
+}
+__global__ void k_col_parts_final(const double* part, int G, double* out) {
+    __shared__ double sh[32];
+    const bool is_sum[8] = {true, false, true, false, false, true, false, false};
+    for (int f = 0; f < 8; ++f) {
+        const double v = is_sum[f] ? reduce_partials(part + f * G, G, sh, SumOp()) : reduce_partials(part + f * G, G, sh, MaxOp());
+        if (threadIdx.x == 0) out[f] = v;
     }
 }
 __global__ void k_row_parts_final(const double* part_row, int G, double* out) {
@@ -1362,9 +1373,14 @@ int launch_col_update_p2p(int64_t n, const double* const* parts, int world, cons
     return CF_OK;
 }
 
+int col_parts_ctas(int64_t n) { return (int)std::min<int64_t>(148 * 8, std::max<int64_t>(1, (n + 2047) / 2048)); }
+
 int launch_col_parts(int64_t n, const double* atl, const double* c, const double* x, const double* z,
-                     const double* delta, double* out8_dev, cudaStream_t st) {
-    k_col_parts<<<1, 1024, 0, st>>>(n, atl, c, x, z, delta, out8_dev);
+                     const double* delta, double* out8_dev, double* work, cudaStream_t st) {
+    const int G = col_parts_ctas(n);
+    k_col_parts<<<G, 256, 0, st>>>(n, atl, c, x, z, delta, work);
+    CF_LAUNCHED();
+    k_col_parts_final<<<1, 1024, 0, st>>>(work, G, out8_dev);
     CF_LAUNCHED();
     return CF_OK;
 }
