@@ -66,6 +66,16 @@ class TripletMatrix:
         return int(self.vals.size)
 
     @classmethod
+    def _view(cls, num_rows, num_cols, rows, cols, vals):
+        """Internal: wrap 1-d arrays of the right dtypes without the copy of __init__ (slices of
+        a problem the caller already handed over, e.g. one rank's share in sharded.py)."""
+        obj = object.__new__(cls)
+        for name, v in (("num_rows", int(num_rows)), ("num_cols", int(num_cols)), ("rows", rows), ("cols", cols),
+                        ("vals", vals)):
+            object.__setattr__(obj, name, v)
+        return obj
+
+    @classmethod
     def from_entries(cls, num_rows, num_cols, entries):
         triples = list(entries)
         return cls(num_rows, num_cols, [t[0] for t in triples], [t[1] for t in triples],
@@ -163,6 +173,14 @@ class ProblemInstance:
     def __post_init__(self):
         object.__setattr__(self, "b", _readonly_1d(self.b, np.float64))
         object.__setattr__(self, "c", _readonly_1d(self.c, np.float64))
+
+    @classmethod
+    def _view(cls, A, b, c, cones):
+        """Internal: no copies (see TripletMatrix._view)."""
+        obj = object.__new__(cls)
+        for name, v in (("A", A), ("b", b), ("c", c), ("cones", cones)):
+            object.__setattr__(obj, name, v)
+        return obj
 
     @property
     def m(self) -> int:

@@ -73,8 +73,10 @@ def local_problem(p, r0: int, r1: int):
     """The rank's rows [r0, r1) renumbered from 0, all columns (cones do not matter to the row block)."""
     rows = np.asarray(p.A.rows, dtype=np.int64)
     sel = (rows >= r0) & (rows < r1)
-    a = TripletMatrix(r1 - r0, p.A.num_cols, rows[sel] - r0, np.asarray(p.A.cols)[sel], np.asarray(p.A.vals)[sel])
-    return ProblemInstance(a, np.asarray(p.b)[r0:r1], np.asarray(p.c), ConeSpec.orthant(p.A.num_cols))
+    a = TripletMatrix._view(r1 - r0, p.A.num_cols, rows[sel] - r0, np.asarray(p.A.cols, dtype=np.int64)[sel],
+                            np.asarray(p.A.vals, dtype=np.float64)[sel])   # fresh arrays already: no second copy
+    return ProblemInstance._view(a, np.ascontiguousarray(np.asarray(p.b, dtype=np.float64)[r0:r1]),
+                                 np.asarray(p.c, dtype=np.float64), ConeSpec.orthant(p.A.num_cols))
 
 
 def assemble_report(k: int, f: list) -> IterationReport:
@@ -697,11 +699,16 @@ def local_columns(p, c0: int, c1: int):
         sel = slice(k0, k1)
     else:
         sel = (cols >= c0) & (cols < c1)
-    a = TripletMatrix(p.A.num_rows, c1 - c0, np.asarray(p.A.rows)[sel], cols[sel] - c0, np.asarray(p.A.vals)[sel])
+    # views where possible (no copy of the caller's 100M-entry arrays: the plan copies them to the GPU)
+    rows = np.ascontiguousarray(np.asarray(p.A.rows, dtype=np.int64)[sel])
+    vals = np.ascontiguousarray(np.asarray(p.A.vals, dtype=np.float64)[sel])
+    lcols = np.ascontiguousarray(cols[sel]) if c0 == 0 else cols[sel] - c0
+    a = TripletMatrix._view(p.A.num_rows, c1 - c0, rows, lcols, vals)
     sizes = cone_sizes_array(p.cones)
     starts = np.concatenate(([0], np.cumsum(sizes)))
     q0, q1 = int(np.searchsorted(starts, c0)), int(np.searchsorted(starts, c1))
-    return ProblemInstance(a, np.asarray(p.b), np.asarray(p.c)[c0:c1], ConeSpec(sizes[q0:q1]))
+    return ProblemInstance._view(a, np.asarray(p.b, dtype=np.float64), np.ascontiguousarray(np.asarray(p.c, dtype=np.float64)[c0:c1]),
+                                 ConeSpec(sizes[q0:q1]))
 
 
 class CudaColBackend:
