@@ -846,6 +846,9 @@ def run_strong(args, spec, rank, world, local_rank, group=None, factories=None, 
         tol = SolverConfig(eps_prim=args.eps, eps_dual=args.eps, eps_gap=args.eps,
                            max_iters=args.e2e_max_iters or 100_000)
         kw = {} if on_gpu else {"backend_factory": factories[mode]}
+        # one untimed warm-up solve, as on the single-GPU line: first-use costs of a fresh
+        # process (lazy kernel-module loading, first touch of the host pages) are not per-solve
+        solve_distributed(problem, SolverConfig(max_iters=25), group=group, mode="auto", **kw)
         dist.barrier(group=group)
         t0 = time.perf_counter()
         eres = solve_distributed(problem, tol, group=group, mode="auto", **kw)
