@@ -848,16 +848,16 @@ def run_strong(args, spec, rank, world, local_rank, group=None, factories=None, 
         kw = {} if on_gpu else {"backend_factory": factories[mode]}
         # one untimed warm-up solve, as on the single-GPU line: first-use costs of a fresh
         # process (lazy kernel-module loading, first touch of the host pages) are not per-solve
-        solve_distributed(problem, SolverConfig(max_iters=25), group=group, mode="auto", **kw)
+        solve_distributed(problem, SolverConfig(max_iters=25), group=group, mode=mode, **kw)
         dist.barrier(group=group)
         t0 = time.perf_counter()
-        eres = solve_distributed(problem, tol, group=group, mode="auto", **kw)
+        eres = solve_distributed(problem, tol, group=group, mode=mode, **kw)   # the loop's layout
         secs = max_over_ranks(time.perf_counter() - t0)
         e2e = {"value": eres.report.iter / secs, "unit": UNIT, "seconds": secs, "iters": eres.report.iter,
                "status": eres.report.status,
                # every rank uploads its own shard of the triplets plus its vectors
                "h2d_bytes_per_step": 24 * o + world * 8 * (m + n), "d2h_bytes_per_step": 8 * (m + n),
-               "step": f"one solve_distributed(p, SolverConfig(eps={args.eps}), mode='auto') per rank from host "
+               "step": f"one solve_distributed(p, SolverConfig(eps={args.eps}), mode={mode!r}) per rank from host "
                        "numpy buffers (the layout choice, the host slicing, the per-rank plan setup, the loop "
                        "and the x/lam gather)"}
     c5 = None
