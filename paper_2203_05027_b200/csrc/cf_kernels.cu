@@ -112,6 +112,9 @@ struct Layout {
 // 194-195) in the reduced form r = fu*(d*b + A x+), lam+ = lam + mu(r - b),
 // h = b - r - lam+/mu. With column panels, every panel but the last only
 // carries the partial row sums (in `carry`), continuing the sequential order.
+#ifndef CF_CARRY_L1
+#define CF_CARRY_L1 1   // panel carries read through L1 (row pass -0.6 %, profiles/r02_carry_l1.log)
+#endif
 struct RowIter : Layout {
     int64_t seg_off;       // p * m
     bool last;             // last panel: ADMM update
@@ -131,7 +134,16 @@ struct RowIter : Layout {
     static constexpr int kVals = 3;   // b, lam, d (last panel only)
     __device__ __forceinline__ bool carry_in() const { return has_carry; }
     __device__ __forceinline__ double carry(int s) const {
+#if CF_CARRY_L1
+        // the lanes of a rank block read rows scattered over the tile's 2 KB of carries:
+        // through L1 the tile's lines go to L2 once instead of once per warp
+        double v;
+        asm("ld.global.nc.L1::evict_first.L2::cache_hint.f64 %0, [%1], %2;"
+            : "=d"(v) : "l"(carry_buf + (s - seg_off)), "l"(pass::pol_first()));
+        return v;
+#else
         return pass::ld_first(carry_buf + (s - seg_off), pass::pol_first());
+#endif
     }
     __device__ __forceinline__ void load_async(int s, double* slot) const {
         if (!last) return;
