@@ -15,16 +15,20 @@
 // equal, so nearly every diagonal is full: 0.10 L1TEX requests per nonzero for
 // idx/val instead of 0.20 with per-block ranking (profiles/r02_probes.md).
 // pl[rank] = local segment | length << 8 | start_w << 17, so each lane knows its
-// segment, its length and its block's offset; the diagonal offsets come from
-// warp ballots.
+// segment, its length and its block's offset. While k is below the block's
+// shortest length every diagonal is 32 wide (constant offsets); the narrower
+// diagonals after it take their offsets from warp ballots.
 //   * lane r owns one segment: it loads idx/val of its nonzeros straight from
 //     global memory (L1 no-allocate, L2 evict-first), gathers g[idx] (kUnroll
 //     independent loads in flight, L2 evict-last) and sums the products
 //     SEQUENTIALLY in canonical order — np.bincount's order (uv.py:10-12),
 //     bit-identical;
-//   * the sums go through shared memory back to natural segment order (one CTA
-//     barrier per tile, double-buffered), so the epilogue runs in natural order:
-//     its vectors are cp.async'ed at tile start and its stores coalesce.
+//   * the sums go through shared memory back to natural segment order, so the
+//     epilogue runs in natural order with coalesced vector loads and stores. The
+//     large passes hand the sums over through mbarriers without a CTA barrier
+//     (the deferred flow, see k_pass) and load the epilogue vectors straight into
+//     registers; the staged small passes and the cone group epilogue use one CTA
+//     barrier per tile and cp.async the vectors at tile start.
 // Measured (profiles/r01_probes.md, r02_probes.md): a random fp64 gather costs one
 // L1TEX->L2 request, ~1 per SM-cycle, and that request port is the bound; TMA
 // staging and TMA gathers were slower; shared memory above ~128 KB per SM starves
