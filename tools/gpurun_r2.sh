@@ -1,3 +1,4 @@
-CF_LIB_PATH=paper_2203_05027_b200/libcfb200_ee1.so timeout 900 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -1
-CF_LIB_PATH=paper_2203_05027_b200/libcfb200_ee2.so timeout 900 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -1
-STEPS=1000 bash tools/lib_sweep.sh base ee1 ee2 base ee1 ee2 base ee1 ee2 2>&1
+for lib in base nc1 nc2 base; do
+  if [ "$lib" = base ]; then path=""; else path="paper_2203_05027_b200/libcfb200_$lib.so"; fi
+  echo -n "$lib: "; CF_LIB_PATH=$path timeout 120 python tools/cluster_one.py 2>&1 | tail -1
+done
