@@ -313,6 +313,9 @@ int cf_column_parts(int64_t n, const double* atl, const double* c, const double*
  * profiling was enabled with cf_plan_set_profiling(plan, 1). */
 int cf_plan_last_timing(const cf_plan* plan, double* loop_ms, int64_t* launches,
                         double* row_pass_ms, double* col_pass_ms, int64_t* timed_iters);
+/* enable = 0: off; 1: events around both passes of every iteration; k > 1: of every k-th
+ * iteration only (the events break the passes' programmatic-launch overlap; last_timing
+ * scales the sampled sums to the whole loop) */
 int cf_plan_set_profiling(cf_plan* plan, int enable);
 /* Synchronise the plan's stream. */
 int cf_plan_sync(cf_plan* plan);

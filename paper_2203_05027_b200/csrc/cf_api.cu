@@ -665,8 +665,11 @@ int cf_plan_last_timing(const cf_plan* p, double* loop_ms, int64_t* launches, do
     CF_TRY(check_plan(p, "cf_plan_last_timing"));
     if (loop_ms) *loop_ms = p->last_loop_ms;
     if (launches) *launches = p->last_launches;
-    if (row_pass_ms) *row_pass_ms = p->prof_row_ms;
-    if (col_pass_ms) *col_pass_ms = p->prof_col_ms;
+    // totals over the loop: the sampled iterations' sums scaled to every timed iteration
+    const double scale = (p->prof_samples > 0 && p->last_timed_iters > 0)
+                             ? (double)p->last_timed_iters / (double)p->prof_samples : 1.0;
+    if (row_pass_ms) *row_pass_ms = p->prof_row_ms * scale;
+    if (col_pass_ms) *col_pass_ms = p->prof_col_ms * scale;
     if (timed_iters) *timed_iters = p->last_timed_iters;
     return CF_OK;
 }
@@ -674,6 +677,7 @@ int cf_plan_last_timing(const cf_plan* p, double* loop_ms, int64_t* launches, do
 int cf_plan_set_profiling(cf_plan* p, int enable) {
     CF_TRY(check_plan(p, "cf_plan_set_profiling"));
     p->profiling = enable != 0;
+    p->prof_stride = enable > 1 ? enable : 1;
     return CF_OK;
 }
 

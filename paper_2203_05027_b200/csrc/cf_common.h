@@ -245,7 +245,9 @@ struct cf_plan {
     int64_t last_launches = 0;
     int64_t last_timed_iters = 0;
     bool profiling = false;
-    double prof_row_ms = 0.0, prof_col_ms = 0.0;
+    int32_t prof_stride = 1;               // events on every prof_stride-th iteration of a loop
+    int64_t prof_iter = 0, prof_samples = 0;
+    double prof_row_ms = 0.0, prof_col_ms = 0.0;   // summed over the sampled iterations
     std::vector<cudaEvent_t> prof_events;  // 3 per profiled iteration: start, after col pass, after row pass
     size_t prof_used = 0;
 };

@@ -200,8 +200,9 @@ class DevicePlan:
         return {"loop_ms": ms.value, "launches": nl.value, "row_pass_ms": rms.value, "col_pass_ms": cms.value,
                 "iters": it.value}
 
-    def set_profiling(self, enable: bool):
-        check(lib().cf_plan_set_profiling(self.handle, 1 if enable else 0))
+    def set_profiling(self, enable, stride: int = 1):
+        """Per-pass CUDA events on every ``stride``-th iteration of the next loops (off: False)."""
+        check(lib().cf_plan_set_profiling(self.handle, max(1, int(stride)) if enable else 0))
 
     # ------------------------------------------------------------------ operators (device pointers)
     def apply_A(self, x_ptr: int, y_ptr: int):
