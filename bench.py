@@ -591,7 +591,11 @@ def run_ours(args, spec, rank, world, local_rank):
             traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": f"k_{dom}", "bytes_per_launch": dbytes, "avg_launch_ms": dms,
-                "peak_source": peak_src}
+                "peak_source": peak_src,
+                # both passes (the two take nearly the same time, so "dominant" flips between runs)
+                "passes": {k: {"bytes_per_launch": b_, "avg_launch_ms": t_,
+                               "frac": (b_ / (t_ / 1000.0) / 1e9) / peak if t_ > 0 else None}
+                           for k, (b_, t_) in passes.items()}}
     iteration_roofline = {"achieved": it_achieved, "frac": it_achieved / peak, "bytes_per_iteration": row_b + col_b,
                           "ms_per_iteration": per_iter_ms, "row_pass_ms": row_ms, "col_pass_ms": col_ms,
                           "report_and_launch_ms": (per_iter_ms - row_ms - col_ms) if profile_in_timed else None,
