@@ -493,8 +493,9 @@ __device__ __forceinline__ void block_sums(P& p, const Jds& L, const int32_t* ib
                 nv[u] = ok ? vb[pos] : 0.0;
             } else {
                 if (ok) CF_DASSERT(pos >= 0 && pos < L.n_idx);
-                nj[u] = ld_first_if(L.idx + pos, pol_first(), ok);
-                nv[u] = ld_first_if(L.val + pos, pol_first(), ok);
+                const uint32_t upos = (uint32_t)pos;   // one IMAD.WIDE.U32 per address
+                nj[u] = ld_first_if(L.idx + upos, pol_first(), ok);
+                nv[u] = ld_first_if(L.val + upos, pol_first(), ok);
             }
             pos += __popc(__ballot_sync(0xffffffffu, ok));   // width of diagonal k+u
         }
