@@ -156,13 +156,13 @@ struct RowIter : Layout {
     __device__ __forceinline__ void load_direct(int s, Vals& v) const {
         if (!last) return;
         const uint64_t pf = pass::pol_first();
-        const int64_t i = s - seg_off;
+        const uint32_t i = (uint32_t)(s - seg_off);   // local row (< m): one IMAD.WIDE.U32 per address
         v.v[0] = pass::ld_first(b + i, pf);
         v.v[1] = pass::ld_first(lam + i, pf);
         v.v[2] = pass::ld_first(dn + i, pf);
     }
     __device__ __forceinline__ void segment(Smem&, int, int s0, int q, int, double axi, const Vals& v) {
-        const int64_t i = s0 + q - seg_off;
+        const uint32_t i = (uint32_t)(s0 + q - seg_off);   // local row (< m)
         if (!last) {
             carry_buf[i] = axi;
             return;
