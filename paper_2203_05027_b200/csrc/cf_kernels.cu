@@ -948,7 +948,9 @@ int launch_iteration(cf_plan* p, const IterOpts& opt, const int32_t* done, int64
     cudaEvent_t e_a = nullptr, e_b = nullptr, e_c = nullptr;
     // per-pass events break the programmatic-launch overlap of the passes they bracket
     // (~11 us per iteration at C2), so a loop can sample every prof_stride-th iteration
-    const bool prof = p->profiling && (p->prof_iter++ % p->prof_stride) == 0;
+    // (the last iteration of each stride: the loop's first iteration, with its launch
+    // latency exposed, is sampled only when every iteration is)
+    const bool prof = p->profiling && (p->prof_iter++ % p->prof_stride) == p->prof_stride - 1;
     if (prof) {
         while (p->prof_events.size() < p->prof_used + 3) {
             cudaEvent_t e;
